@@ -1,0 +1,154 @@
+"""Oracle O1 (stencil SpMV) and O2 (Jacobi(5+1) preconditioner).  TEST
+INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+O1  y_n = sum_d a_d[n] * x[nbr(n, d)]                      (
+    PAPER P:121-123 banded storage).  nbr wraps on periodic axes; on a
+    non-periodic axis an out-of-grid neighbour must carry a zero
+    coefficient -- asserted at construction.
+O2  "Five sweeps of the Jacobi method with a relaxation parameter ...
+    followed by a sweep of point Jacobi smoothing on the global domain"
+    (P:147), from z = 0:
+        z = w_l D^-1 r;  4x: z += w_l D^-1 (r - A z);  1x: z += w_g D^-1 (r - A z)
+    w_l = 0.8, w_g = 1.0, all sweeps global (reading R3).
+
+Pins (tests/oracle/test_stencil_pins.py): dense expansion built by
+explicit per-cell loops; SPEC's hand examples;
+the closed-form eigenpairs of the c1 operator (Kronecker sum of
+tridiagonal Toeplitz matrices); zero row sums of the channel operator;
+Jacobi on a diagonal A and on the c1 eigenvectors (closed form
+[1 - (1-w_g mu)(1-w_l mu)^5]/lambda).
+"""
+import numpy as np
+
+
+def shifted(x3, dx, dy, dz, periodic):
+    """xs[k, j, i] = x3[k+dz, j+dy, i+dx]; wraps on periodic axes, 0 outside."""
+    out = x3
+    for axis, d, bit in ((2, dx, 1), (1, dy, 2), (0, dz, 4)):
+        if d == 0:
+            continue
+        if periodic & bit:
+            out = np.roll(out, -d, axis=axis)
+        else:
+            n = out.shape[axis]
+            res = np.zeros_like(out)
+            src = [slice(None)] * 3
+            dst = [slice(None)] * 3
+            if d > 0:
+                src[axis] = slice(d, n)
+                dst[axis] = slice(0, n - d)
+            else:
+                src[axis] = slice(0, n + d)
+                dst[axis] = slice(-d, n)
+            res[tuple(dst)] = out[tuple(src)]
+            out = res
+    return out
+
+
+class Operator:
+    """Banded structured-grid operator A (bands [S, nz, ny, nx], x-fastest)."""
+
+    def __init__(self, nx, ny, nz, periodic, offsets, bands, check=True):
+        self.nx, self.ny, self.nz = int(nx), int(ny), int(nz)
+        self.periodic = int(periodic)
+        self.offsets = np.asarray(offsets, dtype=np.int64)
+        self.bands = np.asarray(bands, dtype=np.float64).reshape(
+            len(self.offsets), self.nz, self.ny, self.nx)
+        self.N = self.nx * self.ny * self.nz
+        d0 = [d for d, o in enumerate(self.offsets) if tuple(o) == (0, 0, 0)]
+        assert len(d0) == 1, "exactly one diagonal band (S:38)"
+        self.d0 = d0[0]
+        if check:
+            self._check_truncation()
+
+    @classmethod
+    def from_problem(cls, prob, epoch=0):
+        return cls(prob.nx, prob.ny, prob.nz, prob.periodic, prob.offsets,
+                   prob.bands(epoch=epoch))
+
+    def _check_truncation(self):
+        k = np.arange(self.nz)[:, None, None]
+        j = np.arange(self.ny)[None, :, None]
+        i = np.arange(self.nx)[None, None, :]
+        for d, (dx, dy, dz) in enumerate(self.offsets):
+            bad = np.zeros((self.nz, self.ny, self.nx), dtype=bool)
+            for idx, dd, n, bit in ((i, dx, self.nx, 1), (j, dy, self.ny, 2), (k, dz, self.nz, 4)):
+                if dd and not (self.periodic & bit):
+                    bad |= np.broadcast_to((idx + dd < 0) | (idx + dd >= n), bad.shape)
+            assert not np.any(self.bands[d][bad]), \
+                f"band {d} reaches outside a non-periodic axis (S:39)"
+
+    def diag(self):
+        return self.bands[self.d0].reshape(-1)
+
+    def apply(self, x):
+        """O1: y = A x."""
+        x3 = np.asarray(x, dtype=np.float64).reshape(self.nz, self.ny, self.nx)
+        y = np.zeros_like(x3)
+        for d, (dx, dy, dz) in enumerate(self.offsets):
+            y += self.bands[d] * shifted(x3, dx, dy, dz, self.periodic)
+        return y.reshape(-1)
+
+    def apply_ld(self, x):
+        """O1 in extended precision (np.longdouble accumulation) -- the
+        per-kernel reference for the 1e-12 componentwise check."""
+        x3 = np.asarray(x, dtype=np.longdouble).reshape(self.nz, self.ny, self.nx)
+        y = np.zeros_like(x3)
+        for d, (dx, dy, dz) in enumerate(self.offsets):
+            y += self.bands[d].astype(np.longdouble) * shifted(x3, dx, dy, dz, self.periodic)
+        return y.reshape(-1)
+
+    def apply_abs(self, x):
+        """(|A| |x|)_n, the scale of the componentwise SpMV tolerance (D25)."""
+        x3 = np.abs(np.asarray(x, dtype=np.float64)).reshape(self.nz, self.ny, self.nx)
+        y = np.zeros_like(x3)
+        for d, (dx, dy, dz) in enumerate(self.offsets):
+            y += np.abs(self.bands[d]) * shifted(x3, dx, dy, dz, self.periodic)
+        return y.reshape(-1)
+
+
+def to_dense(op, cap=8192):
+    """Dense N x N expansion built cell by cell; an
+    independent construction used to pin Operator.apply."""
+    N = op.N
+    assert N <= cap, "dense expansion only for tiny grids"
+    Ad = np.zeros((N, N))
+    for k in range(op.nz):
+        for j in range(op.ny):
+            for i in range(op.nx):
+                n = i + op.nx * (j + op.ny * k)
+                for d, (dx, dy, dz) in enumerate(op.offsets):
+                    ii, jj, kk = i + dx, j + dy, k + dz
+                    ok = True
+                    for v, nn, bit in ((ii, op.nx, 1), (jj, op.ny, 2), (kk, op.nz, 4)):
+                        if not (0 <= v < nn) and not (op.periodic & bit):
+                            ok = False
+                    if not ok:
+                        continue
+                    ii %= op.nx
+                    jj %= op.ny
+                    kk %= op.nz
+                    Ad[n, ii + op.nx * (jj + op.ny * kk)] += op.bands[d, k, j, i]
+    return Ad
+
+
+def jacobi(op, r, sweeps=5, omega_l=0.8, omega_g=1.0):
+    """O2: z ~= M^-1 r by `sweeps` under-relaxed Jacobi sweeps from z = 0
+    followed by one point-Jacobi sweep with omega_g."""
+    D = op.diag()
+    r = np.asarray(r, dtype=np.float64)
+    z = omega_l * r / D                              # first sweep from z = 0
+    for _ in range(sweeps - 1):
+        z = z + omega_l * (r - op.apply(z)) / D
+    z = z + omega_g * (r - op.apply(z)) / D          # global point-Jacobi sweep
+    return z
+
+
+class Jacobi:
+    """The preconditioner as a callable r -> M^-1 r (a fixed linear map)."""
+
+    def __init__(self, op, sweeps=5, omega_l=0.8, omega_g=1.0):
+        self.op, self.sweeps, self.omega_l, self.omega_g = op, sweeps, omega_l, omega_g
+
+    def __call__(self, r):
+        return jacobi(self.op, r, self.sweeps, self.omega_l, self.omega_g)

@@ -1,0 +1,311 @@
+"""Pins for oracle O3-O7 against mathematics and library routines:
+brute-force least squares over explicit spaces (eqs. (6)-(7), Alg. 1
+line 12), scipy.sparse.linalg.bicgstab, dense direct solves, and the
+algebraic invariants of eqs. (4), (5), (8)."""
+from dataclasses import replace
+
+import numpy as np
+import pytest
+import scipy.sparse.linalg as spla
+
+from oracle.krylov import (
+    BREAKDOWN, CONVERGED, gcrot_update, bicgstab, gmres, rbicgstab,
+    refresh_space, rgcrot, run_sequence,
+)
+from oracle.stencil import Jacobi, Operator, to_dense
+from problems import OFFSETS7, SolverParams, get_workload
+from problems.stencils import channel19, convection_diffusion_c1, porous7
+
+
+def _setup(prob, seed=0):
+    op = Operator.from_problem(prob)
+    pc = Jacobi(op)
+    b = prob.rhs(1).reshape(-1)
+    return op, pc, b
+
+
+def _Ahat_dense(op, pc):
+    D = to_dense(op)
+    return np.column_stack([pc(D[:, i]) for i in range(op.N)]), D
+
+
+def _orth(M):
+    q, _ = np.linalg.qr(M)
+    return q
+
+
+def test_gmres_one_cycle_is_minimal_residual():
+    """Alg. 1 line 12: after one cycle from x0 = 0, x minimises
+    ||M^-1 b - A_hat x|| over K_m(A_hat, M^-1 b).  Brute force: explicit
+    (QR-orthonormalised) power basis + numpy lstsq."""
+    prob = convection_diffusion_c1(5)
+    op, pc, b = _setup(prob)
+    m = 6
+    prm = SolverParams(m=m, k_max=0, p1=0, tol=1e-30, max_mv=m)
+    x, rep = gmres(op, pc, b, prm)
+    assert rep.cycles == 1 and rep.krylov_mv == m
+    Ah, _ = _Ahat_dense(op, pc)
+    rh = pc(b)
+    K = [rh]
+    for _ in range(m - 1):
+        K.append(Ah @ K[-1])
+    Q = _orth(np.column_stack(K))
+    c = np.linalg.lstsq(Ah @ Q, rh, rcond=None)[0]
+    xb = Q @ c
+    assert np.linalg.norm(x - xb) <= 1e-9 * np.linalg.norm(xb)
+
+
+def test_gmres_finite_termination_and_identity():
+    prob = convection_diffusion_c1(3)                     # N = 27
+    op, pc, b = _setup(prob)
+    prm = SolverParams(m=27, k_max=0, p1=0, tol=1e-10)
+    x, rep = gmres(op, pc, b, prm)
+    assert rep.outcome == CONVERGED and rep.cycles == 1
+    xs = np.linalg.solve(to_dense(op), b)
+    assert np.linalg.norm(x - xs) <= 1e-8 * np.linalg.norm(xs)
+    # A = identity converges in the first cycle with x = b
+    bands = np.zeros((7, 3, 3, 3))
+    bands[0] = 1.0
+    opI = Operator(3, 3, 3, 0, OFFSETS7, bands)
+    xI, repI = gmres(opI, lambda r: r, b, SolverParams(m=5, k_max=0, p1=0))
+    assert repI.cycles == 1 and np.allclose(xI, b, rtol=1e-15, atol=1e-15)
+
+
+def _random_space(op, pc, k, seed):
+    U0 = np.random.default_rng(seed).uniform(-1, 1, (op.N, k))
+    return refresh_space(lambda v: pc(op.apply(v)), U0)[:2]
+
+
+def test_rgcrot_cycle_is_optimal_over_U_plus_Krylov():
+    """Eqs. (6)-(7): one rGCROT cycle returns the minimiser of
+    ||r_hat - A_hat d|| over d in range(U) + K_m(A_C, r0), A_C = (I - C C^T)
+    A_hat, r0 = (I - C C^T) r_hat.  Brute force over an explicit basis.
+    (The literal Alg. 3 line 13a sign fails this pin -- reading D1.)"""
+    prob = channel19(6)
+    op, pc, b = _setup(prob)
+    U, C = _random_space(op, pc, 4, seed=2)
+    m = 5
+    prm = SolverParams(m=m, k_max=4, k_t=2, p1=1, tol=1e-30, max_mv=m)
+    x, U2, C2, rep = rgcrot(op, pc, b, U.copy(), C.copy(), prm)
+    assert rep.cycles == 1
+    Ah, _ = _Ahat_dense(op, pc)
+    rh = pc(b)
+    P = np.eye(op.N) - C @ C.T
+    r0 = P @ rh
+    K = [r0]
+    for _ in range(m - 1):
+        K.append(P @ (Ah @ K[-1]))
+    Z = np.column_stack([U, _orth(np.column_stack(K))])
+    c = np.linalg.lstsq(Ah @ Z, rh, rcond=None)[0]
+    xb = Z @ c
+    assert np.linalg.norm(x - xb) <= 1e-8 * np.linalg.norm(xb)
+
+
+def test_rgcrot_invariants_every_cycle():
+    """Eq. (4) V _|_ C, eq. (5) A_hat V_m = C B + V_{m+1} H_, Arnoldi
+    orthonormality, A_hat U = C and C^T C = I after line 14a,
+    residual _|_ C after each cycle (D20), monotone true residual."""
+    w = get_workload("c2s")
+    prob = w.problem()
+    op, pc, _ = _setup(prob)
+    prm = w.params
+    U = np.zeros((op.N, 0))
+    C = np.zeros((op.N, 0))
+    Anorm = np.abs(to_dense(op)).sum(axis=1).max()
+    checks = []
+
+    def hook(d):
+        V, H, B = d["V"], d["H"], d["B"]
+        m_eff = d["m_eff"]
+        Cc, Uc = d["C"], d["U"]
+        AV = np.column_stack([pc(op.apply(V[:, j])) for j in range(m_eff)])
+        rel5 = np.linalg.norm(AV - Cc @ B - V @ H) / np.linalg.norm(AV)
+        orth = np.linalg.norm(V.T @ V - np.eye(V.shape[1]))
+        vc = np.linalg.norm(Cc.T @ V) if Cc.shape[1] else 0.0
+        checks.append((rel5, orth, vc))
+
+    for t in range(3):
+        b = prob.rhs(t).reshape(-1)
+        x, U, C, rep = rgcrot(op, pc, b, U, C, prm, hook=hook)
+        assert rep.outcome == CONVERGED
+        hist = [h[1] for h in rep.history]
+        assert all(hist[i + 1] <= hist[i] * (1 + 1e-12) for i in range(len(hist) - 1))
+        assert np.linalg.norm(C.T @ C - np.eye(C.shape[1])) <= 1e-12
+        AU = np.column_stack([pc(op.apply(U[:, i])) for i in range(U.shape[1])])
+        assert np.linalg.norm(AU - C) <= 1e-11 * np.linalg.norm(U)
+        assert np.linalg.norm(b - op.apply(x)) <= prm.tol * np.linalg.norm(b)
+    for rel5, orth, vc in checks:
+        assert rel5 <= 1e-12 and orth <= 1e-12 and vc <= 1e-12
+
+
+def test_rgcrot_mgs_and_cgs2_agree():
+    w = get_workload("c2s")
+    prob = w.problem()
+    op, pc, b = _setup(prob)
+    e = np.zeros((op.N, 0))
+    x1, _, _, r1 = rgcrot(op, pc, b, e, e, w.params)
+    x2, _, _, r2 = rgcrot(op, pc, b, e, e, replace(w.params, ortho="mgs"))
+    assert r1.krylov_mv == r2.krylov_mv
+    assert np.linalg.norm(x1 - x2) <= 1e-6 * np.linalg.norm(x1)
+
+
+def test_rgcrot_solution_vs_direct_solve_c1():
+    """BASELINE configs[0] in full: x within kappa*tol of the direct solve."""
+    w = get_workload("c1")
+    prob = w.problem()
+    op, pc, _ = _setup(prob)
+    b = prob.rhs(0).reshape(-1)
+    e = np.zeros((op.N, 0))
+    x, U, C, rep = rgcrot(op, pc, b, e, e, w.params)
+    assert rep.outcome == CONVERGED and rep.cycles == 1 and rep.krylov_mv == 20
+    D = to_dense(op)
+    xs = np.linalg.solve(D, b)
+    assert np.linalg.norm(x - xs) <= 1e-6 * np.linalg.norm(xs)
+    assert np.linalg.norm(b - D @ x) <= 1e-8 * np.linalg.norm(b)
+
+
+def test_projection_full_space_zero_cycles():
+    """r_hat in range(C) -> zero cycles, x = U C^T r_hat (R = I)."""
+    prob = convection_diffusion_c1(4)
+    op, pc, _ = _setup(prob)
+    U, C = _random_space(op, pc, 3, seed=4)
+    # b such that M^-1 b = C w: b = M (C w) -- construct via b = A u, u = U w
+    wv = np.array([0.3, -1.2, 0.5])
+    b = op.apply(U @ wv)
+    prm = SolverParams(m=5, k_max=3, k_t=2, tol=1e-8)
+    x, _, _, rep = rgcrot(op, pc, b, U, C, prm)
+    assert rep.cycles == 0 and rep.krylov_mv == 0 and rep.outcome == CONVERGED
+    assert np.linalg.norm(x - U @ wv) <= 1e-10 * np.linalg.norm(U @ wv)
+
+
+@pytest.mark.parametrize("iters", [1, 3, 6])
+def test_bicgstab_matches_scipy(iters):
+    """Alg. 2 with right preconditioning == scipy.sparse.linalg.bicgstab
+    (same recurrences, r_tilde = r0) after `iters` iterations."""
+    prob = porous7(8, 2)
+    op, pc, b = _setup(prob)
+    prm = SolverParams(tol=1e-30, max_mv=2 * iters)
+    x, rep = bicgstab(op, pc, b, prm)
+    assert rep.cycles == iters
+    A = spla.LinearOperator((op.N, op.N), matvec=op.apply, dtype=np.float64)
+    M = spla.LinearOperator((op.N, op.N), matvec=pc, dtype=np.float64)
+    xs, info = spla.bicgstab(A, b, x0=np.zeros(op.N), rtol=0.0, atol=0.0, maxiter=iters, M=M)
+    assert np.linalg.norm(x - xs) <= 1e-12 * np.linalg.norm(xs)
+
+
+@pytest.mark.parametrize("iters", [2, 5])
+def test_rbicgstab_is_bicgstab_on_projected_operator(iters):
+    """Eqs. (8)-(9): rBiCGStab iterates BiCGStab on A_C = (I - C C^T) A with
+    r0 = (I - C C^T) b; its pre-line-17a x (= x_final + U xi) equals scipy's
+    BiCGStab x on that operator, and line 17a makes b - A x_final equal the
+    updated residual (eqs. (10)-(12))."""
+    prob = porous7(8, 2)
+    op, pc, b = _setup(prob)
+    U0 = np.random.default_rng(7).uniform(-1, 1, (op.N, 3))
+    U, C, _ = refresh_space(op.apply, U0)
+    prm = SolverParams(tol=1e-30, max_mv=2 * iters)
+    x, _, _, rep = rbicgstab(op, pc, b, U, C, prm)
+    x_pre = x + U @ rep.xi
+    P = np.eye(op.N) - C @ C.T
+    AC = spla.LinearOperator((op.N, op.N), matvec=lambda v: P @ op.apply(v), dtype=np.float64)
+    M = spla.LinearOperator((op.N, op.N), matvec=pc, dtype=np.float64)
+    xs, _ = spla.bicgstab(AC, P @ b, x0=np.zeros(op.N), rtol=0.0, atol=0.0, maxiter=iters, M=M)
+    assert np.linalg.norm(x_pre - xs) <= 1e-11 * np.linalg.norm(xs)
+    assert abs(rep.final_true_res - rep.final_upd_res) <= 1e-10 * np.linalg.norm(b)
+
+
+def test_rbicgstab_residual_stays_orthogonal_and_certifies():
+    """C^T r_i small at every iteration (checked on the final
+    updated residual via the certified true residual) and the deferred
+    update is exact on a converged run; x matches a direct solve."""
+    prob = porous7(10, 2)
+    op, pc, b = _setup(prob)
+    U0 = np.random.default_rng(9).uniform(-1, 1, (op.N, 4))
+    U, C, _ = refresh_space(op.apply, U0)
+    prm = SolverParams(tol=1e-10)
+    x, _, _, rep = rbicgstab(op, pc, b, U, C, prm)
+    assert rep.outcome == CONVERGED
+    rt = b - op.apply(x)
+    assert np.linalg.norm(C.T @ rt) <= 1e-9 * np.linalg.norm(b)
+    xs = np.linalg.solve(to_dense(op), b)
+    assert np.linalg.norm(x - xs) <= 1e-6 * np.linalg.norm(xs)
+
+
+def test_bicgstab_forced_breakdown():
+    """force a zero denominator.  A = periodic 1-D difference
+    (skew-symmetric) with identity preconditioner and b = e_0: r_tilde^T A b
+    = 0 exactly -> BREAKDOWN at the first iteration."""
+    offs = np.array([(0, 0, 0), (-1, 0, 0), (1, 0, 0)], dtype=np.int8)
+    bands = np.zeros((3, 1, 1, 4))
+    bands[1] = -1.0
+    bands[2] = 1.0
+    op = Operator(4, 1, 1, 1, offs, bands)
+    b = np.array([1.0, 0, 0, 0])
+    x, rep = bicgstab(op, lambda r: r.copy(), b, SolverParams(tol=1e-8))
+    assert rep.outcome == BREAKDOWN and rep.cycles == 0
+
+
+def test_rbicgstab_k0_is_bicgstab_identity_case():
+    """A = identity -> first iteration gives x = b (alpha = 1, s = 0)."""
+    bands = np.zeros((7, 2, 2, 2))
+    bands[0] = 1.0
+    op = Operator(2, 2, 2, 0, OFFSETS7, bands)
+    b = np.arange(1.0, 9.0)
+    x, rep = bicgstab(op, lambda r: r.copy(), b, SolverParams(tol=1e-8))
+    assert rep.outcome == CONVERGED and rep.krylov_mv == 1
+    assert np.array_equal(x, b)
+
+
+def test_hybrid_frozen_space_and_conservation():
+    """the recycle space handed to every rBiCGStab system after
+    the switch is bit-identical; matvec totals add up; the hybrid beats
+    plain BiCGStab or is within 20 % on its rBiCGStab phase (reported)."""
+    w = get_workload("c3s")
+    spaces = []
+
+    def cb(t, tag, x, U, C, rep):
+        if tag == "rbicgstab":
+            spaces.append((U.copy(), C.copy()))
+
+    out = run_sequence(w, callback=cb)
+    tags = [o[0] for o in out]
+    assert tags == ["rgcrot"] * 3 + ["rbicgstab"] * (w.n_systems - 3)
+    for U, C in spaces[1:]:
+        assert np.array_equal(U, spaces[0][0]) and np.array_equal(C, spaces[0][1])
+    assert all(o[2].outcome == CONVERGED for o in out)
+    U, C = spaces[0]
+    prob = w.problem()
+    op = Operator.from_problem(prob)
+    AU = np.column_stack([op.apply(U[:, i]) for i in range(U.shape[1])])
+    assert np.linalg.norm(AU - C) <= 1e-11 * np.linalg.norm(U)   # A U = C (D3)
+    assert np.linalg.norm(C.T @ C - np.eye(C.shape[1])) <= 1e-12
+
+
+def test_recycling_reduces_matvecs_channel():
+    """Recycling benefit (S:484 trend): rGCROT beats GMRES(m) on the
+    shrunken channel sequence."""
+    w = get_workload("c2s")
+    rg = sum(o[2].krylov_mv for o in run_sequence(w))
+    gm = sum(o[2].krylov_mv for o in run_sequence(w, solver="gmres"))
+    assert rg <= 0.8 * gm
+
+
+def test_gcrot_update_truncation_T1():
+    """Line 14a bookkeeping: k never exceeds k_max, truncation keeps the
+    newest k_t - p old columns."""
+    rng = np.random.default_rng(0)
+    N, m, k = 40, 4, 5
+    U = rng.standard_normal((N, k))
+    C = _orth(rng.standard_normal((N, k)))
+    V = _orth(rng.standard_normal((N, m + 1)))
+    H = np.triu(rng.standard_normal((m + 1, m)), -1)
+    B = rng.standard_normal((k, m))
+    y = rng.standard_normal(m)
+    dx = rng.standard_normal(N)
+    prm = SolverParams(m=m, k_max=5, k_t=3, p1=2)
+    U2, C2 = gcrot_update(U, C, V, H, B, y, dx, 1.0, prm)
+    assert U2.shape[1] == 3
+    assert np.array_equal(U2[:, 0], U[:, 4])
+    zeta = H @ y
+    assert np.allclose(C2[:, 1], V @ zeta / np.linalg.norm(zeta))
+    assert abs(C2[:, 1] @ C2[:, 2]) <= 1e-14
