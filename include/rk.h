@@ -1,0 +1,190 @@
+/*
+ * rk.h -- C-ABI of librk, the B200 (sm_100a) hot path of the recycling
+ * Krylov solvers of arXiv:1501.03358 (Amritkar, de Sturler, Swirydowicz,
+ * Tafti, Ahuja): rGCROT(m,k) (Alg. 3), rBiCGStab with
+ * one recycle space (Alg. 4), their k = 0 special cases GMRES(m)
+ * (Alg. 1) and BiCGStab (Alg. 2), and the hybrid
+ * rGCROT -> rBiCGStab sequence strategy.
+ *
+ * Conventions (apply to every entry point unless stated otherwise)
+ *  - Vectors are fp64, the caller's LOCAL z-slab of the grid in x-fastest
+ *    order n = i + nx*(j + ny*k), nz_local planes, no ghosts.
+ *    "device" pointers are CUDA device memory on the context's device;
+ *    "host" pointers are ordinary host memory.
+ *  - Ownership: the caller owns every pointer it passes.  librk copies
+ *    bands and recycle spaces into memory it owns; export copies out.
+ *  - Streams: all work is enqueued on the context stream.  Functions that
+ *    return results (rk_solve*, rk_op_apply, rk_precond_apply, exports)
+ *    return after that stream has synchronised.
+ *  - Errors: API/runtime failures return an rk_status != RK_OK and set a
+ *    thread-local message readable with rk_last_error().  No C++ exception
+ *    crosses the ABI.  Numerical outcomes (breakdown, no convergence,
+ *    instability) are NOT errors: they are rk_report.outcome.
+ *  - Threading: one context per host thread and stream.
+ *  - Multi-GPU: one process per GPU; every rank calls every function
+ *    collectively with identical arguments except the slab data.
+ */
+#ifndef RK_H
+#define RK_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct rk_ctx rk_ctx;
+typedef struct rk_op rk_op;
+typedef struct rk_solver rk_solver;
+
+typedef enum {
+  RK_OK = 0,
+  RK_EINVAL = 1,       /* bad argument (sizes, offsets, truncation violated, NULL) */
+  RK_ECUDA = 2,        /* CUDA runtime error */
+  RK_ENCCL = 3,        /* NCCL error */
+  RK_ENOMEM = 4,       /* device allocation failed */
+  RK_ESTATE = 5,       /* call not valid in the object's current state */
+  RK_EUNSUPPORTED = 6  /* option not implemented */
+} rk_status;
+
+/* Solve outcome (SURVEY.md §5 failure detection). */
+typedef enum {
+  RK_CONVERGED = 0,    /* ||b - A x||_2 <= tol ||b||_2 (true residual)            */
+  RK_MAX_MATVECS = 1,  /* Krylov matvec budget exhausted                           */
+  RK_BREAKDOWN = 2,    /* rho, sigma, tau or omega exactly 0 (Alg. 2/4 line 5)     */
+  RK_STAGNATION = 3,   /* reserved                                                 */
+  RK_UNSTABLE = 4,     /* ||r_i|| > divergence_factor ||r_0|| ("unstable") */
+  RK_DRIFT = 5         /* rBiCGStab updated residual converged, certified did not  */
+} rk_outcome;
+
+/* GMRES == rGCROT with k_max = 0; BICGSTAB == rBiCGStab with k = 0. */
+typedef enum { RK_GMRES = 0, RK_RGCROT = 1, RK_BICGSTAB = 2, RK_RBICGSTAB = 3 } rk_method;
+
+/* Grid of the operator.  Global nx x ny x nz_global; this rank owns planes
+ * [z0, z0 + nz_local).  periodic_mask: bit0 x, bit1 y, bit2 z. */
+typedef struct {
+  int64_t nx, ny, nz_global, z0, nz_local;
+  uint32_t periodic_mask;
+} rk_grid;
+
+/* Jacobi(5+1) preconditioner: z = w_l D^-1 r; (sweeps-1) x
+ * z += w_l D^-1 (r - A z); then z += w_g D^-1 (r - A z).  kind 0 = none. */
+typedef struct {
+  int kind;            /* 0 none, 1 jacobi                          */
+  int sweeps;          /* local relaxed sweeps (paper: 5)           */
+  double omega_local;  /* 0.8 (reading D9)                          */
+  double omega_global; /* 1.0 (reading D9)                          */
+} rk_precond;
+
+typedef struct {
+  rk_method method;
+  int m;               /* inner cycle length (rGCROT/GMRES)                 */
+  int k_max;           /* max recycle dimension                             */
+  int k_keep;          /* k_t: dimension after truncation       */
+  int select_count;    /* p1: candidates added per cycle, 0..2  */
+  int ortho;           /* 0 = CGS2 (block classical Gram-Schmidt, twice)    */
+  int trunc;           /* 0 = T1 (drop oldest)                              */
+  rk_precond pc;
+  double tol;          /* default tolerance (rk_solve's tol overrides)      */
+  int64_t max_matvecs; /* Krylov matvec budget per solve (paper: 2000)      */
+  double divergence_factor; /* UNSTABLE threshold (1e4)         */
+} rk_config;
+
+typedef struct {
+  int32_t outcome;               /* rk_outcome                                   */
+  int32_t k_after;               /* recycle dimension after the solve            */
+  int64_t krylov_matvecs;        /* preconditioned operator applications in the Krylov loop */
+  int64_t operator_applications; /* other applications of A: true residuals, refresh, certification */
+  int64_t cycles_or_iters;       /* rGCROT cycles or rBiCGStab iterations        */
+  double bnorm;                  /* ||b||_2                                      */
+  double final_true_res;         /* ||b - A x||_2 at exit                        */
+  double final_updated_res;      /* preconditioned LS residual (rGCROT) / updated ||r|| (rBiCGStab) */
+  double seconds;                /* host wall time of the solve                  */
+  int64_t history_len;
+} rk_report;
+
+/* Thread-local message describing the last non-OK status. */
+const char* rk_last_error(void);
+
+/* Library build/version string. */
+const char* rk_version(void);
+
+/* NCCL unique id for multi-GPU bootstrap (rank 0 calls it and broadcasts
+ * the 128 bytes through torch.distributed).  RK_EUNSUPPORTED if librk was
+ * built without NCCL. */
+rk_status rk_nccl_unique_id(uint8_t out[128]);
+
+/* Create a context on CUDA device `device`.  cuda_stream: a cudaStream_t
+ * (e.g. torch.cuda.current_stream().cuda_stream) or NULL for a library-
+ * owned non-blocking stream.  uid must be NULL iff nranks == 1. */
+rk_status rk_ctx_create(int device, int rank, int nranks, const uint8_t* uid,
+                        void* cuda_stream, rk_ctx** out);
+void rk_ctx_destroy(rk_ctx* ctx);
+
+/* Create a grid operator A in banded storage.
+ * offsets: nbands x 3 int8 (dx, dy, dz), each in {-1, 0, 1}, exactly one
+ * (0,0,0) (the diagonal, nonzero everywhere).  bands: DEVICE pointer,
+ * [nbands][nz_local][ny][nx] fp64, band d multiplies x at offset d.
+ * A coefficient reaching outside a non-periodic axis must be exactly 0
+ * (SPEC S:39): checked on the device, RK_EINVAL otherwise.  librk copies the
+ * bands (reordered into its canonical 7-, 19- or 27-point layout). */
+rk_status rk_op_create(rk_ctx* ctx, const rk_grid* grid, int nbands,
+                       const int8_t* offsets, const double* bands, rk_op** out);
+/* New matrix epoch (same offsets): copies new bands, invalidates every
+ * solver's C (it is rebuilt by QR of A U on the next solve, Alg. 3 l.1a). */
+rk_status rk_op_update_bands(rk_op* op, const double* bands);
+void rk_op_destroy(rk_op* op);
+
+/* y = A x (O1 / kernel K1).  DEVICE pointers, no ghosts. */
+rk_status rk_op_apply(rk_op* op, const double* x, double* y);
+/* z = M^-1 r (O2 / kernel K2 chain).  DEVICE pointers. */
+rk_status rk_precond_apply(rk_op* op, const rk_precond* pc, const double* r, double* z);
+
+/* Solver bound to an operator.  Allocates the workspace for (m, k_max). */
+rk_status rk_solver_create(rk_op* op, const rk_config* cfg, rk_solver** out);
+void rk_solver_destroy(rk_solver* s);
+/* Hybrid switch: keeps U, invalidates C (reading D3). */
+rk_status rk_solver_set_method(rk_solver* s, rk_method method);
+/* Recycle space.  U (and optionally C) are DEVICE pointers to k
+ * column-major local columns with leading dimension ld >= N_local.  C == NULL
+ * -> QR refresh C R = op(U) on the next solve, op = M^-1 A for rGCROT and A
+ * for rBiCGStab (reading D3).  R is a HOST k x k column-major upper
+ * triangular matrix or NULL (= I); it is absorbed into U (U <- U R^-1,
+ * reading D14).  A given C must satisfy op(U) = C R for the solver's current
+ * method.  k = 0 empties the space.  k <= k_max. */
+rk_status rk_recycle_set(rk_solver* s, int k, const double* U, const double* C,
+                         const double* R, int64_t ld);
+rk_status rk_recycle_dim(rk_solver* s, int* k);
+/* Copies U, C (DEVICE, ld) and R (HOST k x k, always I after absorption). */
+rk_status rk_recycle_export(rk_solver* s, double* U, double* C, double* R, int64_t ld);
+
+/* Solve A x = b (rGCROT/GMRES: Alg. 3/1 left-preconditioned; rBiCGStab/
+ * BiCGStab: Alg. 4/2 right-preconditioned).  b, x DEVICE; x holds x0 on
+ * entry (the paper always uses x0 = 0) and the solution on exit.
+ * tol <= 0 uses cfg.tol.  rep may be NULL. */
+rk_status rk_solve(rk_solver* s, const double* b, double* x, double tol, rk_report* rep);
+/* Same with HOST b and x: the host<->device copies are part of the call. */
+rk_status rk_solve_host(rk_solver* s, const double* b_host, double* x_host, double tol,
+                        rk_report* rep);
+/* Residual history of the last solve: rows (krylov_matvecs, ||b-Ax|| or NaN,
+ * preconditioned / updated ||r||).  out is HOST [cap][3]. */
+rk_status rk_history(rk_solver* s, double* out, int64_t cap, int64_t* len);
+/* Workspace audit: number of N_local-length vectors allocated. */
+rk_status rk_solver_workspace(rk_solver* s, int64_t* nvec);
+
+/* Instrumentation.  Every kernel launch increments a per-context counter.
+ * With profiling on, launches of the kernel classes whose names contain
+ * `filter` (NULL = all) are bracketed by CUDA events on the context stream;
+ * rk_profile_read returns, per class, launches, summed device ms and summed
+ * algorithmic bytes. */
+rk_status rk_launch_count(rk_ctx* ctx, int64_t* count);
+rk_status rk_profile_enable(rk_ctx* ctx, int on, const char* filter);
+/* names: HOST buffer of cap x 32 chars; launches, ms, bytes: HOST [cap]. */
+rk_status rk_profile_read(rk_ctx* ctx, int cap, char* names, int64_t* launches,
+                          double* ms, double* bytes, int* n);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RK_H */

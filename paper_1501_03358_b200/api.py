@@ -1,0 +1,244 @@
+"""Thin Python binding of librk (include/rk.h).
+
+PyTorch is used only for device memory, streams and process groups: every
+numeric step of the solvers runs in librk's sm_100a kernels behind the
+C-ABI.  The objects mirror the ABI one to one:
+
+  Context       rk_ctx_create / rk_launch_count / rk_profile_*
+  GridOperator  rk_op_create / rk_op_apply / rk_precond_apply / rk_op_update_bands
+  Solver        rk_solver_create / rk_solve / rk_solve_host / rk_solver_set_method /
+                rk_recycle_set / rk_recycle_dim / rk_recycle_export / rk_history
+  solve_sequence  the hybrid/sequence controller of PAPER P:662-669 (host
+                  control only: switch, epoch refresh, one rk_solve per system)
+"""
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib as L
+
+
+def _p(t):
+    """Device (or host) pointer of a contiguous float64 tensor."""
+    if t is None:
+        return None
+    assert t.is_contiguous() and t.dtype == torch.float64, "need contiguous float64"
+    return C.c_void_p(t.data_ptr())
+
+
+class Context:
+    def __init__(self, device=0, rank=0, nranks=1, uid=None, stream=None):
+        lib = L.lib()
+        self.device = device
+        if stream is None:
+            stream = torch.cuda.current_stream(device).cuda_stream
+        h = C.c_void_p()
+        L.check(lib.rk_ctx_create(device, rank, nranks, uid, C.c_void_p(stream), C.byref(h)),
+                "rk_ctx_create")
+        self.h = h
+        self.rank, self.nranks = rank, nranks
+
+    def launches(self):
+        n = C.c_int64()
+        L.check(L.lib().rk_launch_count(self.h, C.byref(n)), "rk_launch_count")
+        return n.value
+
+    def profile(self, on=True, filter=None):
+        L.check(L.lib().rk_profile_enable(self.h, 1 if on else 0,
+                                          filter.encode() if filter else None), "rk_profile_enable")
+
+    def profile_read(self, reset=False):
+        cap = 64
+        names = C.create_string_buffer(32 * cap)
+        la = (C.c_int64 * cap)()
+        ms = (C.c_double * cap)()
+        by = (C.c_double * cap)()
+        n = C.c_int()
+        L.check(L.lib().rk_profile_read(self.h, -1 if reset else cap, names, la, ms, by, C.byref(n)),
+                "rk_profile_read")
+        out = {}
+        for i in range(min(n.value, cap)):
+            nm = names.raw[32 * i:32 * i + 32].split(b"\0")[0].decode()
+            out[nm] = {"launches": la[i], "ms": ms[i], "bytes": by[i]}
+        return out
+
+    def close(self):
+        if getattr(self, "h", None):
+            L.lib().rk_ctx_destroy(self.h)
+            self.h = None
+
+
+def nccl_unique_id():
+    buf = C.create_string_buffer(128)
+    L.check(L.lib().rk_nccl_unique_id(buf), "rk_nccl_unique_id")
+    return buf.raw
+
+
+class GridOperator:
+    """A in banded storage.  bands: float64 device tensor [S, nz_local, ny, nx];
+    offsets: int8 [S, 3] (dx, dy, dz)."""
+
+    def __init__(self, ctx, nx, ny, nz_global, offsets, bands, periodic=0, z0=0, nz_local=None):
+        nz_local = nz_global if nz_local is None else nz_local
+        self.ctx = ctx
+        self.nx, self.ny, self.nz_global, self.z0, self.nz_local = nx, ny, nz_global, z0, nz_local
+        self.N = nx * ny * nz_local
+        self.offsets = np.ascontiguousarray(np.asarray(offsets, dtype=np.int8).reshape(-1, 3))
+        g = L.rk_grid(nx, ny, nz_global, z0, nz_local, periodic)
+        bands = bands.contiguous()
+        assert bands.numel() == len(self.offsets) * self.N
+        h = C.c_void_p()
+        L.check(L.lib().rk_op_create(ctx.h, C.byref(g), len(self.offsets),
+                                     self.offsets.ctypes.data_as(C.c_void_p), _p(bands), C.byref(h)),
+                "rk_op_create")
+        self.h = h
+
+    def update_bands(self, bands):
+        L.check(L.lib().rk_op_update_bands(self.h, _p(bands.contiguous())), "rk_op_update_bands")
+
+    def apply(self, x, y=None):
+        y = torch.empty_like(x) if y is None else y
+        L.check(L.lib().rk_op_apply(self.h, _p(x), _p(y)), "rk_op_apply")
+        return y
+
+    def precond(self, r, z=None, kind=1, sweeps=5, omega_l=0.8, omega_g=1.0):
+        z = torch.empty_like(r) if z is None else z
+        pc = L.rk_precond(kind, sweeps, omega_l, omega_g)
+        L.check(L.lib().rk_precond_apply(self.h, C.byref(pc), _p(r), _p(z)), "rk_precond_apply")
+        return z
+
+    def close(self):
+        if getattr(self, "h", None):
+            L.lib().rk_op_destroy(self.h)
+            self.h = None
+
+
+def make_config(method="rgcrot", m=20, k_max=10, k_keep=5, select_count=1, precond="jacobi",
+                sweeps=5, omega_l=0.8, omega_g=1.0, tol=1e-8, max_matvecs=2000,
+                divergence=1e4):
+    pc = L.rk_precond(1 if precond == "jacobi" else 0, sweeps, omega_l, omega_g)
+    return L.rk_config(L.METHODS[method], m, k_max, k_keep, select_count, 0, 0, pc, tol,
+                       max_matvecs, divergence)
+
+
+def config_from_params(prm, method=None):
+    """rk_config from any object with SolverParams-like attributes."""
+    meth = method or prm.method
+    if meth == "hybrid":
+        meth = "rgcrot"
+    k = 0 if meth in ("gmres", "bicgstab") else prm.k_max
+    return make_config(method=meth, m=prm.m, k_max=k, k_keep=min(prm.k_t, k),
+                       select_count=0 if k == 0 else prm.p1,
+                       sweeps=prm.sweeps, omega_l=prm.omega_l, omega_g=prm.omega_g,
+                       tol=prm.tol, max_matvecs=prm.max_mv, divergence=prm.divergence)
+
+
+def _report(r):
+    return {
+        "outcome": L.OUTCOME_NAMES[r.outcome], "k_after": r.k_after,
+        "krylov_matvecs": r.krylov_matvecs, "operator_applications": r.operator_applications,
+        "cycles_or_iters": r.cycles_or_iters, "bnorm": r.bnorm,
+        "final_true_res": r.final_true_res, "final_updated_res": r.final_updated_res,
+        "seconds": r.seconds, "history_len": r.history_len,
+    }
+
+
+class Solver:
+    def __init__(self, op, config):
+        self.op = op
+        self.config = config
+        h = C.c_void_p()
+        L.check(L.lib().rk_solver_create(op.h, C.byref(config), C.byref(h)), "rk_solver_create")
+        self.h = h
+
+    def set_method(self, method):
+        L.check(L.lib().rk_solver_set_method(self.h, L.METHODS[method]), "rk_solver_set_method")
+
+    def solve(self, b, x=None, tol=0.0):
+        x = torch.zeros_like(b) if x is None else x
+        rep = L.rk_report()
+        L.check(L.lib().rk_solve(self.h, _p(b), _p(x), tol, C.byref(rep)), "rk_solve")
+        return x, _report(rep)
+
+    def solve_host(self, b_host, x_host, tol=0.0):
+        """b_host, x_host: CPU float64 tensors (pinned for async copies)."""
+        rep = L.rk_report()
+        L.check(L.lib().rk_solve_host(self.h, _p(b_host), _p(x_host), tol, C.byref(rep)),
+                "rk_solve_host")
+        return x_host, _report(rep)
+
+    def recycle_dim(self):
+        k = C.c_int()
+        L.check(L.lib().rk_recycle_dim(self.h, C.byref(k)), "rk_recycle_dim")
+        return k.value
+
+    def recycle_set(self, U, C_=None, R=None):
+        """U, C: device float64 [k, N] (column c = row c); R: host [k, k] or None."""
+        k = 0 if U is None else U.shape[0]
+        Rh = None
+        if R is not None:
+            Rh = np.asfortranarray(np.asarray(R, dtype=np.float64))
+        L.check(L.lib().rk_recycle_set(self.h, k, _p(U) if k else None,
+                                       _p(C_) if C_ is not None else None,
+                                       Rh.ctypes.data_as(C.c_void_p) if Rh is not None else None,
+                                       self.op.N), "rk_recycle_set")
+
+    def recycle_export(self):
+        k = self.recycle_dim()
+        dev = torch.device("cuda", self.op.ctx.device)
+        U = torch.empty((k, self.op.N), dtype=torch.float64, device=dev)
+        Cm = torch.empty((k, self.op.N), dtype=torch.float64, device=dev)
+        R = np.zeros((k, k))
+        L.check(L.lib().rk_recycle_export(self.h, _p(U) if k else None, _p(Cm) if k else None,
+                                          R.ctypes.data_as(C.c_void_p) if k else None,
+                                          self.op.N), "rk_recycle_export")
+        return U, Cm, R
+
+    def history(self):
+        n = C.c_int64()
+        L.check(L.lib().rk_history(self.h, None, 0, C.byref(n)), "rk_history")
+        out = np.zeros((n.value, 3))
+        L.check(L.lib().rk_history(self.h, out.ctypes.data_as(C.c_void_p), n.value, C.byref(n)),
+                "rk_history")
+        return out
+
+    def workspace(self):
+        n = C.c_int64()
+        L.check(L.lib().rk_solver_workspace(self.h, C.byref(n)), "rk_solver_workspace")
+        return n.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            L.lib().rk_solver_destroy(self.h)
+            self.h = None
+
+
+def solve_sequence(solver, rhs, n, method, n_sw=0, epoch_of=None, bands_for_epoch=None,
+                   tol=0.0, host=False, x_out=None):
+    """Sequence controller (reading D3): for the hybrid,
+    systems t < n_sw use rGCROT and later ones rBiCGStab with the recycle
+    space frozen; a new A epoch uploads its bands (librk then invalidates C
+    and rebuilds it by QR of op(U) in the next solve).  rhs(t) -> b_t (device
+    tensor, or pinned host tensor if host=True).  Returns the reports;
+    solutions go to x_out[t] when given.  The operator must hold the bands of
+    epoch_of(0) on entry."""
+    reps = []
+    cur = epoch_of(0) if epoch_of else 0
+    for t in range(n):
+        e = epoch_of(t) if epoch_of else 0
+        if e != cur:
+            solver.op.update_bands(bands_for_epoch(e))
+            cur = e
+        if method == "hybrid":
+            solver.set_method("rgcrot" if t < n_sw else "rbicgstab")
+        b = rhs(t)
+        x = x_out[t] if x_out is not None else torch.zeros_like(b)
+        x.zero_()
+        if host:
+            _, r = solver.solve_host(b, x, tol)
+        else:
+            _, r = solver.solve(b, x, tol)
+        r["tag"] = ("rgcrot" if t < n_sw else "rbicgstab") if method == "hybrid" else method
+        reps.append(r)
+    return reps

@@ -1,0 +1,176 @@
+// Internal declarations of librk (not part of the ABI; see include/rk.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "rk.h"
+
+#ifdef RK_WITH_NCCL
+#include <nccl.h>
+#endif
+
+namespace rk {
+
+constexpr int MAXCOL = 80;      // columns of one block product ([C V_j w] <= k_max + m + 1)
+constexpr int MAXOUT = 5;       // outputs of one lincomb (dx, u1, c1, u2, c2)
+
+struct Error : std::runtime_error {
+  rk_status st;
+  Error(rk_status s, const std::string& m) : std::runtime_error(m), st(s) {}
+};
+
+#define RK_CUDA(call)                                                                  \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      throw ::rk::Error(RK_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define RK_REQUIRE(cond, st, msg)                    \
+  do {                                               \
+    if (!(cond)) throw ::rk::Error((st), (msg));     \
+  } while (0)
+
+// ---------------------------------------------------------------- kernels
+struct ColPtrs {
+  const double* p[MAXCOL];
+};
+
+struct RedArgs {
+  double* partials;     // [nval][gridDim.x]
+  unsigned* counter;    // last-block ticket (reset by the last block)
+  double* out;          // nval results
+};
+
+// Stencil kernel modes (K1/K2 of SURVEY §2.4)
+enum StencilMode {
+  SM_SPMV = 0,          // out0 = A x
+  SM_SPMV_SWEEP1 = 1,   // out0 = t = A x ; out1 = w t / D            (first Jacobi sweep fused)
+  SM_SWEEP = 2,         // out0 = x + w (r - A x) / D                 (Jacobi sweep, x = z_in)
+  SM_SWEEP_NORM = 3,    // SM_SWEEP + red ||out0||^2
+  SM_RESID = 4,         // out0 = r - A x ; red ||out0||^2            (true residual, r = b)
+  SM_RESID_SWEEP1 = 5,  // SM_RESID + out1 = w out0 / D
+  SM_SCALE = 6,         // out0 = w r / D   (first sweep from z = 0; no stencil)
+};
+
+struct StencilParams {
+  const double* bands;  // [S][N] canonical order, band 0 = diagonal
+  int64_t N, P;
+  int nx, ny, nzl;
+  int px, py, wrapz;
+  const double* x;      // padded stencil input (ghost planes at -P and N)
+  const double* r;
+  double* out0;
+  double* out1;
+  double omega;
+  RedArgs red;
+};
+
+struct LcOut {
+  double* out[MAXOUT];
+  double scale[MAXOUT];
+  int acc[MAXOUT];
+};
+
+// Per-iteration device scalars of rBiCGStab (one 64-byte record per iteration).
+struct BiIter {
+  double rho;    // r~^T r_i            (written by iteration i-1 or the setup)
+  double rr;     // ||r_i||^2
+  double sigma;  // r~^T v_i            (v projected)
+  double ss;     // ||s_i||^2
+  double ts;     // t_i^T s_i           (t projected)
+  double tt;     // ||t_i||^2
+  double flag;   // 0 normal, 1 exact exit (s = 0), 2 breakdown
+  double pad;
+};
+
+}  // namespace rk
+
+// ----------------------------------------------------------------- objects
+struct ProfAgg {
+  int64_t launches = 0;
+  double ms = 0.0;
+  double bytes = 0.0;
+};
+
+struct rk_ctx {
+  int device = 0, rank = 0, nranks = 1, sms = 148;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  double* partials = nullptr;
+  size_t partials_cap = 0;      // doubles
+  unsigned* counter = nullptr;
+  int64_t launches = 0;
+  // profiling
+  bool prof_on = false;
+  std::string prof_filter;
+  struct Pending {
+    std::string cls;
+    cudaEvent_t a, b;
+    double bytes;
+  };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> pool;
+  std::map<std::string, ProfAgg> agg;
+#ifdef RK_WITH_NCCL
+  ncclComm_t comm = nullptr;
+#endif
+  // grid sizes per kernel family (multiples of the SM count)
+  int grid_stencil = 0, grid_blas = 0;
+};
+
+struct rk_op {
+  rk_ctx* ctx = nullptr;
+  rk_grid g{};
+  int S = 7;                    // 7, 19 or 27 (canonical layout)
+  int64_t N = 0, P = 0;
+  double* bands = nullptr;      // [S][N]
+  int64_t epoch = 0;
+  // scratch (padded) for rk_op_apply / rk_precond_apply
+  double* scratch_base[2] = {nullptr, nullptr};
+  double* scratch[2] = {nullptr, nullptr};
+  int wrapz = 0;
+  std::vector<int8_t> user_offsets;   // caller's band order (for rk_op_update_bands)
+};
+
+namespace rk {
+
+// ------------------------------------------------------------ launch layer
+// All kernels are launched through these wrappers (kernels.cu).  Each
+// increments ctx->launches and, when profiling, is bracketed by events.
+void init_ctx_kernels(rk_ctx* ctx);
+void stencil(rk_op* op, int mode, const double* x, const double* r, double* out0,
+             double* out1, double omega, double* red_out);
+void bdot(rk_ctx* ctx, const std::vector<const double*>& cols, const double* w, int64_t N,
+          double* out);
+void bupd(rk_ctx* ctx, const std::vector<const double*>& cols, const double* g, double gscale,
+          double* w, int64_t N, const std::vector<const double*>& dots, double* red_out);
+void normalize(rk_ctx* ctx, double* w, int64_t N, const double* nrm2, const double* nin2,
+               double* flag);
+void lincomb(rk_ctx* ctx, const std::vector<const double*>& cols, const double* coef, int nout,
+             const LcOut& lo, int64_t N);
+void proj(rk_ctx* ctx, const std::vector<const double*>& C, const std::vector<const double*>& U,
+          const double* xi, double* r, double* x, int64_t N, double* red_out);
+void rotate(rk_ctx* ctx, const std::vector<double*>& cols, const double* T, int64_t N);
+void bicg_p(rk_op* op, const double* r, double* p, const double* v, double* z, double wl,
+            bool jacobi, const BiIter* cur, const BiIter* prev, int first);
+void bicg_s(rk_op* op, const double* r, const double* v, double* s, double* z, double wl,
+            bool jacobi, BiIter* cur);
+void bicg_xr(rk_ctx* ctx, double* x, double* r, const double* s, const double* t, const double* ph,
+             const double* sh, const double* rt, int64_t N, BiIter* cur, BiIter* next, double* xi,
+             const double* eta1, const double* eta2, int k);
+void bicg_setup(rk_ctx* ctx, double* xi, const double* eta0, int k, BiIter* it0);
+int validate_bands(rk_op* op);
+
+// communication (comm.cpp): no-ops for one rank
+void halo(rk_op* op, const double* v);
+void allreduce(rk_ctx* ctx, double* buf, int n);
+
+}  // namespace rk

@@ -1,0 +1,347 @@
+"""GPU parity: the CUDA path through the C-ABI vs the oracle, element by
+element on the same seeded inputs.  Tolerances (BASELINE north_star and
+DESIGN.md "Tolerances"):
+  * per kernel: componentwise |y_gpu - y_ref| <= 1e-12 (|A||x|)_i for the
+    SpMV against an extended-precision reference (reading D25); 1e-12
+    relative (inf-norm) for the 6-sweep preconditioner;
+  * per solve: true relative residual <= tol (1e-8), ||x_gpu - x_or|| /
+    ||x_or|| <= 1e-6, Krylov matvecs within +-10 % of the oracle per
+    sequence and within one cycle (rGCROT) / 10 % (rBiCGStab) per system.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import run_sequence
+from oracle.krylov import OUTCOME_NAMES, refresh_space, rgcrot
+from oracle.stencil import Jacobi, Operator
+from problems import OFFSETS7, OFFSETS19, SolverParams, get_workload
+from problems.stencils import channel19, convection_diffusion_c1, porous7
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def rk():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_1501_03358_b200 as rk
+    rk.lib()
+    return rk
+
+
+@pytest.fixture(scope="module")
+def ctx(rk):
+    c = rk.Context(0)
+    yield c
+    c.close()
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
+def make_op(rk, ctx, prob, epoch=0):
+    return rk.GridOperator(ctx, prob.nx, prob.ny, prob.nz, prob.offsets, dev(prob.bands(epoch=epoch)),
+                           prob.periodic)
+
+
+def random_op_problem(nx, ny, nz, periodic, offsets, seed):
+    rng = np.random.default_rng(seed)
+    S = len(offsets)
+    bands = rng.uniform(-1, 1, size=(S, nz, ny, nx))
+    bands[0] += 8.0
+    k = np.arange(nz)[:, None, None]
+    j = np.arange(ny)[None, :, None]
+    i = np.arange(nx)[None, None, :]
+    for d, (dx, dy, dz) in enumerate(offsets):
+        for idx, dd, n, bit in ((i, dx, nx, 1), (j, dy, ny, 2), (k, dz, nz, 4)):
+            if dd and not (periodic & bit):
+                bad = np.broadcast_to((idx + dd < 0) | (idx + dd >= n), bands[d].shape)
+                bands[d][bad] = 0.0
+    return bands
+
+
+# ------------------------------------------------------------ K1 SpMV
+SPMV_CASES = [
+    ("c1", lambda: convection_diffusion_c1(16)),
+    ("channel24", lambda: channel19(24)),
+    ("porous40", lambda: porous7(40, 4)),
+    ("c2_full", lambda: channel19(64)),
+    ("c3_full", lambda: porous7(128, 6)),
+]
+
+
+@pytest.mark.parametrize("name,mk", SPMV_CASES, ids=[c[0] for c in SPMV_CASES])
+def test_spmv_parity(rk, ctx, name, mk):
+    prob = mk()
+    op = make_op(rk, ctx, prob)
+    ref = Operator.from_problem(prob)
+    x = np.random.default_rng(1).uniform(-1, 1, prob.N)
+    y = op.apply(dev(x)).cpu().numpy()
+    yr = ref.apply_ld(x).astype(np.float64)
+    scale = ref.apply_abs(x)
+    assert np.all(np.abs(y - yr) <= 1e-12 * scale)
+    op.close()
+
+
+@pytest.mark.parametrize("offs,periodic,shape", [
+    (OFFSETS7, 0, (5, 7, 3)),            # odd sizes: scalar path, ragged rows
+    (OFFSETS19, 7, (6, 5, 4)),           # fully periodic, 19-point
+    (OFFSETS19, 5, (33, 9, 5)),          # nx not a multiple of 32
+    (np.array([(0, 0, 0), (1, 1, 1), (-1, 1, 0), (0, 0, -1)], dtype=np.int8), 2, (7, 6, 5)),  # 27-pt layout
+])
+def test_spmv_random_bands(rk, ctx, offs, periodic, shape):
+    nx, ny, nz = shape
+    bands = random_op_problem(nx, ny, nz, periodic, offs, seed=nx * ny + nz)
+    op = rk.GridOperator(ctx, nx, ny, nz, offs, dev(bands), periodic)
+    ref = Operator(nx, ny, nz, periodic, offs, bands)
+    x = np.random.default_rng(2).uniform(-1, 1, ref.N)
+    y = op.apply(dev(x)).cpu().numpy()
+    yr = ref.apply_ld(x).astype(np.float64)
+    assert np.all(np.abs(y - yr) <= 1e-12 * ref.apply_abs(x))
+    op.close()
+
+
+def test_truncation_violation_rejected(rk, ctx):
+    b = np.zeros((7, 2, 2, 2))
+    b[0] = 1.0
+    b[1] = 1.0
+    with pytest.raises(rk.RkError, match="EINVAL"):
+        rk.GridOperator(ctx, 2, 2, 2, OFFSETS7, dev(b), 0)
+    with pytest.raises(rk.RkError, match="EINVAL"):
+        rk.GridOperator(ctx, 2, 2, 2, np.array([(2, 0, 0), (0, 0, 0)], dtype=np.int8),
+                        dev(np.ones((2, 2, 2, 2))), 0)
+
+
+# ------------------------------------------------------------ K2 Jacobi(5+1)
+@pytest.mark.parametrize("name,mk", SPMV_CASES[:4], ids=[c[0] for c in SPMV_CASES[:4]])
+def test_precond_parity(rk, ctx, name, mk):
+    prob = mk()
+    op = make_op(rk, ctx, prob)
+    ref = Operator.from_problem(prob)
+    r = np.random.default_rng(3).uniform(-1, 1, prob.N)
+    z = op.precond(dev(r)).cpu().numpy()
+    zr = Jacobi(ref)(r)
+    assert np.max(np.abs(z - zr)) <= 1e-12 * np.max(np.abs(zr))
+    op.close()
+
+
+# ------------------------------------------------------------ solves
+def gpu_sequence(rk, ctx, w, solver_name=None, host=False):
+    prob = w.problem()
+    prm = w.params
+    method = solver_name or prm.method
+    op = make_op(rk, ctx, prob, epoch=w.epoch(0))
+    s = rk.Solver(op, rk.config_from_params(prm, method))
+    xs = [torch.zeros(prob.N, dtype=torch.float64, device="cuda") for _ in range(w.n_systems)]
+    if host:
+        xs = [torch.zeros(prob.N, dtype=torch.float64).pin_memory() for _ in range(w.n_systems)]
+    rhs = (lambda t: torch.from_numpy(prob.rhs(t).reshape(-1)).pin_memory()) if host else \
+        (lambda t: dev(prob.rhs(t).reshape(-1)))
+    reps = rk.solve_sequence(s, rhs, w.n_systems, method, n_sw=prm.n_sw, epoch_of=w.epoch,
+                             bands_for_epoch=lambda e: dev(prob.bands(epoch=e)), host=host, x_out=xs)
+    out = [(r, x.cpu().numpy()) for r, x in zip(reps, xs)]
+    U, C, R = s.recycle_export()
+    s.close()
+    op.close()
+    return out, (U.cpu().numpy(), C.cpu().numpy())
+
+
+def compare_sequences(w, gpu, ora, method):
+    prob = w.problem()
+    m = w.params.m
+    tot_g = tot_o = 0
+    for t, ((rg, xg), (tag, xo, ro)) in enumerate(zip(gpu, ora)):
+        e = w.epoch(t)
+        op = Operator.from_problem(prob, epoch=e)
+        b = prob.rhs(t).reshape(-1)
+        assert rg["outcome"] == OUTCOME_NAMES[ro.outcome], (t, rg, ro)
+        if rg["outcome"] == "CONVERGED":
+            tr = np.linalg.norm(b - op.apply(xg)) / np.linalg.norm(b)
+            assert tr <= w.params.tol * (1 + 1e-6), (t, tr)
+            assert np.linalg.norm(xg - xo) <= 1e-6 * np.linalg.norm(xo), t
+        ng, no = rg["krylov_matvecs"], ro.krylov_mv
+        tot_g += ng
+        tot_o += no
+        if rg["tag"] == "rbicgstab" or method in ("bicgstab",):
+            assert abs(ng - no) <= max(0.1 * no, 2), (t, ng, no)
+        else:
+            assert abs(ng - no) <= m, (t, ng, no)
+    assert abs(tot_g - tot_o) <= 0.1 * tot_o + 2, (tot_g, tot_o)
+
+
+@pytest.mark.parametrize("name,solver", [
+    ("c1", None), ("c1s", None), ("c2s", None), ("c3s", None), ("c4s", None), ("c4hs", None),
+    ("c2s", "gmres"), ("c3s", "bicgstab"), ("c3s", "rgcrot"),
+])
+def test_sequence_parity(rk, ctx, name, solver):
+    w = get_workload(name)
+    method = solver or w.params.method
+    ora = run_sequence(w, solver=method)
+    gpu, _ = gpu_sequence(rk, ctx, w, method)
+    compare_sequences(w, gpu, ora, method)
+
+
+def test_sequence_parity_host_buffers(rk, ctx):
+    """The same through rk_solve_host (host b and x; copies inside the call)."""
+    w = get_workload("c3s")
+    ora = run_sequence(w)
+    gpu, _ = gpu_sequence(rk, ctx, w, host=True)
+    compare_sequences(w, gpu, ora, w.params.method)
+
+
+def test_recycle_space_invariants_after_hybrid(rk, ctx):
+    """After the hybrid the exported space satisfies A U = C, C^T C = I
+    (BASELINE north_star: 1e-12), i.e. the rBiCGStab-side QR refresh."""
+    w = get_workload("c3s")
+    _, (U, C) = gpu_sequence(rk, ctx, w)
+    op = Operator.from_problem(w.problem())
+    k = U.shape[0]
+    assert k > 0
+    AU = np.stack([op.apply(U[c]) for c in range(k)])
+    assert np.linalg.norm(C @ C.T - np.eye(k)) <= 1e-12 * k
+    assert np.linalg.norm(AU - C) <= 1e-12 * np.linalg.norm(AU) * 10
+
+
+def test_rgcrot_space_invariants(rk, ctx):
+    """rGCROT-side space: M^-1 A U = C and C^T C = I to 1e-12."""
+    w = get_workload("c2s")
+    _, (U, C) = gpu_sequence(rk, ctx, w)
+    op = Operator.from_problem(w.problem())
+    pc = Jacobi(op)
+    k = U.shape[0]
+    AU = np.stack([pc(op.apply(U[c])) for c in range(k)])
+    assert np.linalg.norm(C @ C.T - np.eye(k)) <= 1e-12 * k
+    assert np.linalg.norm(AU - C) <= 1e-11 * np.linalg.norm(AU)
+
+
+def test_zero_rhs_and_zero_cycle_exit(rk, ctx):
+    prob = convection_diffusion_c1(6)
+    op = make_op(rk, ctx, prob)
+    prm = SolverParams(m=5, k_max=3, k_t=2, p1=1)
+    s = rk.Solver(op, rk.config_from_params(prm))
+    x, r = s.solve(torch.zeros(prob.N, dtype=torch.float64, device="cuda"))
+    assert r["outcome"] == "CONVERGED" and r["krylov_matvecs"] == 0
+    assert float(x.abs().max()) == 0.0
+    # S:243 r_hat in range(C): zero cycles, x = U w
+    ref = Operator.from_problem(prob)
+    pc = Jacobi(ref)
+    U0 = np.random.default_rng(4).uniform(-1, 1, (prob.N, 3))
+    U, C, _ = refresh_space(lambda v: pc(ref.apply(v)), U0)
+    s.recycle_set(dev(U.T.copy()), dev(C.T.copy()))
+    wv = np.array([0.3, -1.2, 0.5])
+    b = ref.apply(U @ wv)
+    x, r = s.solve(dev(b))
+    assert r["krylov_matvecs"] == 0 and r["cycles_or_iters"] == 0 and r["outcome"] == "CONVERGED"
+    assert np.linalg.norm(x.cpu().numpy() - U @ wv) <= 1e-9 * np.linalg.norm(U @ wv)
+    # refresh path: U without C -> QR of A_hat U on the next solve
+    s.recycle_set(dev(U0.T.copy()))
+    x, r = s.solve(dev(b))
+    assert r["operator_applications"] >= 3 and r["outcome"] == "CONVERGED"
+    Ue, Ce, R = s.recycle_export()
+    Ue, Ce = Ue.cpu().numpy(), Ce.cpu().numpy()
+    AU = np.stack([pc(ref.apply(Ue[c])) for c in range(Ue.shape[0])])
+    assert np.linalg.norm(AU - Ce) <= 1e-11 * np.linalg.norm(AU)
+    assert np.array_equal(R, np.eye(Ue.shape[0]))
+    s.close()
+    op.close()
+
+
+def test_happy_breakdown_identity(rk, ctx):
+    """A = I: Arnoldi breaks down after one step (reading D18); one cycle, x = b."""
+    b = np.zeros((7, 4, 4, 4))
+    b[0] = 1.0
+    op = rk.GridOperator(ctx, 4, 4, 4, OFFSETS7, dev(b), 0)
+    s = rk.Solver(op, rk.make_config("gmres", m=6, k_max=0, k_keep=0, select_count=0,
+                                     precond="none"))
+    rhs = np.random.default_rng(0).uniform(-1, 1, 64)
+    x, r = s.solve(dev(rhs))
+    assert r["outcome"] == "CONVERGED" and r["krylov_matvecs"] == 1 and r["cycles_or_iters"] == 1
+    assert np.allclose(x.cpu().numpy(), rhs, rtol=1e-14, atol=1e-15)
+    s.close()
+    op.close()
+
+
+def test_bicgstab_forced_breakdown(rk, ctx):
+    """A = diag(1,-1,1,1) + periodic skew difference, identity
+    preconditioner, b = e0 + e1: sigma = b^T A b = 0 exactly -> BREAKDOWN."""
+    offs = np.array([(0, 0, 0), (-1, 0, 0), (1, 0, 0)], dtype=np.int8)
+    bands = np.zeros((3, 1, 1, 4))
+    bands[0] = np.array([1.0, -1.0, 1.0, 1.0])
+    bands[1] = -1.0
+    bands[2] = 1.0
+    op = rk.GridOperator(ctx, 4, 1, 1, offs, dev(bands), 1)
+    s = rk.Solver(op, rk.make_config("bicgstab", m=4, k_max=0, k_keep=0, select_count=0,
+                                     precond="none"))
+    x, r = s.solve(dev(np.array([1.0, 1.0, 0, 0])))
+    assert r["outcome"] == "BREAKDOWN" and r["cycles_or_iters"] == 0
+    assert torch.isfinite(x).all()
+    s.close()
+    op.close()
+
+
+def test_workspace_audit(rk, ctx):
+    """the audit reports the N-vectors actually allocated:
+    max(m+1, 8) basis/work + 2 (k_max + 2) recycle slots + 5 work vectors."""
+    prob = convection_diffusion_c1(8)
+    op = make_op(rk, ctx, prob)
+    for m, k in ((10, 6), (4, 0), (30, 20)):
+        s = rk.Solver(op, rk.make_config("rgcrot", m=m, k_max=k, k_keep=k // 2))
+        assert s.workspace() == max(m + 1, 8) + (2 * (k + 2) if k else 0) + 5
+        s.close()
+    op.close()
+
+
+# ------------------------------------------------- full BASELINE sizes
+def test_c3_full_size_first_cycle_and_sequence_properties(rk, ctx):
+    """configs[2] at full size: (a) the first rGCROT cycle of system 0 equals
+    the oracle's cycle (x after m = 10 matvecs); (b) the whole 20-system
+    hybrid sequence converges with true residual <= tol for every system
+    (residuals recomputed by the oracle SpMV), and the frozen recycle space
+    satisfies A U = C, C^T C = I."""
+    w = get_workload("c3")
+    prob = w.problem()
+    prm = w.params
+    ref = Operator.from_problem(prob)
+    pc = Jacobi(ref)
+    b0 = prob.rhs(0).reshape(-1)
+    from dataclasses import replace
+    one = replace(prm, max_mv=prm.m, tol=1e-30)
+    e = np.zeros((prob.N, 0))
+    xo, _, _, ro = rgcrot(ref, pc, b0, e, e, one)
+    op = make_op(rk, ctx, prob)
+    s = rk.Solver(op, rk.config_from_params(one, "rgcrot"))
+    xg, rg = s.solve(dev(b0), tol=1e-30)
+    assert rg["krylov_matvecs"] == prm.m and rg["cycles_or_iters"] == 1
+    assert np.linalg.norm(xg.cpu().numpy() - xo) <= 1e-10 * np.linalg.norm(xo)
+    s.close()
+    gpu, (U, C) = gpu_sequence(rk, ctx, w)
+    for t, (r, x) in enumerate(gpu):
+        b = prob.rhs(t).reshape(-1)
+        assert r["outcome"] == "CONVERGED", (t, r)
+        assert np.linalg.norm(b - ref.apply(x)) <= prm.tol * np.linalg.norm(b)
+    assert [r["tag"] for r, _ in gpu] == ["rgcrot"] * 3 + ["rbicgstab"] * 17
+    k = U.shape[0]
+    G = C @ C.T
+    assert np.linalg.norm(G - np.eye(k)) <= 1e-12 * k
+    AU = np.stack([ref.apply(U[c]) for c in range(k)])
+    assert np.linalg.norm(AU - C) <= 1e-11 * np.linalg.norm(AU)
+    op.close()
+
+
+def test_c2_full_size_sequence_properties(rk, ctx):
+    """configs[1] at full size (64^3, 19-point, 10 systems): every system
+    converges to the true relative residual tol; recycling reduces the
+    matvecs after the first system; the space satisfies M^-1 A U = C."""
+    w = get_workload("c2")
+    prob = w.problem()
+    ref = Operator.from_problem(prob)
+    gpu, (U, C) = gpu_sequence(rk, ctx, w)
+    for t, (r, x) in enumerate(gpu):
+        b = prob.rhs(t).reshape(-1)
+        assert r["outcome"] == "CONVERGED"
+        assert np.linalg.norm(b - ref.apply(x)) <= w.params.tol * np.linalg.norm(b)
+    mv = [r["krylov_matvecs"] for r, _ in gpu]
+    assert np.mean(mv[1:]) < mv[0]
+    k = U.shape[0]
+    assert np.linalg.norm(C @ C.T - np.eye(k)) <= 1e-12 * k

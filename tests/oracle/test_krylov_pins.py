@@ -243,6 +243,12 @@ def test_bicgstab_forced_breakdown():
     b = np.array([1.0, 0, 0, 0])
     x, rep = bicgstab(op, lambda r: r.copy(), b, SolverParams(tol=1e-8))
     assert rep.outcome == BREAKDOWN and rep.cycles == 0
+    # nonzero diagonal variant (the one the GPU test uses): A = diag(1,-1,1,1)
+    # + skew, b = e0 + e1 -> sigma = b^T A b = 1 - 1 + b^T K b = 0 exactly
+    bands[0] = np.array([1.0, -1.0, 1.0, 1.0]).reshape(1, 1, 4)
+    op = Operator(4, 1, 1, 1, offs, bands)
+    x, rep = bicgstab(op, lambda r: r.copy(), np.array([1.0, 1.0, 0, 0]), SolverParams(tol=1e-8))
+    assert rep.outcome == BREAKDOWN and rep.cycles == 0 and rep.krylov_mv == 1
 
 
 def test_rbicgstab_k0_is_bicgstab_identity_case():
