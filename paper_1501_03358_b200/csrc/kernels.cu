@@ -1,23 +1,74 @@
 // sm_100a kernels of librk: the per-iteration hot path of rGCROT / rBiCGStab
 // (SURVEY.md §2.4 K1-K8).  Every kernel here is HBM-bound fp64 work on the
-// CUDA cores (0.1-0.3 flop/B, SURVEY §8(a) "Tensor cores"): coalesced
-// x-fastest rows, streaming (L1::no_allocate) loads for data read once
-// (bands, basis columns), grids sized as a multiple of the SM count with
-// grid-stride loops, and deterministic two-stage reductions (per-CTA
-// partials + last-CTA fixed-order finalisation, no float atomics).
+// CUDA cores (0.1-0.3 flop/B, SURVEY §8(a) "Tensor cores"):
+//  * coalesced x-fastest rows, two consecutive cells per thread with 16-byte
+//    loads wherever the data allows (VEC = 2);
+//  * streaming (ld.global.nc.L1::no_allocate) loads for data read once per
+//    launch (bands, basis columns);
+//  * grids sized from each instantiation's occupancy: SMs x resident CTAs,
+//    grid-stride loops;
+//  * deterministic two-stage reductions (per-CTA partials + fixed-order
+//    finalisation by the last CTA; no floating-point atomics).
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <initializer_list>
 
 #include "rk_internal.h"
 
 namespace rk {
 
 // ------------------------------------------------------------------ helpers
-__device__ __forceinline__ double ld_stream(const double* p) {
-  double v;
-  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
-  return v;
+template <int VEC>
+struct Vec {
+  double v[VEC];
+};
+
+template <int VEC>
+__device__ __forceinline__ Vec<VEC> ldv_stream(const double* p) {
+  Vec<VEC> r;
+  if constexpr (VEC == 2) {
+    asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(r.v[0]), "=d"(r.v[1]) : "l"(p));
+  } else {
+    asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r.v[0]) : "l"(p));
+  }
+  return r;
+}
+
+// read-only (non-coherent) path: data not written by the same launch
+template <int VEC>
+__device__ __forceinline__ Vec<VEC> ldv_ro(const double* p) {
+  Vec<VEC> r;
+  if constexpr (VEC == 2) {
+    const double2 t = __ldg(reinterpret_cast<const double2*>(p));
+    r.v[0] = t.x;
+    r.v[1] = t.y;
+  } else {
+    r.v[0] = __ldg(p);
+  }
+  return r;
+}
+
+template <int VEC>
+__device__ __forceinline__ Vec<VEC> ldv(const double* p) {
+  Vec<VEC> r;
+  if constexpr (VEC == 2) {
+    const double2 t = *reinterpret_cast<const double2*>(p);
+    r.v[0] = t.x;
+    r.v[1] = t.y;
+  } else {
+    r.v[0] = *p;
+  }
+  return r;
+}
+
+template <int VEC>
+__device__ __forceinline__ void stv(double* p, const Vec<VEC>& a) {
+  if constexpr (VEC == 2) {
+    *reinterpret_cast<double2*>(p) = make_double2(a.v[0], a.v[1]);
+  } else {
+    *p = a.v[0];
+  }
 }
 
 // Canonical stencil layouts.  Band 0 is the diagonal.
@@ -26,9 +77,9 @@ __device__ __forceinline__ double ld_stream(const double* p) {
 //     xz edges (x,z) = (-1,-1)(1,-1)(-1,1)(1,1)
 // 27: centre, then the other 26 offsets in lexicographic (dz, dy, dx) order.
 template <int ST>
-__host__ __device__ __forceinline__ void offs(int d, int& dx, int& dy, int& dz) {
+__host__ __device__ constexpr void offs(int d, int& dx, int& dy, int& dz) {
   if (ST == 27) {
-    int e = d == 0 ? 13 : (d <= 13 ? d - 1 : d);
+    const int e = d == 0 ? 13 : (d <= 13 ? d - 1 : d);
     dx = e % 3 - 1;
     dy = (e / 3) % 3 - 1;
     dz = e / 9 - 1;
@@ -40,6 +91,16 @@ __host__ __device__ __forceinline__ void offs(int d, int& dx, int& dy, int& dz) 
   dx = DX[d];
   dy = DY[d];
   dz = DZ[d];
+}
+
+template <int ST>
+__host__ __device__ constexpr bool uses(int dx, int dy, int dz) {
+  for (int d = 0; d < ST; ++d) {
+    int a = 0, b = 0, c = 0;
+    offs<ST>(d, a, b, c);
+    if (a == dx && b == dy && c == dz) return true;
+  }
+  return false;
 }
 
 // Block reduction of NV per-thread values -> per-CTA partials -> the last CTA
@@ -87,23 +148,38 @@ __device__ __forceinline__ void block_reduce_store(const double (&v)[NV], int nv
 }
 
 // -------------------------------------------------------------- K1 / K2
-// One thread per cell of an x-row; rows (j, k) grid-strided over the CTAs.
-// Out-of-grid neighbours on non-periodic x/y are clamped onto the cell itself
-// (their coefficient is 0 by the truncation invariant); z neighbours read the
-// ghost planes (zero, or halo data from the neighbouring rank), or wrap for
-// a single-rank periodic z.
-template <int ST, int MODE>
+// Each thread owns VEC consecutive cells of an x-row (VEC = 2: 16-byte band
+// and centre loads, the x-1 / x+VEC neighbours as scalars); rows (j, k) are
+// grid-strided over the CTAs.  Out-of-grid neighbours on non-periodic x/y
+// are clamped onto a valid cell (their coefficient is 0 by the truncation
+// invariant); z neighbours read the ghost planes (zero, or halo data from the
+// neighbouring rank), or wrap for a single-rank periodic z.
+template <int ST, int MODE, int VEC>
 __global__ void __launch_bounds__(256) stencil_kernel(StencilParams sp) {
   constexpr bool RED = (MODE == SM_SWEEP_NORM || MODE == SM_RESID || MODE == SM_RESID_SWEEP1);
   const int BX = blockDim.x, BY = blockDim.y;
   const int tx = threadIdx.x, ty = threadIdx.y;
   double red[1] = {0.0};
   const int64_t R = (int64_t)sp.ny * sp.nzl;
+  const int nxv = sp.nx / VEC;
   for (int64_t row = (int64_t)blockIdx.x * BY + ty; row < R; row += (int64_t)gridDim.x * BY) {
     const int k = (int)(row / sp.ny);
     const int j = (int)(row - (int64_t)k * sp.ny);
+    const int64_t base = (int64_t)k * sp.P + (int64_t)j * sp.nx;
+    if constexpr (MODE == SM_SCALE) {
+      for (int iv = tx; iv < nxv; iv += BX) {
+        const int64_t n = base + (int64_t)iv * VEC;
+        const Vec<VEC> D = ldv_stream<VEC>(sp.bands + n);
+        const Vec<VEC> r = ldv_ro<VEC>(sp.r + n);
+        Vec<VEC> o;
+#pragma unroll
+        for (int t = 0; t < VEC; ++t) o.v[t] = sp.omega * r.v[t] / D.v[t];
+        stv<VEC>(sp.out0 + n, o);
+      }
+      continue;
+    }
     int64_t zo[3], yo[3];
-    if (MODE != SM_SCALE) {
+    {
       int km = k - 1, kp = k + 1;
       if (sp.wrapz) {
         if (km < 0) km = sp.nzl - 1;
@@ -124,55 +200,84 @@ __global__ void __launch_bounds__(256) stencil_kernel(StencilParams sp) {
       yo[1] = (int64_t)j * sp.nx;
       yo[2] = (int64_t)jp * sp.nx;
     }
-    const int64_t base = (int64_t)k * sp.P + (int64_t)j * sp.nx;
-    for (int i = tx; i < sp.nx; i += BX) {
-      const int64_t n = base + i;
-      if (MODE == SM_SCALE) {
-        const double D = ld_stream(sp.bands + n);
-        sp.out0[n] = sp.omega * __ldg(sp.r + n) / D;
-        continue;
+    for (int iv = tx; iv < nxv; iv += BX) {
+      const int i0 = iv * VEC;
+      const int64_t n = base + i0;
+      int im = i0 - 1, ip = i0 + VEC;
+      if (sp.px) {
+        if (im < 0) im = sp.nx - 1;
+        if (ip >= sp.nx) ip = 0;
+      } else {
+        im = im < 0 ? 0 : im;
+        ip = ip >= sp.nx ? sp.nx - 1 : ip;
       }
-      int xo[3];
-      {
-        int im = i - 1, ip = i + 1;
-        if (sp.px) {
-          if (im < 0) im = sp.nx - 1;
-          if (ip >= sp.nx) ip = 0;
-        } else {
-          im = im < 0 ? 0 : im;
-          ip = ip >= sp.nx ? sp.nx - 1 : ip;
+      // gather the x values the stencil touches: per (dy, dz) a centre
+      // vector plus the left / right scalar when the stencil reaches dx = -1/+1
+      Vec<VEC> xc[3][3];
+      double xl[3][3], xr[3][3];
+#pragma unroll
+      for (int dz = -1; dz <= 1; ++dz)
+#pragma unroll
+        for (int dy = -1; dy <= 1; ++dy) {
+          const bool any = uses<ST>(-1, dy, dz) || uses<ST>(0, dy, dz) || uses<ST>(1, dy, dz);
+          if (any) {
+            const double* p = sp.x + zo[dz + 1] + yo[dy + 1];
+            xc[dy + 1][dz + 1] = ldv_ro<VEC>(p + i0);
+            if (uses<ST>(-1, dy, dz)) xl[dy + 1][dz + 1] = __ldg(p + im);
+            if (uses<ST>(1, dy, dz)) xr[dy + 1][dz + 1] = __ldg(p + ip);
+          }
         }
-        xo[0] = im;
-        xo[1] = i;
-        xo[2] = ip;
-      }
-      double y = 0.0, a0 = 0.0, x0 = 0.0;
+      double y[VEC], a0[VEC];
+#pragma unroll
+      for (int t = 0; t < VEC; ++t) y[t] = 0.0;
 #pragma unroll
       for (int d = 0; d < ST; ++d) {
-        int dx, dy, dz;
+        int dx = 0, dy = 0, dz = 0;
         offs<ST>(d, dx, dy, dz);
-        const double a = ld_stream(sp.bands + (int64_t)d * sp.N + n);
-        const double xv = __ldg(sp.x + zo[dz + 1] + yo[dy + 1] + xo[dx + 1]);
-        if (d == 0) {
-          a0 = a;
-          x0 = xv;
+        const Vec<VEC> a = ldv_stream<VEC>(sp.bands + (int64_t)d * sp.N + n);
+        const Vec<VEC>& c = xc[dy + 1][dz + 1];
+#pragma unroll
+        for (int t = 0; t < VEC; ++t) {
+          double xv;
+          if (dx == 0) xv = c.v[t];
+          else if (dx < 0) xv = (t == 0) ? xl[dy + 1][dz + 1] : c.v[t - 1];
+          else xv = (t == VEC - 1) ? xr[dy + 1][dz + 1] : c.v[t + 1];
+          if (d == 0) a0[t] = a.v[t];
+          y[t] = fma(a.v[t], xv, y[t]);
         }
-        y = fma(a, xv, y);
       }
-      if (MODE == SM_SPMV) {
-        sp.out0[n] = y;
-      } else if (MODE == SM_SPMV_SWEEP1) {
-        sp.out0[n] = y;
-        sp.out1[n] = sp.omega * y / a0;
-      } else if (MODE == SM_SWEEP || MODE == SM_SWEEP_NORM) {
-        const double z = x0 + sp.omega * (__ldg(sp.r + n) - y) / a0;
-        sp.out0[n] = z;
-        if (MODE == SM_SWEEP_NORM) red[0] = fma(z, z, red[0]);
+      const Vec<VEC>& x0 = xc[1][1];
+      Vec<VEC> o0, o1;
+      if constexpr (MODE == SM_SPMV) {
+#pragma unroll
+        for (int t = 0; t < VEC; ++t) o0.v[t] = y[t];
+        stv<VEC>(sp.out0 + n, o0);
+      } else if constexpr (MODE == SM_SPMV_SWEEP1) {
+#pragma unroll
+        for (int t = 0; t < VEC; ++t) {
+          o0.v[t] = y[t];
+          o1.v[t] = sp.omega * y[t] / a0[t];
+        }
+        stv<VEC>(sp.out0 + n, o0);
+        stv<VEC>(sp.out1 + n, o1);
+      } else if constexpr (MODE == SM_SWEEP || MODE == SM_SWEEP_NORM) {
+        const Vec<VEC> r = ldv_ro<VEC>(sp.r + n);
+#pragma unroll
+        for (int t = 0; t < VEC; ++t) {
+          o0.v[t] = x0.v[t] + sp.omega * (r.v[t] - y[t]) / a0[t];
+          if constexpr (MODE == SM_SWEEP_NORM) red[0] = fma(o0.v[t], o0.v[t], red[0]);
+        }
+        stv<VEC>(sp.out0 + n, o0);
       } else {  // residual
-        const double v = __ldg(sp.r + n) - y;
-        sp.out0[n] = v;
-        red[0] = fma(v, v, red[0]);
-        if (MODE == SM_RESID_SWEEP1) sp.out1[n] = sp.omega * v / a0;
+        const Vec<VEC> r = ldv_ro<VEC>(sp.r + n);
+#pragma unroll
+        for (int t = 0; t < VEC; ++t) {
+          o0.v[t] = r.v[t] - y[t];
+          red[0] = fma(o0.v[t], o0.v[t], red[0]);
+          if constexpr (MODE == SM_RESID_SWEEP1) o1.v[t] = sp.omega * o0.v[t] / a0[t];
+        }
+        stv<VEC>(sp.out0 + n, o0);
+        if constexpr (MODE == SM_RESID_SWEEP1) stv<VEC>(sp.out1 + n, o1);
       }
     }
   }
@@ -182,8 +287,8 @@ __global__ void __launch_bounds__(256) stencil_kernel(StencilParams sp) {
 // Truncation check: counts coefficients that reach outside a
 // non-periodic axis and zero diagonals.
 template <int ST>
-__global__ void validate_kernel(const double* bands, int64_t N, int nx, int ny, int nz_local,
-                                int z0, int nz_global, int pmask, unsigned* bad) {
+__global__ void validate_kernel(const double* bands, int64_t N, int nx, int ny, int z0,
+                                int nz_global, int pmask, unsigned* bad) {
   for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < N;
        n += (int64_t)gridDim.x * blockDim.x) {
     const int i = (int)(n % nx);
@@ -192,7 +297,7 @@ __global__ void validate_kernel(const double* bands, int64_t N, int nx, int ny, 
     unsigned cnt = 0;
     if (bands[n] == 0.0) ++cnt;
     for (int d = 1; d < ST; ++d) {
-      int dx, dy, dz;
+      int dx = 0, dy = 0, dz = 0;
       offs<ST>(d, dx, dy, dz);
       bool out = false;
       if (!(pmask & 1) && (i + dx < 0 || i + dx >= nx)) out = true;
@@ -201,47 +306,6 @@ __global__ void validate_kernel(const double* bands, int64_t N, int nx, int ny, 
       if (out && bands[(int64_t)d * N + n] != 0.0) ++cnt;
     }
     if (cnt) atomicAdd(bad, cnt);
-  }
-}
-
-// ------------------------------------------------- vector load helpers
-// VEC = 2: two consecutive rows per thread with 16-byte loads (requires
-// 16-byte aligned columns and even N; checked on the host).
-template <int VEC>
-struct Vec {
-  double v[VEC];
-};
-
-template <int VEC>
-__device__ __forceinline__ Vec<VEC> ldv_stream(const double* p) {
-  Vec<VEC> r;
-  if constexpr (VEC == 2) {
-    asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(r.v[0]), "=d"(r.v[1]) : "l"(p));
-  } else {
-    asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r.v[0]) : "l"(p));
-  }
-  return r;
-}
-
-template <int VEC>
-__device__ __forceinline__ Vec<VEC> ldv(const double* p) {
-  Vec<VEC> r;
-  if constexpr (VEC == 2) {
-    const double2 t = *reinterpret_cast<const double2*>(p);
-    r.v[0] = t.x;
-    r.v[1] = t.y;
-  } else {
-    r.v[0] = *p;
-  }
-  return r;
-}
-
-template <int VEC>
-__device__ __forceinline__ void stv(double* p, const Vec<VEC>& a) {
-  if constexpr (VEC == 2) {
-    *reinterpret_cast<double2*>(p) = make_double2(a.v[0], a.v[1]);
-  } else {
-    *p = a.v[0];
   }
 }
 
@@ -263,7 +327,7 @@ __global__ void __launch_bounds__(256) bdot_kernel(ColPtrs Q, int ncol, const do
   const int64_t NE = N / VEC;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < NE; e += stride) {
     const int64_t r = e * VEC;
-    const Vec<VEC> wv = ldv<VEC>(w + r);
+    const Vec<VEC> wv = ldv_ro<VEC>(w + r);
 #pragma unroll
     for (int g = 0; g < NC / GRP; ++g) {
       if (g * GRP < ncol) {
@@ -316,7 +380,7 @@ __global__ void __launch_bounds__(256) bupd_kernel(ColPtrs Q, int ncol, const do
 #pragma unroll
     for (int q = 0; q < ND; ++q) {
       Vec<VEC> o = wv;
-      if (dv[q]) o = ldv<VEC>(dv[q] + r);
+      if (dv[q]) o = ldv_ro<VEC>(dv[q] + r);
 #pragma unroll
       for (int t = 0; t < VEC; ++t) acc[q] = fma(o.v[t], wv.v[t], acc[q]);
     }
@@ -326,14 +390,21 @@ __global__ void __launch_bounds__(256) bupd_kernel(ColPtrs Q, int ncol, const do
 
 // v_{j+1} = w / h_{j+1,j}, with the happy-breakdown test h <= 1e-14 ||A_hat v_j||
 // (reading D18): on breakdown v_{j+1} = 0 and *flag = 1.
-__global__ void normalize_kernel(double* __restrict__ w, int64_t N, const double* nrm2,
-                                 const double* nin2, double* flag) {
+template <int VEC>
+__global__ void __launch_bounds__(256) normalize_kernel(double* __restrict__ w, int64_t N,
+                                                        const double* nrm2, const double* nin2,
+                                                        double* flag) {
   const double h = sqrt(*nrm2);
   bool brk = false;
   if (nin2) brk = !(h > 1e-14 * sqrt(*nin2));
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < N; r += stride)
-    w[r] = brk ? 0.0 : w[r] / h;
+  const int64_t NE = N / VEC;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < NE; e += stride) {
+    Vec<VEC> v = ldv<VEC>(w + e * VEC);
+#pragma unroll
+    for (int t = 0; t < VEC; ++t) v.v[t] = brk ? 0.0 : v.v[t] / h;
+    stv<VEC>(w + e * VEC, v);
+  }
   if (flag && blockIdx.x == 0 && threadIdx.x == 0) *flag = brk ? 1.0 : 0.0;
 }
 
@@ -476,7 +547,8 @@ __global__ void __launch_bounds__(256) rotate_kernel(ColPtrs Qc, int k, const do
 // ------------------------------------------------------------ K6 rBiCGStab
 // Alg. 4 line 6 fused with the first Jacobi sweep of p_hat = M^-1 p:
 // p = r (i = 0) or p = r + beta (p - omega v), beta = (rho_i/rho_{i-1})(alpha/omega);
-// z = w_l p / D.
+// z = w_l p / D (D == nullptr: no preconditioner, z = p).
+template <int VEC>
 __global__ void __launch_bounds__(256) bicg_p_kernel(const double* __restrict__ r, double* __restrict__ p,
                                                      const double* __restrict__ v, const double* __restrict__ D,
                                                      double* __restrict__ z, double wl, int64_t N,
@@ -488,16 +560,33 @@ __global__ void __launch_bounds__(256) bicg_p_kernel(const double* __restrict__ 
     beta = (cur->rho / prev->rho) * (alpha / omega);
   }
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; n < N; n += stride) {
-    const double rn = __ldg(r + n);
-    const double pn = first ? rn : rn + beta * (p[n] - omega * __ldg(v + n));
-    p[n] = pn;
-    z[n] = D ? wl * pn / ld_stream(D + n) : pn;
+  const int64_t NE = N / VEC;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < NE; e += stride) {
+    const int64_t n = e * VEC;
+    const Vec<VEC> rn = ldv_ro<VEC>(r + n);
+    Vec<VEC> pn;
+    if (first) {
+      pn = rn;
+    } else {
+      const Vec<VEC> po = ldv<VEC>(p + n);
+      const Vec<VEC> vn = ldv_ro<VEC>(v + n);
+#pragma unroll
+      for (int t = 0; t < VEC; ++t) pn.v[t] = rn.v[t] + beta * (po.v[t] - omega * vn.v[t]);
+    }
+    stv<VEC>(p + n, pn);
+    Vec<VEC> zn = pn;
+    if (D) {
+      const Vec<VEC> dn = ldv_stream<VEC>(D + n);
+#pragma unroll
+      for (int t = 0; t < VEC; ++t) zn.v[t] = wl * pn.v[t] / dn.v[t];
+    }
+    stv<VEC>(z + n, zn);
   }
 }
 
 // Alg. 4 line 8 fused with the first sweep of s_hat = M^-1 s:
 // alpha = rho/sigma; s = r - alpha v; z = w_l s / D; red ||s||^2.
+template <int VEC>
 __global__ void __launch_bounds__(256) bicg_s_kernel(const double* __restrict__ r, const double* __restrict__ v,
                                                      double* __restrict__ s, const double* __restrict__ D,
                                                      double* __restrict__ z, double wl, int64_t N,
@@ -505,11 +594,25 @@ __global__ void __launch_bounds__(256) bicg_s_kernel(const double* __restrict__ 
   const double alpha = cur->rho / cur->sigma;
   double acc[1] = {0.0};
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; n < N; n += stride) {
-    const double sn = __ldg(r + n) - alpha * __ldg(v + n);
-    s[n] = sn;
-    z[n] = D ? wl * sn / ld_stream(D + n) : sn;
-    acc[0] = fma(sn, sn, acc[0]);
+  const int64_t NE = N / VEC;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < NE; e += stride) {
+    const int64_t n = e * VEC;
+    const Vec<VEC> rn = ldv_ro<VEC>(r + n);
+    const Vec<VEC> vn = ldv_ro<VEC>(v + n);
+    Vec<VEC> sn, zn;
+#pragma unroll
+    for (int t = 0; t < VEC; ++t) {
+      sn.v[t] = rn.v[t] - alpha * vn.v[t];
+      acc[0] = fma(sn.v[t], sn.v[t], acc[0]);
+    }
+    stv<VEC>(s + n, sn);
+    zn = sn;
+    if (D) {
+      const Vec<VEC> dn = ldv_stream<VEC>(D + n);
+#pragma unroll
+      for (int t = 0; t < VEC; ++t) zn.v[t] = wl * sn.v[t] / dn.v[t];
+    }
+    stv<VEC>(z + n, zn);
   }
   block_reduce_store<1>(acc, 1, ra);
 }
@@ -518,6 +621,7 @@ __global__ void __launch_bounds__(256) bicg_s_kernel(const double* __restrict__ 
 // reading D17 evaluated on the device so a breakdown never touches x:
 // x += alpha p_hat + omega s_hat ; r = s - omega t ; xi += alpha eta1 + omega eta2 ;
 // red (r~^T r, ||r||^2) -> next->rho, next->rr.
+template <int VEC>
 __global__ void __launch_bounds__(256) bicg_xr_kernel(double* __restrict__ x, double* __restrict__ r,
                                                       const double* __restrict__ s, const double* __restrict__ t,
                                                       const double* __restrict__ ph, const double* __restrict__ sh,
@@ -533,21 +637,38 @@ __global__ void __launch_bounds__(256) bicg_xr_kernel(double* __restrict__ x, do
   else mode = 0;
   double acc[2] = {0.0, 0.0};
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; n < N; n += stride) {
-    double rn;
+  const int64_t NE = N / VEC;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < NE; e += stride) {
+    const int64_t n = e * VEC;
+    Vec<VEC> rn;
     if (mode == 0) {
-      x[n] = x[n] + alpha * __ldg(ph + n) + omega * __ldg(sh + n);
-      rn = __ldg(s + n) - omega * __ldg(t + n);
-      r[n] = rn;
+      Vec<VEC> xn = ldv<VEC>(x + n);
+      const Vec<VEC> pn = ldv_ro<VEC>(ph + n), sn = ldv_ro<VEC>(sh + n);
+      const Vec<VEC> s0 = ldv_ro<VEC>(s + n), t0 = ldv_ro<VEC>(t + n);
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) {
+        xn.v[q] = xn.v[q] + alpha * pn.v[q] + omega * sn.v[q];
+        rn.v[q] = s0.v[q] - omega * t0.v[q];
+      }
+      stv<VEC>(x + n, xn);
+      stv<VEC>(r + n, rn);
     } else if (mode == 1) {
-      x[n] = x[n] + alpha * __ldg(ph + n);
-      rn = __ldg(s + n);
-      r[n] = rn;
+      Vec<VEC> xn = ldv<VEC>(x + n);
+      const Vec<VEC> pn = ldv_ro<VEC>(ph + n);
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) xn.v[q] = xn.v[q] + alpha * pn.v[q];
+      stv<VEC>(x + n, xn);
+      rn = ldv_ro<VEC>(s + n);
+      stv<VEC>(r + n, rn);
     } else {
-      rn = r[n];
+      rn = ldv<VEC>(r + n);
     }
-    acc[0] = fma(__ldg(rt + n), rn, acc[0]);
-    acc[1] = fma(rn, rn, acc[1]);
+    const Vec<VEC> rtn = ldv_ro<VEC>(rt + n);
+#pragma unroll
+    for (int q = 0; q < VEC; ++q) {
+      acc[0] = fma(rtn.v[q], rn.v[q], acc[0]);
+      acc[1] = fma(rn.v[q], rn.v[q], acc[1]);
+    }
   }
   if (blockIdx.x == 0) {
     for (int c = threadIdx.x; c < k; c += blockDim.x) {
@@ -601,39 +722,62 @@ struct Launch {
   }
 };
 
-inline RedArgs red_args(rk_ctx* ctx, double* out, int nval, int grid) {
-  RK_REQUIRE((size_t)nval * grid <= ctx->partials_cap, RK_ESTATE, "reduction scratch too small");
+// Grid = min(work / CTA, SMs x resident CTAs of this instantiation).
+template <typename... KArgs, typename... Args>
+void launch_k(rk_ctx* ctx, void (*kern)(KArgs...), int64_t work_threads, dim3 blk,
+              Args&&... args) {
+  const int threads = (int)(blk.x * blk.y);
+  auto it = ctx->occ_cache.find((const void*)kern);
+  int occ;
+  if (it == ctx->occ_cache.end()) {
+    RK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, 0));
+    occ = std::max(1, occ);
+    ctx->occ_cache[(const void*)kern] = occ;
+  } else {
+    occ = it->second;
+  }
+  const int64_t want = std::max<int64_t>(1, (work_threads + threads - 1) / threads);
+  const int grid = (int)std::min<int64_t>(want, (int64_t)ctx->sms * occ);
+  kern<<<grid, blk, 0, ctx->stream>>>(std::forward<Args>(args)...);
+}
+
+inline RedArgs red_args(rk_ctx* ctx, double* out) {
   return RedArgs{ctx->partials, ctx->counter, out};
 }
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// VEC = 2 iff N is even and every pointer is 16-byte aligned.
+int pick_vec(int64_t N, std::initializer_list<const void*> ps,
+             const std::vector<const double*>& cols = {}) {
+  if (N & 1) return 1;
+  for (auto p : ps)
+    if (p && !aligned16(p)) return 1;
+  for (auto p : cols)
+    if (p && !aligned16(p)) return 1;
+  return 2;
+}
+
+// Pad to a multiple of GRP with the first column of the last group.
+ColPtrs make_cols_padded(const std::vector<const double*>& v, int nc) {
+  ColPtrs c;
+  memset(&c, 0, sizeof(c));
+  for (size_t i = 0; i < v.size(); ++i) c.p[i] = v[i];
+  for (int i = (int)v.size(); i < nc && !v.empty(); ++i) {
+    const int g0 = (i / GRP) * GRP;
+    c.p[i] = v[g0 < (int)v.size() ? g0 : 0];
+  }
+  return c;
+}
+
+inline int nc_round(int n) { return ((std::max(n, 1) + GRP - 1) / GRP) * GRP; }
 
 inline int nc_bucket(int n) {
   if (n <= 8) return 8;
   if (n <= 16) return 16;
   if (n <= 32) return 32;
-  if (n <= 48) return 48;
-  if (n <= 64) return 64;
-  RK_REQUIRE(n <= MAXCOL, RK_EINVAL, "too many columns in a block product");
-  return 80;
-}
-
-
-template <int ST, int MODE>
-void launch_stencil(rk_op* op, const StencilParams& sp, dim3 blk, int grid) {
-  stencil_kernel<ST, MODE><<<grid, blk, 0, op->ctx->stream>>>(sp);
-}
-
-template <int ST>
-void stencil_dispatch(rk_op* op, int mode, const StencilParams& sp, dim3 blk, int grid) {
-  switch (mode) {
-    case SM_SPMV: launch_stencil<ST, SM_SPMV>(op, sp, blk, grid); break;
-    case SM_SPMV_SWEEP1: launch_stencil<ST, SM_SPMV_SWEEP1>(op, sp, blk, grid); break;
-    case SM_SWEEP: launch_stencil<ST, SM_SWEEP>(op, sp, blk, grid); break;
-    case SM_SWEEP_NORM: launch_stencil<ST, SM_SWEEP_NORM>(op, sp, blk, grid); break;
-    case SM_RESID: launch_stencil<ST, SM_RESID>(op, sp, blk, grid); break;
-    case SM_RESID_SWEEP1: launch_stencil<ST, SM_RESID_SWEEP1>(op, sp, blk, grid); break;
-    case SM_SCALE: launch_stencil<ST, SM_SCALE>(op, sp, blk, grid); break;
-    default: throw Error(RK_EINVAL, "bad stencil mode");
-  }
+  RK_REQUIRE(n <= 48, RK_EINVAL, "rotation supports k <= 48");
+  return 48;
 }
 
 const char* stencil_cls(int mode) {
@@ -661,20 +805,34 @@ double stencil_words(int S, int mode) {
   }
 }
 
+template <int ST, int MODE>
+void stencil_launch(rk_op* op, const StencilParams& sp, int vec, int64_t work, dim3 blk) {
+  if (vec == 2) launch_k(op->ctx, stencil_kernel<ST, MODE, 2>, work, blk, sp);
+  else launch_k(op->ctx, stencil_kernel<ST, MODE, 1>, work, blk, sp);
+}
+
+template <int ST>
+void stencil_dispatch(rk_op* op, int mode, const StencilParams& sp, int vec, int64_t work, dim3 blk) {
+  switch (mode) {
+    case SM_SPMV: stencil_launch<ST, SM_SPMV>(op, sp, vec, work, blk); break;
+    case SM_SPMV_SWEEP1: stencil_launch<ST, SM_SPMV_SWEEP1>(op, sp, vec, work, blk); break;
+    case SM_SWEEP: stencil_launch<ST, SM_SWEEP>(op, sp, vec, work, blk); break;
+    case SM_SWEEP_NORM: stencil_launch<ST, SM_SWEEP_NORM>(op, sp, vec, work, blk); break;
+    case SM_RESID: stencil_launch<ST, SM_RESID>(op, sp, vec, work, blk); break;
+    case SM_RESID_SWEEP1: stencil_launch<ST, SM_RESID_SWEEP1>(op, sp, vec, work, blk); break;
+    case SM_SCALE: stencil_launch<ST, SM_SCALE>(op, sp, vec, work, blk); break;
+    default: throw Error(RK_EINVAL, "bad stencil mode");
+  }
+}
+
 }  // namespace
 
 void init_ctx_kernels(rk_ctx* ctx) {
   int sms = 0;
   RK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
   ctx->sms = sms;
-  int occ = 0;
-  RK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stencil_kernel<19, SM_SWEEP>, 256, 0));
-  ctx->grid_stencil = sms * std::max(1, occ);
-  RK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bupd_kernel<32, 1, 2>, 256, 0));
-  ctx->grid_blas = sms * std::max(1, std::min(occ, 4));
-  // partial sums: up to MAXCOL values for up to max(grid) CTAs
-  const int gmax = std::max(ctx->grid_stencil, ctx->grid_blas * 2);
-  ctx->partials_cap = (size_t)(MAXCOL + 4) * gmax;
+  // per-CTA partials for up to MAXCOL + 4 values, up to 8 resident 256-thread CTAs per SM
+  ctx->partials_cap = (size_t)(MAXCOL + 4) * sms * 8;
   RK_CUDA(cudaMalloc(&ctx->partials, ctx->partials_cap * sizeof(double)));
   RK_CUDA(cudaMalloc(&ctx->counter, 64));
   RK_CUDA(cudaMemset(ctx->counter, 0, 64));
@@ -699,18 +857,20 @@ void stencil(rk_op* op, int mode, const double* x, const double* r, double* out0
   sp.out0 = out0;
   sp.out1 = out1;
   sp.omega = omega;
-  int bx = sp.nx >= 128 ? 128 : (sp.nx > 32 ? ((sp.nx + 31) / 32) * 32 : 32);
-  if (bx > 128) bx = 128;
+  const bool red = (mode == SM_SWEEP_NORM || mode == SM_RESID || mode == SM_RESID_SWEEP1);
+  sp.red = red ? red_args(ctx, red_out) : RedArgs{nullptr, nullptr, nullptr};
+  // VEC = 2 needs even rows and 16-byte aligned rows of every array
+  int vec = (sp.nx % 2 == 0 && op->P % 2 == 0) ? pick_vec(op->N, {op->bands, x, r, out0, out1}) : 1;
+  const int nxv = sp.nx / vec;
+  const int bx = nxv >= 128 ? 128 : ((nxv + 31) / 32) * 32;
   dim3 blk(bx, 256 / bx);
   const int64_t rows = (int64_t)sp.ny * sp.nzl;
-  int grid = (int)std::min<int64_t>((rows + blk.y - 1) / blk.y, ctx->grid_stencil);
-  const bool red = (mode == SM_SWEEP_NORM || mode == SM_RESID || mode == SM_RESID_SWEEP1);
-  sp.red = red ? red_args(ctx, red_out, 1, grid) : RedArgs{nullptr, nullptr, nullptr};
+  const int64_t work = ((rows + blk.y - 1) / blk.y) * 256;
   Launch L(ctx, stencil_cls(mode), 8.0 * op->N * stencil_words(op->S, mode));
   switch (op->S) {
-    case 7: stencil_dispatch<7>(op, mode, sp, blk, grid); break;
-    case 19: stencil_dispatch<19>(op, mode, sp, blk, grid); break;
-    case 27: stencil_dispatch<27>(op, mode, sp, blk, grid); break;
+    case 7: stencil_dispatch<7>(op, mode, sp, vec, work, blk); break;
+    case 19: stencil_dispatch<19>(op, mode, sp, vec, work, blk); break;
+    case 27: stencil_dispatch<27>(op, mode, sp, vec, work, blk); break;
     default: throw Error(RK_EINVAL, "unsupported stencil");
   }
   L.done();
@@ -726,8 +886,8 @@ int validate_bands(rk_op* op) {
   Launch L(ctx, "validate", 0);
 #define RK_VAL(STV)                                                                              \
   validate_kernel<STV><<<grid, 256, 0, ctx->stream>>>(op->bands, op->N, (int)op->g.nx,          \
-                                                      (int)op->g.ny, (int)op->g.nz_local,       \
-                                                      (int)op->g.z0, (int)op->g.nz_global,      \
+                                                      (int)op->g.ny, (int)op->g.z0,             \
+                                                      (int)op->g.nz_global,                     \
                                                       (int)op->g.periodic_mask, bad)
   if (op->S == 7) RK_VAL(7);
   else if (op->S == 19) RK_VAL(19);
@@ -741,34 +901,6 @@ int validate_bands(rk_op* op) {
   return (int)h;
 }
 
-namespace {
-
-bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
-
-// VEC = 2 iff N is even and every pointer is 16-byte aligned.
-int pick_vec(int64_t N, std::initializer_list<const void*> ps,
-             const std::vector<const double*>& cols = {}) {
-  if (N & 1) return 1;
-  for (auto p : ps)
-    if (p && !aligned16(p)) return 1;
-  for (auto p : cols)
-    if (p && !aligned16(p)) return 1;
-  return 2;
-}
-
-// Pad to a multiple of GRP with the first column of the last group.
-ColPtrs make_cols_padded(const std::vector<const double*>& v, int nc) {
-  ColPtrs c;
-  memset(&c, 0, sizeof(c));
-  for (size_t i = 0; i < v.size(); ++i) c.p[i] = v[i];
-  for (int i = (int)v.size(); i < nc && !v.empty(); ++i) c.p[i] = v[(i / GRP) * GRP < (int)v.size() ? (i / GRP) * GRP : 0];
-  return c;
-}
-
-inline int nc_round(int n) { return ((std::max(n, 1) + GRP - 1) / GRP) * GRP; }
-
-}  // namespace
-
 // bdot launches cover <= 40 columns each (register budget: 40 accumulators).
 void bdot(rk_ctx* ctx, const std::vector<const double*>& cols_all, const double* w, int64_t N,
           double* out) {
@@ -780,13 +912,13 @@ void bdot(rk_ctx* ctx, const std::vector<const double*>& cols_all, const double*
     const int ncol = (int)cols.size();
     const int nc = nc_round(ncol);
     const int vec = pick_vec(N, {w}, cols);
-    const int grid = ctx->grid_blas;
-    RedArgs ra = red_args(ctx, out + off, ncol, grid);
+    RedArgs ra = red_args(ctx, out + off);
     ColPtrs Q = make_cols_padded(cols, nc);
+    const int64_t work = N / vec;
     Launch L(ctx, "bdot", 8.0 * N * (ncol + 1));
 #define RK_BDOT(NCV)                                                                     \
-  if (vec == 2) bdot_kernel<NCV, 2><<<grid, 256, 0, ctx->stream>>>(Q, ncol, w, N, ra);   \
-  else bdot_kernel<NCV, 1><<<grid, 256, 0, ctx->stream>>>(Q, ncol, w, N, ra);
+  if (vec == 2) launch_k(ctx, bdot_kernel<NCV, 2>, work, dim3(256), Q, ncol, w, N, ra);  \
+  else launch_k(ctx, bdot_kernel<NCV, 1>, work, dim3(256), Q, ncol, w, N, ra);
     switch (nc) {
       case 8: RK_BDOT(8); break;
       case 16: RK_BDOT(16); break;
@@ -809,21 +941,21 @@ void bupd(rk_ctx* ctx, const std::vector<const double*>& cols, const double* g, 
   const int nc = nc_round(ncol);
   const int vec = pick_vec(N, {w, nd > 0 ? dots[0] : nullptr, nd > 1 ? dots[1] : nullptr,
                                nd > 2 ? dots[2] : nullptr}, cols);
-  const int grid = ctx->grid_blas;
-  RedArgs ra = nd ? red_args(ctx, red_out, nd, grid) : RedArgs{nullptr, nullptr, nullptr};
+  RedArgs ra = nd ? red_args(ctx, red_out) : RedArgs{nullptr, nullptr, nullptr};
   ColPtrs Q = make_cols_padded(cols, nc);
   const double* d[3] = {nullptr, nullptr, nullptr};
   for (int q = 0; q < nd; ++q) d[q] = dots[q];
   double words = ncol + 2;
   for (int q = 0; q < nd; ++q) words += dots[q] ? 1 : 0;
+  const int64_t work = N / vec;
   Launch L(ctx, "bupd", 8.0 * N * words);
-#define RK_BUPD(NCV, NDV)                                                                        \
-  if (vec == 2)                                                                                  \
-    bupd_kernel<NCV, NDV, 2><<<grid, 256, 0, ctx->stream>>>(Q, ncol, g, gscale, w, N, d[0], d[1], \
-                                                            d[2], ra);                            \
-  else                                                                                           \
-    bupd_kernel<NCV, NDV, 1><<<grid, 256, 0, ctx->stream>>>(Q, ncol, g, gscale, w, N, d[0], d[1], \
-                                                            d[2], ra);
+#define RK_BUPD(NCV, NDV)                                                                      \
+  if (vec == 2)                                                                                \
+    launch_k(ctx, bupd_kernel<NCV, NDV, 2>, work, dim3(256), Q, ncol, g, gscale, w, N, d[0],   \
+             d[1], d[2], ra);                                                                  \
+  else                                                                                         \
+    launch_k(ctx, bupd_kernel<NCV, NDV, 1>, work, dim3(256), Q, ncol, g, gscale, w, N, d[0],   \
+             d[1], d[2], ra);
 #define RK_BUPD_NC(NCV)               \
   switch (nd) {                       \
     case 0: RK_BUPD(NCV, 0); break;   \
@@ -851,8 +983,10 @@ void bupd(rk_ctx* ctx, const std::vector<const double*>& cols, const double* g, 
 
 void normalize(rk_ctx* ctx, double* w, int64_t N, const double* nrm2, const double* nin2,
                double* flag) {
+  const int vec = pick_vec(N, {w});
   Launch L(ctx, "normalize", 16.0 * N);
-  normalize_kernel<<<ctx->grid_blas, 256, 0, ctx->stream>>>(w, N, nrm2, nin2, flag);
+  if (vec == 2) launch_k(ctx, normalize_kernel<2>, N / 2, dim3(256), w, N, nrm2, nin2, flag);
+  else launch_k(ctx, normalize_kernel<1>, N, dim3(256), w, N, nrm2, nin2, flag);
   L.done();
 }
 
@@ -868,11 +1002,11 @@ void lincomb(rk_ctx* ctx, const std::vector<const double*>& cols, const double* 
     if (!aligned16(lo.out[o])) vec = 1;
   double words = ncol;
   for (int o = 0; o < nout; ++o) words += lo.acc[o] ? 2 : 1;
-  const int grid = ctx->grid_blas;
+  const int64_t work = N / vec;
   Launch L(ctx, "lincomb", 8.0 * N * words);
-#define RK_LC(NCV)                                                                           \
-  if (vec == 2) lincomb_kernel<NCV, 2><<<grid, 256, 0, ctx->stream>>>(Q, ncol, coef, nout, lo, N); \
-  else lincomb_kernel<NCV, 1><<<grid, 256, 0, ctx->stream>>>(Q, ncol, coef, nout, lo, N);
+#define RK_LC(NCV)                                                                              \
+  if (vec == 2) launch_k(ctx, lincomb_kernel<NCV, 2>, work, dim3(256), Q, ncol, coef, nout, lo, N); \
+  else launch_k(ctx, lincomb_kernel<NCV, 1>, work, dim3(256), Q, ncol, coef, nout, lo, N);
   switch (nc) {
     case 8: RK_LC(8); break;
     case 16: RK_LC(16); break;
@@ -894,15 +1028,15 @@ void proj(rk_ctx* ctx, const std::vector<const double*>& C, const std::vector<co
   const int k = (int)C.size();
   RK_REQUIRE(k >= 1 && k <= 48, RK_EINVAL, "projection supports 1 <= k <= 48");
   const int nc = nc_round(k);
-  const int grid = ctx->grid_blas;
-  RedArgs ra = red_args(ctx, red_out, 1, grid);
+  RedArgs ra = red_args(ctx, red_out);
   ColPtrs Cp = make_cols_padded(C, nc), Up = make_cols_padded(U, nc);
   int vec = pick_vec(N, {r, x}, C);
   if (x && pick_vec(N, {}, U) == 1) vec = 1;
+  const int64_t work = N / vec;
   Launch L(ctx, "proj", 8.0 * N * (k * (x ? 2 : 1) + 2 + (x ? 2 : 0)));
-#define RK_PJ(NCV)                                                                           \
-  if (vec == 2) proj_kernel<NCV, 2><<<grid, 256, 0, ctx->stream>>>(Cp, Up, k, xi, r, x, N, ra); \
-  else proj_kernel<NCV, 1><<<grid, 256, 0, ctx->stream>>>(Cp, Up, k, xi, r, x, N, ra);
+#define RK_PJ(NCV)                                                                               \
+  if (vec == 2) launch_k(ctx, proj_kernel<NCV, 2>, work, dim3(256), Cp, Up, k, xi, r, x, N, ra); \
+  else launch_k(ctx, proj_kernel<NCV, 1>, work, dim3(256), Cp, Up, k, xi, r, x, N, ra);
   switch (nc) {
     case 8: RK_PJ(8); break;
     case 16: RK_PJ(16); break;
@@ -920,17 +1054,15 @@ void rotate(rk_ctx* ctx, const std::vector<double*>& cols, const double* T, int6
   const int k = (int)cols.size();
   if (k == 0) return;
   const int nc = nc_bucket(k);
-  RK_REQUIRE(nc <= 48, RK_EINVAL, "rotation supports k <= 48");
   ColPtrs Q;
   memset(&Q, 0, sizeof(Q));
   for (int c = 0; c < k; ++c) Q.p[c] = cols[c];
-  const int grid = ctx->grid_blas;
   Launch L(ctx, "rotate", 16.0 * N * k);
   switch (nc) {
-    case 8: rotate_kernel<8><<<grid, 256, 0, ctx->stream>>>(Q, k, T, N); break;
-    case 16: rotate_kernel<16><<<grid, 256, 0, ctx->stream>>>(Q, k, T, N); break;
-    case 32: rotate_kernel<32><<<grid, 256, 0, ctx->stream>>>(Q, k, T, N); break;
-    default: rotate_kernel<48><<<grid, 256, 0, ctx->stream>>>(Q, k, T, N); break;
+    case 8: launch_k(ctx, rotate_kernel<8>, N, dim3(256), Q, k, T, N); break;
+    case 16: launch_k(ctx, rotate_kernel<16>, N, dim3(256), Q, k, T, N); break;
+    case 32: launch_k(ctx, rotate_kernel<32>, N, dim3(256), Q, k, T, N); break;
+    default: launch_k(ctx, rotate_kernel<48>, N, dim3(256), Q, k, T, N); break;
   }
   L.done();
 }
@@ -938,20 +1070,29 @@ void rotate(rk_ctx* ctx, const std::vector<double*>& cols, const double* T, int6
 void bicg_p(rk_op* op, const double* r, double* p, const double* v, double* z, double wl,
             bool jacobi, const BiIter* cur, const BiIter* prev, int first) {
   rk_ctx* ctx = op->ctx;
+  const double* D = jacobi ? op->bands : nullptr;
+  const int vec = pick_vec(op->N, {r, p, v, z, D});
   Launch L(ctx, "bicg_p", 8.0 * op->N * ((first ? 3 : 5) + (jacobi ? 1 : 0)));
-  bicg_p_kernel<<<ctx->grid_blas, 256, 0, ctx->stream>>>(r, p, v, jacobi ? op->bands : nullptr, z,
-                                                          wl, op->N, cur, prev, first);
+  if (vec == 2)
+    launch_k(ctx, bicg_p_kernel<2>, op->N / 2, dim3(256), r, p, v, D, z, wl, op->N, cur, prev, first);
+  else
+    launch_k(ctx, bicg_p_kernel<1>, op->N, dim3(256), r, p, v, D, z, wl, op->N, cur, prev, first);
   L.done();
 }
 
 void bicg_s(rk_op* op, const double* r, const double* v, double* s, double* z, double wl,
             bool jacobi, BiIter* cur) {
   rk_ctx* ctx = op->ctx;
-  const int grid = ctx->grid_blas;
-  RedArgs ra = red_args(ctx, &cur->ss, 1, grid);
-  Launch L(ctx, "bicg_s", 8.0 * op->N * (jacobi ? 5 : 3));
-  bicg_s_kernel<<<grid, 256, 0, ctx->stream>>>(r, v, s, jacobi ? op->bands : nullptr, z, wl, op->N,
-                                               cur, ra);
+  const double* D = jacobi ? op->bands : nullptr;
+  RedArgs ra = red_args(ctx, &cur->ss);
+  const int vec = pick_vec(op->N, {r, v, s, z, D});
+  Launch L(ctx, "bicg_s", 8.0 * op->N * (jacobi ? 5 : 4));
+  if (vec == 2)
+    launch_k(ctx, bicg_s_kernel<2>, op->N / 2, dim3(256), r, v, s, D, z, wl, op->N,
+             (const BiIter*)cur, ra);
+  else
+    launch_k(ctx, bicg_s_kernel<1>, op->N, dim3(256), r, v, s, D, z, wl, op->N,
+             (const BiIter*)cur, ra);
   L.done();
   allreduce(ctx, &cur->ss, 1);
 }
@@ -959,11 +1100,15 @@ void bicg_s(rk_op* op, const double* r, const double* v, double* s, double* z, d
 void bicg_xr(rk_ctx* ctx, double* x, double* r, const double* s, const double* t, const double* ph,
              const double* sh, const double* rt, int64_t N, BiIter* cur, BiIter* next, double* xi,
              const double* eta1, const double* eta2, int k) {
-  const int grid = ctx->grid_blas;
-  RedArgs ra = red_args(ctx, &next->rho, 2, grid);
+  RedArgs ra = red_args(ctx, &next->rho);
+  const int vec = pick_vec(N, {x, r, s, t, ph, sh, rt});
   Launch L(ctx, "bicg_xr", 8.0 * N * 8);
-  bicg_xr_kernel<<<grid, 256, 0, ctx->stream>>>(x, r, s, t, ph, sh, rt, N, cur, xi, eta1, eta2,
-                                                 k, ra);
+  if (vec == 2)
+    launch_k(ctx, bicg_xr_kernel<2>, N / 2, dim3(256), x, r, s, t, ph, sh, rt, N, cur, xi, eta1,
+             eta2, k, ra);
+  else
+    launch_k(ctx, bicg_xr_kernel<1>, N, dim3(256), x, r, s, t, ph, sh, rt, N, cur, xi, eta1,
+             eta2, k, ra);
   L.done();
   allreduce(ctx, &next->rho, 2);
 }

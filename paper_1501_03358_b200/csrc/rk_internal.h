@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <map>
 #include <stdexcept>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -122,8 +123,8 @@ struct rk_ctx {
 #ifdef RK_WITH_NCCL
   ncclComm_t comm = nullptr;
 #endif
-  // grid sizes per kernel family (multiples of the SM count)
-  int grid_stencil = 0, grid_blas = 0;
+  // resident CTAs per SM of each kernel instantiation (grid = SMs x occupancy)
+  std::unordered_map<const void*, int> occ_cache;
 };
 
 struct rk_op {
