@@ -1,0 +1,502 @@
+// Temporally blocked preconditioned-operator chain (K1 + K2 fused), fed by TMA.
+//
+// The left-preconditioned operator of rGCROT (t = A v, then the Jacobi(5+1)
+// sweeps z <- z + w D^-1 (t - A z)) and the right-
+// preconditioned application of rBiCGStab (p_hat = M^-1 p by the sweeps, then
+// v = A p_hat) are chains of 6 stencil stages over the SAME bands.  One stage
+// per launch streams the S bands from HBM six times (~(S+3) W per stage).
+// Here NST consecutive stages run in one launch:
+//  * the grid tiles x-y (CTX x CTY interior + an (NST-1)-cell halo that is
+//    recomputed) and chunks z; each CTA marches through its z range;
+//  * stage s computes plane tau - s at step tau (a wavefront in z) and keeps
+//    the three most recent planes of its output in a shared-memory ring that
+//    stage s+1 reads;
+//  * thread 0 streams, TWO planes ahead, the band tile, the sweep right-hand
+//    side tile and the input tile (+1 halo) of each plane into a shared-memory
+//    slot ring with cp.async.bulk.tensor (TMA), completion tracked by one
+//    mbarrier per slot; out-of-grid boxes are zero-filled by TMA, which is
+//    exactly the zero-ghost semantics of non-periodic boundaries.
+// Every band coefficient therefore crosses HBM once per NST stages: ~(S + 4)
+// W per launch instead of NST (S + 3) W.  The per-cell arithmetic (FMA order,
+// the division by D) is that of stencil_kernel, so the fused and unfused
+// paths agree bit for bit.
+//
+// Scope: 7-point operators whose x and y axes are not periodic (the porous
+// configs c1, c3, c5) on one rank; everything else uses the unfused path.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "rk_internal.h"
+
+namespace rk {
+
+template <int ST>
+__host__ __device__ constexpr void coffs(int d, int& dx, int& dy, int& dz) {
+  constexpr int DX[19] = {0, -1, 1, 0, 0, 0, 0, -1, 1, -1, 1, 0, 0, 0, 0, -1, 1, -1, 1};
+  constexpr int DY[19] = {0, 0, 0, -1, 1, 0, 0, -1, -1, 1, 1, -1, 1, -1, 1, 0, 0, 0, 0};
+  constexpr int DZ[19] = {0, 0, 0, 0, 0, -1, 1, 0, 0, 0, 0, -1, -1, 1, 1, -1, -1, 1, 1};
+  dx = DX[d];
+  dy = DY[d];
+  dz = DZ[d];
+}
+
+constexpr int CTX = 32, CTY = 16;  // interior tile of a chain CTA
+
+// TMA box starts must be 16-byte aligned in the innermost (x) dimension, so
+// every box starts at an even x and the shared-memory rows carry PAD cells.
+// Shared memory: NB = 3 band/rhs buffers (plane phase (q - tau0) mod 3; a
+// plane's bands are read into registers by stage 0 and the buffer is free
+// after that step), NXB = 4 input-tile buffers (planes tau-1 .. tau+2, one
+// mbarrier each), and the (NST-1) x 3-plane stage rings.
+template <int ST, int NST>
+struct ChainGeom {
+  static constexpr int CTY_ = CTY;
+  static constexpr int HALO = NST - 1;
+  static constexpr int EX = CTX + 2 * HALO, EY = CTY + 2 * HALO;     // stage tile (threads)
+  static constexpr int PADB = HALO % 2;                               // band/rhs box starts at gx0 - PADB
+  static constexpr int SX = (EX + PADB + 1) / 2 * 2;                  // band/rhs smem row (even)
+  static constexpr int PADX = (HALO + 1) % 2;                         // input box starts at gx0 - 1 - PADX
+  static constexpr int XX = (EX + 2 + PADX + 1) / 2 * 2, XY = EY + 2; // input tile (+1 halo)
+  static constexpr int NB = 3, NXB = 4;
+  static constexpr int B_BYTES = ST * EY * SX * 8;
+  static constexpr int R_BYTES = EY * SX * 8;
+  static constexpr int X_BYTES = XY * XX * 8;
+  __host__ __device__ static constexpr int al(int b) { return (b + 127) / 128 * 128; }
+  static constexpr int BSLOT = al(B_BYTES) + al(R_BYTES);             // bands + rhs of one plane
+  static constexpr int R_OFF = al(B_BYTES);
+  static constexpr int XSLOT = al(X_BYTES);
+  static constexpr int X_BASE = NB * BSLOT;
+  // guard zones around the rings: edge threads of the branch-free stages read
+  // one row / column beyond their plane (values nobody uses)
+  static constexpr int GUARD = al((EX + 2) * 8);
+  static constexpr int RING_BASE = X_BASE + NXB * XSLOT + GUARD;
+  static constexpr int RING = (NST > 1 ? NST - 1 : 1) * 3 * EY * EX * 8;
+  static constexpr int BAR_BASE = RING_BASE + al(RING) + GUARD;
+  static constexpr int SMEM = BAR_BASE + 128;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity), "r"(1000000u)
+      : "memory");
+  return ok != 0;
+}
+
+// Bounded wait: a TMA that never lands (a descriptor error) traps the kernel
+// (a reported launch failure) instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  for (uint32_t it = 0; !mbar_try(b, parity); ++it)
+    if (it > (1u << 22)) __trap();
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                            int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                            int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
+// One z-step of the chain for loop phase PH = (tau - tau0) mod 3: register
+// sets (bands / rhs / 1/D of the planes stages 0..NST-1 work on), band
+// buffers and ring slots all rotate with PH at compile time.  The code is
+// branch-free per cell: TMA zero-fills every band and input value outside the
+// grid (x/y) and outside [0, nz) (non-periodic z), and the guarded reciprocal
+// 1/D = 0 there, so such cells evaluate to exactly 0 -- the zero-ghost value
+// -- without tests.  Threads outside a stage's shrinking valid region compute
+// values nobody reads.
+template <int ST, int NST, int K0, int K1, int K2, int PH>
+struct ChainStep {
+  using G = ChainGeom<ST, NST>;
+  static constexpr int EX = G::EX, EY = G::EY, XX = G::XX, SX = G::SX, RPL = EY * EX;
+  static constexpr int HALO = G::HALO;
+  static __device__ __forceinline__ void stage0(int tau, bool st_ok, int pl_tau,
+                                                const unsigned char* smem, int x_m1, int x_0, int x_p1,
+                                                double* ring, double (&bnd)[3][ST], double (&rr)[3],
+                                                double (&inv)[3], int64_t cxy, int xoff, int boff,
+                                                int roff, const ChainParams& cp) {
+    constexpr bool LOAD_R = (K0 != CK_SPMV1);
+    const unsigned char* sb = smem + PH * G::BSLOT;
+    const double* bs = reinterpret_cast<const double*>(sb) + boff;
+#pragma unroll
+    for (int d = 0; d < ST; ++d) bnd[PH][d] = bs[d * EY * SX];
+    if (LOAD_R) rr[PH] = reinterpret_cast<const double*>(sb + G::R_OFF)[boff];
+    const double* xm = reinterpret_cast<const double*>(smem + G::X_BASE + x_m1 * G::XSLOT) + xoff;
+    const double* x0 = reinterpret_cast<const double*>(smem + G::X_BASE + x_0 * G::XSLOT) + xoff;
+    const double* xp = reinterpret_cast<const double*>(smem + G::X_BASE + x_p1 * G::XSLOT) + xoff;
+    inv[PH] = bnd[PH][0] != 0.0 ? 1.0 / bnd[PH][0] : 0.0;
+    double ya = 0.0, yb = 0.0, xc = 0.0;
+#pragma unroll
+    for (int d = 0; d < ST; ++d) {
+      int dx = 0, dy = 0, dz = 0;
+      coffs<ST>(d, dx, dy, dz);
+      const double* xt = dz < 0 ? xm : (dz > 0 ? xp : x0);
+      const double xv = xt[dy * XX + dx];
+      if (d == 0) xc = xv;
+      if (d % 2 == 0) ya = fma(bnd[PH][d], xv, ya);
+      else yb = fma(bnd[PH][d], xv, yb);
+    }
+    const double y = ya + yb;
+    double val;
+    if (K0 == CK_SPMV1) {
+      rr[PH] = y;
+      val = (cp.omega[0] * y) * inv[PH];
+    } else if (K0 == CK_SWEEP) {
+      val = fma(cp.omega[0] * (rr[PH] - y), inv[PH], xc);
+    } else {
+      val = y;
+    }
+    if (st_ok) {
+      const int64_t n = (int64_t)pl_tau * cp.P + cxy;
+      if (K0 == CK_SPMV1 && cp.out_t) cp.out_t[n] = y;
+      if (NST == 1) cp.out[n] = val;
+      if (NST == 2 && cp.out_mid) cp.out_mid[n] = val;
+    }
+    if (NST > 1) ring[PH * RPL + roff] = val;
+  }
+
+  // stage s at plane q = tau - s (register set / ring slot R of plane q)
+  template <int S>
+  static __device__ __forceinline__ void stage(bool st_ok, int pl_q, double* ring,
+                                               double (&bnd)[3][ST], double (&rr)[3],
+                                               double (&inv)[3], int64_t cxy, int roff,
+                                               const ChainParams& cp) {
+    constexpr int KIND[3] = {K0, K1, K2};
+    constexpr int R = (PH - S + 3) % 3;
+    const double* rb = ring + (S - 1) * 3 * RPL + roff;
+    const double* rm = rb + ((R + 2) % 3) * RPL;
+    const double* r0 = rb + R * RPL;
+    const double* rp = rb + ((R + 1) % 3) * RPL;
+    double ya = 0.0, yb = 0.0, zc = 0.0;
+#pragma unroll
+    for (int d = 0; d < ST; ++d) {
+      int dx = 0, dy = 0, dz = 0;
+      coffs<ST>(d, dx, dy, dz);
+      const double* rt = dz < 0 ? rm : (dz > 0 ? rp : r0);
+      const double zv = rt[dy * EX + dx];
+      if (d == 0) zc = zv;
+      if (d % 2 == 0) ya = fma(bnd[R][d], zv, ya);
+      else yb = fma(bnd[R][d], zv, yb);
+    }
+    const double y = ya + yb;
+    const double val = (KIND[S] == CK_SWEEP) ? fma(cp.omega[S] * (rr[R] - y), inv[R], zc) : y;
+    if (st_ok) {
+      const int64_t nq = (int64_t)pl_q * cp.P + cxy;
+      if (S == NST - 1) cp.out[nq] = val;
+      else if (S == NST - 2 && cp.out_mid) cp.out_mid[nq] = val;
+    }
+    if (S < NST - 1) ring[(S * 3 + R) * RPL + roff] = val;
+  }
+};
+
+template <int ST, int NST, int K0, int K1, int K2>
+__global__ void __launch_bounds__((CTX + 2 * (NST - 1)) * (CTY + 2 * (NST - 1)), 1)
+chain_kernel(const __grid_constant__ CUtensorMap map_b, const __grid_constant__ CUtensorMap map_r,
+             const __grid_constant__ CUtensorMap map_x, ChainParams cp) {
+  using G = ChainGeom<ST, NST>;
+  constexpr int HALO = G::HALO, EX = G::EX, XX = G::XX, NXB = G::NXB;
+  constexpr int SX = G::SX, PADB = G::PADB, PADX = G::PADX;
+  constexpr bool LOAD_R = (K0 != CK_SPMV1);
+  extern __shared__ __align__(128) unsigned char smem[];
+  double* ring = reinterpret_cast<double*>(smem + G::RING_BASE);   // [NST-1][3][EY][EX]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + G::BAR_BASE);
+
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int tid = ty * EX + tx;
+  const int nx = cp.nx, ny = cp.ny, nz = cp.nz;
+  const bool pz = cp.pz != 0;
+  const int gx0 = (int)blockIdx.x * CTX - HALO, gy0 = (int)blockIdx.y * CTY - HALO;
+  const int gx = gx0 + tx, gy = gy0 + ty;
+  const bool inside = gx >= 0 && gx < nx && gy >= 0 && gy < ny;
+  const bool interior = tx >= HALO && tx < HALO + CTX && ty >= HALO && ty < HALO + CTY;
+  const int64_t cxy = inside ? (int64_t)gy * nx + gx : 0;
+  const int z0 = (int)blockIdx.z * cp.zc;
+  const int z1 = min(nz, z0 + cp.zc);
+  const int tau0 = z0 - HALO;
+  const int qfirst = tau0 - 1;                  // first plane loaded (stage 0 needs x at tau-1)
+  const int qlast = z1 + HALO;                  // last plane loaded (x at tau+1, last step)
+  const uint32_t tx_bytes = G::B_BYTES + (LOAD_R ? G::R_BYTES : 0) + G::X_BYTES;
+  const int xoff = (ty + 1) * XX + tx + 1 + PADX;    // own cell in an input tile
+  const int boff = ty * SX + tx + PADB;              // own cell in a band / rhs tile
+  const int roff = ty * EX + tx;                     // own cell in a ring plane
+
+  // thread 0: plane q -> band buffer (q - tau0) mod 3, input buffer xs, barrier xs
+  auto issue = [&](int q, int xs) {
+    const int bb = ((q - tau0) % 3 + 3) % 3;
+    unsigned char* bbase = smem + bb * G::BSLOT;
+    unsigned char* xbase = smem + G::X_BASE + xs * G::XSLOT;
+    const int pl = pz ? ((q % nz) + nz) % nz : q;   // out of range -> TMA zero fill
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(&bars[xs], tx_bytes);
+    tma_load_4d(bbase, &map_b, &bars[xs], gx0 - PADB, gy0, pl, 0);
+    if (LOAD_R) tma_load_3d(bbase + G::R_OFF, &map_r, &bars[xs], gx0 - PADB, gy0, pl);
+    // the input vector is padded: plane pl lives at z-coordinate pl + 1
+    tma_load_3d(xbase, &map_x, &bars[xs], gx0 - 1 - PADX, gy0 - 1, pl + 1);
+  };
+
+  if (tid == 0) {
+    for (int s = 0; s < NXB; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // prologue: planes tau0-1, tau0, tau0+1 (input buffers 0, 1, 2)
+  if (tid == 0)
+    for (int q = qfirst; q <= min(qfirst + 2, qlast); ++q) issue(q, q - qfirst);
+  mbar_wait(&bars[0], 0);
+  if (qfirst + 1 <= qlast) mbar_wait(&bars[1], 0);
+
+  // running input-buffer indices of planes tau-1, tau, tau+1, tau+2 and parity of tau+1
+  int x_m1 = 0, x_0 = 1, x_p1 = 2, x_p2 = 3;
+  uint32_t par_p1 = 0;
+  double bnd[3][ST], rr[3], inv[3];
+#pragma unroll
+  for (int s = 0; s < 3; ++s) {
+    rr[s] = 0.0;
+    inv[s] = 0.0;
+#pragma unroll
+    for (int d = 0; d < ST; ++d) bnd[s][d] = 0.0;
+  }
+  const int tau_end = z1 + HALO;
+  auto pl_of = [&](int q) { return pz ? ((q % nz) + nz) % nz : q; };
+#define RK_CHAIN_STEP(PHV)                                                                         \
+  {                                                                                                \
+    if (tau >= tau_end) break;                                                                     \
+    if (tid == 0 && tau + 2 <= qlast) issue(tau + 2, x_p2);                                       \
+    if (tau + 1 <= qlast) mbar_wait(&bars[x_p1], par_p1);                                         \
+    using SP = ChainStep<ST, NST, K0, K1, K2, PHV>;                                               \
+    SP::stage0(tau, interior && tau >= z0 && tau < z1 && (pz || tau < nz), pl_of(tau), smem,      \
+               x_m1, x_0, x_p1, ring, bnd, rr, inv, cxy, xoff, boff, roff, cp);                   \
+    __syncthreads();                                                                               \
+    if constexpr (NST >= 2) {                                                                      \
+      if (tau >= tau0 + 2) {                                                                       \
+        const int q = tau - 1;                                                                     \
+        SP::template stage<1>(interior && q >= z0 && q < z1, pl_of(q), ring, bnd, rr, inv, cxy,   \
+                              roff, cp);                                                          \
+      }                                                                                            \
+      __syncthreads();                                                                             \
+    }                                                                                              \
+    if constexpr (NST >= 3) {                                                                      \
+      if (tau >= tau0 + 4) {                                                                       \
+        const int q = tau - 2;                                                                     \
+        SP::template stage<2>(interior && q >= z0 && q < z1, pl_of(q), ring, bnd, rr, inv, cxy,   \
+                              roff, cp);                                                          \
+      }                                                                                            \
+      __syncthreads();                                                                             \
+    }                                                                                              \
+    {                                                                                              \
+      const int t = x_m1;                                                                          \
+      x_m1 = x_0;                                                                                  \
+      x_0 = x_p1;                                                                                  \
+      x_p1 = x_p2;                                                                                 \
+      x_p2 = t;                                                                                    \
+      if (x_p1 == 0) par_p1 ^= 1u;                                                                 \
+    }                                                                                              \
+    ++tau;                                                                                         \
+  }
+  for (int tau = tau0; tau < tau_end;) {
+    RK_CHAIN_STEP(0)
+    RK_CHAIN_STEP(1)
+    RK_CHAIN_STEP(2)
+  }
+#undef RK_CHAIN_STEP
+}
+
+// ------------------------------------------------------------------- host
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    RK_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    RK_REQUIRE(p && q == cudaDriverEntryPointSuccess, RK_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+void encode(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims,
+            const cuuint64_t* strides, const cuuint32_t* box) {
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (cuuint32_t)rank,
+                           const_cast<void*>(base), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  RK_REQUIRE(r == CUDA_SUCCESS, RK_ECUDA, "cuTensorMapEncodeTiled failed");
+}
+
+template <int ST, int NST, int K0, int K1, int K2>
+void launch_one(rk_op* op, const ChainParams& cp, dim3 grid) {
+  using G = ChainGeom<ST, NST>;
+  auto kern = chain_kernel<ST, NST, K0, K1, K2>;
+  static bool attr = false;
+  if (!attr) {
+    RK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
+    attr = true;
+  }
+  const cuuint64_t nx = op->g.nx, ny = op->g.ny, nz = op->g.nz_local;
+  CUtensorMap mb, mr, mx;
+  {
+    cuuint64_t dims[4] = {nx, ny, nz, (cuuint64_t)ST};
+    cuuint64_t str[3] = {nx * 8, nx * ny * 8, (cuuint64_t)op->N * 8};
+    cuuint32_t box[4] = {(cuuint32_t)G::SX, (cuuint32_t)G::EY, 1, (cuuint32_t)ST};
+    encode(&mb, cp.bands, 4, dims, str, box);
+  }
+  {
+    cuuint64_t dims[3] = {nx, ny, nz};
+    cuuint64_t str[2] = {nx * 8, nx * ny * 8};
+    cuuint32_t box[3] = {(cuuint32_t)G::SX, (cuuint32_t)G::EY, 1};
+    encode(&mr, cp.r ? cp.r : cp.bands, 3, dims, str, box);
+  }
+  {
+    cuuint64_t dims[3] = {nx, ny, nz + 2};                 // padded: ghost planes at 0, nz + 1
+    cuuint64_t str[2] = {nx * 8, nx * ny * 8};
+    cuuint32_t box[3] = {(cuuint32_t)G::XX, (cuuint32_t)G::XY, 1};
+    encode(&mx, cp.xin - op->P, 3, dims, str, box);
+  }
+  dim3 blk(G::EX, G::EY);
+  kern<<<grid, blk, G::SMEM, op->ctx->stream>>>(mb, mr, mx, cp);
+}
+
+template <int NST>
+void chain_dispatch(rk_op* op, const int* k, const ChainParams& cp, dim3 grid) {
+  if constexpr (NST == 3) {
+    if (k[0] == CK_SPMV1 && k[1] == CK_SWEEP && k[2] == CK_SWEEP)
+      return launch_one<7, 3, CK_SPMV1, CK_SWEEP, CK_SWEEP>(op, cp, grid);
+    if (k[0] == CK_SWEEP && k[1] == CK_SWEEP && k[2] == CK_SWEEP)
+      return launch_one<7, 3, CK_SWEEP, CK_SWEEP, CK_SWEEP>(op, cp, grid);
+    if (k[0] == CK_SWEEP && k[1] == CK_SWEEP && k[2] == CK_SPMV)
+      return launch_one<7, 3, CK_SWEEP, CK_SWEEP, CK_SPMV>(op, cp, grid);
+  } else if constexpr (NST == 2) {
+    if (k[0] == CK_SPMV1 && k[1] == CK_SWEEP)
+      return launch_one<7, 2, CK_SPMV1, CK_SWEEP, 0>(op, cp, grid);
+    if (k[0] == CK_SWEEP && k[1] == CK_SWEEP)
+      return launch_one<7, 2, CK_SWEEP, CK_SWEEP, 0>(op, cp, grid);
+    if (k[0] == CK_SWEEP && k[1] == CK_SPMV)
+      return launch_one<7, 2, CK_SWEEP, CK_SPMV, 0>(op, cp, grid);
+  } else {
+    if (k[0] == CK_SPMV1) return launch_one<7, 1, CK_SPMV1, 0, 0>(op, cp, grid);
+    if (k[0] == CK_SWEEP) return launch_one<7, 1, CK_SWEEP, 0, 0>(op, cp, grid);
+    return launch_one<7, 1, CK_SPMV, 0, 0>(op, cp, grid);
+  }
+  throw Error(RK_EINVAL, "unsupported chain stage combination");
+}
+
+}  // namespace
+
+int chain_max_stages(const rk_op* op) {
+  if (op->ctx->nranks != 1 || op->no_chain) return 0;      // deep halos not exchanged (yet)
+  if (op->S != 7) return 0;
+  if (op->g.periodic_mask & 3) return 0;                    // TMA boxes do not wrap in x/y
+  if (op->g.nx % CTX != 0 || op->g.ny % CTY != 0 || op->g.nx % 2 != 0) return 0;
+  if (op->g.nz_local < 16) return 0;
+  return 3;
+}
+
+void chain_launch(rk_op* op, int nst, const int* kinds, const double* omegas, const double* xin,
+                  const double* r, double* out_t, double* out_mid, double* out) {
+  rk_ctx* ctx = op->ctx;
+  ChainParams cp;
+  std::memset(&cp, 0, sizeof(cp));
+  cp.bands = op->bands;
+  cp.N = op->N;
+  cp.P = op->P;
+  cp.nx = (int)op->g.nx;
+  cp.ny = (int)op->g.ny;
+  cp.nz = (int)op->g.nz_local;
+  cp.px = 0;
+  cp.py = 0;
+  cp.pz = (op->g.periodic_mask & 4) ? 1 : 0;
+  cp.xin = xin;
+  cp.r = r;
+  cp.out_t = out_t;
+  cp.out_mid = out_mid;
+  cp.out = out;
+  for (int s = 0; s < nst; ++s) cp.omega[s] = omegas[s];
+  const int tiles = (int)((op->g.nx / CTX) * (op->g.ny / CTY));
+  // z chunks: one resident CTA per SM (the slot ring uses ~200 KB of shared
+  // memory), so aim for a single wave -- chunks = SMs / tiles (>= 1), long
+  // chunks to amortise the 2 (NST-1)-plane wavefront prologue
+  const int nz = (int)op->g.nz_local;
+  const int chunks = std::max(1, std::min(ctx->sms / std::max(1, tiles), nz / 16));
+  int zc = (nz + chunks - 1) / chunks;
+  zc = std::max(1, std::min(zc, nz));
+  cp.zc = zc;
+  dim3 grid((unsigned)(op->g.nx / CTX), (unsigned)(op->g.ny / CTY), (unsigned)((nz + zc - 1) / zc));
+  // algorithmic bytes: bands once + stage-0 input + rhs (if any) + outputs
+  const double words = op->S + 1 + ((kinds[0] != CK_SPMV1) ? 1 : 0) + 1 + (out_t ? 1 : 0) +
+                       (out_mid ? 1 : 0);
+  Launch L(ctx, "chain", 8.0 * op->N * words);
+  if (nst == 3) chain_dispatch<3>(op, kinds, cp, grid);
+  else if (nst == 2) chain_dispatch<2>(op, kinds, cp, grid);
+  else chain_dispatch<1>(op, kinds, cp, grid);
+  L.done();
+}
+
+void chain_run(rk_op* op, const std::vector<int>& kinds, const std::vector<double>& om,
+               const double* xin, const double* r, double* out_t, double* out_mid, double* out,
+               double* za, double* zb) {
+  const int n = (int)kinds.size();
+  const int nmax = chain_max_stages(op);
+  double* bufs[2] = {za, zb};
+  if (xin == za) std::swap(bufs[0], bufs[1]);
+  const double* rhs = kinds[0] == CK_SPMV1 ? out_t : r;
+  if (nmax == 0) {
+    const double* cur = xin;
+    for (int q = 0; q < n; ++q) {
+      double* dst = (q == n - 1) ? out : ((q == n - 2 && out_mid) ? out_mid : bufs[q % 2]);
+      if (kinds[q] == CK_SPMV1) stencil(op, SM_SPMV_SWEEP1, cur, nullptr, out_t, dst, om[q], nullptr);
+      else if (kinds[q] == CK_SWEEP) stencil(op, SM_SWEEP, cur, rhs, dst, nullptr, om[q], nullptr);
+      else stencil(op, SM_SPMV, cur, nullptr, dst, nullptr, 0.0, nullptr);
+      cur = dst;
+    }
+    return;
+  }
+  const int g = (n + nmax - 1) / nmax;
+  const double* cur = xin;
+  int a = 0;
+  for (int i = 0; i < g; ++i) {
+    const int len = n / g + (i < n % g ? 1 : 0);
+    const bool last = (i == g - 1);
+    double* dst = last ? out : bufs[i % 2];
+    chain_launch(op, len, kinds.data() + a, om.data() + a, cur, rhs,
+                 (kinds[a] == CK_SPMV1) ? out_t : nullptr, last ? out_mid : nullptr, dst);
+    cur = dst;
+    a += len;
+  }
+}
+
+}  // namespace rk

@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(256) stencil_kernel(StencilParams sp) {
         const Vec<VEC> r = ldv_ro<VEC>(sp.r + n);
         Vec<VEC> o;
 #pragma unroll
-        for (int t = 0; t < VEC; ++t) o.v[t] = sp.omega * r.v[t] / D.v[t];
+        for (int t = 0; t < VEC; ++t) o.v[t] = (sp.omega * r.v[t]) * (1.0 / D.v[t]);
         stv<VEC>(sp.out0 + n, o);
       }
       continue;
@@ -227,9 +227,11 @@ __global__ void __launch_bounds__(256) stencil_kernel(StencilParams sp) {
             if (uses<ST>(1, dy, dz)) xr[dy + 1][dz + 1] = __ldg(p + ip);
           }
         }
-      double y[VEC], a0[VEC];
+      // two interleaved FMA chains (even / odd bands), summed at the end --
+      // the same order as the fused chain kernel (chain.cu)
+      double y[VEC], ya[VEC], yb[VEC], a0[VEC];
 #pragma unroll
-      for (int t = 0; t < VEC; ++t) y[t] = 0.0;
+      for (int t = 0; t < VEC; ++t) ya[t] = yb[t] = 0.0;
 #pragma unroll
       for (int d = 0; d < ST; ++d) {
         int dx = 0, dy = 0, dz = 0;
@@ -243,9 +245,12 @@ __global__ void __launch_bounds__(256) stencil_kernel(StencilParams sp) {
           else if (dx < 0) xv = (t == 0) ? xl[dy + 1][dz + 1] : c.v[t - 1];
           else xv = (t == VEC - 1) ? xr[dy + 1][dz + 1] : c.v[t + 1];
           if (d == 0) a0[t] = a.v[t];
-          y[t] = fma(a.v[t], xv, y[t]);
+          if (d % 2 == 0) ya[t] = fma(a.v[t], xv, ya[t]);
+          else yb[t] = fma(a.v[t], xv, yb[t]);
         }
       }
+#pragma unroll
+      for (int t = 0; t < VEC; ++t) y[t] = ya[t] + yb[t];
       const Vec<VEC>& x0 = xc[1][1];
       Vec<VEC> o0, o1;
       if constexpr (MODE == SM_SPMV) {
@@ -256,7 +261,7 @@ __global__ void __launch_bounds__(256) stencil_kernel(StencilParams sp) {
 #pragma unroll
         for (int t = 0; t < VEC; ++t) {
           o0.v[t] = y[t];
-          o1.v[t] = sp.omega * y[t] / a0[t];
+          o1.v[t] = (sp.omega * y[t]) * (1.0 / a0[t]);
         }
         stv<VEC>(sp.out0 + n, o0);
         stv<VEC>(sp.out1 + n, o1);
@@ -264,7 +269,7 @@ __global__ void __launch_bounds__(256) stencil_kernel(StencilParams sp) {
         const Vec<VEC> r = ldv_ro<VEC>(sp.r + n);
 #pragma unroll
         for (int t = 0; t < VEC; ++t) {
-          o0.v[t] = x0.v[t] + sp.omega * (r.v[t] - y[t]) / a0[t];
+          o0.v[t] = fma(sp.omega * (r.v[t] - y[t]), 1.0 / a0[t], x0.v[t]);
           if constexpr (MODE == SM_SWEEP_NORM) red[0] = fma(o0.v[t], o0.v[t], red[0]);
         }
         stv<VEC>(sp.out0 + n, o0);
@@ -274,7 +279,7 @@ __global__ void __launch_bounds__(256) stencil_kernel(StencilParams sp) {
         for (int t = 0; t < VEC; ++t) {
           o0.v[t] = r.v[t] - y[t];
           red[0] = fma(o0.v[t], o0.v[t], red[0]);
-          if constexpr (MODE == SM_RESID_SWEEP1) o1.v[t] = sp.omega * o0.v[t] / a0[t];
+          if constexpr (MODE == SM_RESID_SWEEP1) o1.v[t] = (sp.omega * o0.v[t]) * (1.0 / a0[t]);
         }
         stv<VEC>(sp.out0 + n, o0);
         if constexpr (MODE == SM_RESID_SWEEP1) stv<VEC>(sp.out1 + n, o1);
@@ -578,7 +583,7 @@ __global__ void __launch_bounds__(256) bicg_p_kernel(const double* __restrict__ 
     if (D) {
       const Vec<VEC> dn = ldv_stream<VEC>(D + n);
 #pragma unroll
-      for (int t = 0; t < VEC; ++t) zn.v[t] = wl * pn.v[t] / dn.v[t];
+      for (int t = 0; t < VEC; ++t) zn.v[t] = (wl * pn.v[t]) * (1.0 / dn.v[t]);
     }
     stv<VEC>(z + n, zn);
   }
@@ -610,7 +615,7 @@ __global__ void __launch_bounds__(256) bicg_s_kernel(const double* __restrict__ 
     if (D) {
       const Vec<VEC> dn = ldv_stream<VEC>(D + n);
 #pragma unroll
-      for (int t = 0; t < VEC; ++t) zn.v[t] = wl * sn.v[t] / dn.v[t];
+      for (int t = 0; t < VEC; ++t) zn.v[t] = (wl * sn.v[t]) * (1.0 / dn.v[t]);
     }
     stv<VEC>(z + n, zn);
   }
@@ -688,39 +693,6 @@ __global__ void bicg_setup_kernel(double* xi, const double* eta0, int k, BiIter*
 
 // =================================================================== host
 namespace {
-
-struct Launch {
-  rk_ctx* ctx;
-  bool on = false;
-  size_t idx = 0;
-  Launch(rk_ctx* c, const char* cls, double bytes) : ctx(c) {
-    ++ctx->launches;
-    if (ctx->prof_on && (ctx->prof_filter.empty() || strstr(cls, ctx->prof_filter.c_str()))) {
-      on = true;
-      rk_ctx::Pending p;
-      p.cls = cls;
-      p.bytes = bytes;
-      if (ctx->pool.size() < 2) {
-        cudaEvent_t e;
-        for (int q = 0; q < 64; ++q) {
-          RK_CUDA(cudaEventCreate(&e));
-          ctx->pool.push_back(e);
-        }
-      }
-      p.a = ctx->pool.back();
-      ctx->pool.pop_back();
-      p.b = ctx->pool.back();
-      ctx->pool.pop_back();
-      RK_CUDA(cudaEventRecord(p.a, ctx->stream));
-      ctx->pending.push_back(p);
-      idx = ctx->pending.size() - 1;
-    }
-  }
-  void done() {
-    RK_CUDA(cudaGetLastError());
-    if (on) RK_CUDA(cudaEventRecord(ctx->pending[idx].b, ctx->stream));
-  }
-};
 
 // Grid = min(work / CTA, SMs x resident CTAs of this instantiation).
 template <typename... KArgs, typename... Args>

@@ -11,6 +11,7 @@
 #include <array>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <numeric>
@@ -166,27 +167,57 @@ struct rk_solver {
   }
 
   // ------------------------------------------------- preconditioner chains
+  // Runs n chained stencil stages (CK_SPMV1 / CK_SWEEP / CK_SPMV, chain.cu):
+  // the first reads xin; sweeps use r, or t = A xin when stage 0 is CK_SPMV1
+  // (t is written to out_t).  out_mid receives stage n-2's output.  Uses the
+  // temporally blocked kernel (up to chain_max_stages() stages per launch)
+  // when available, else one stencil launch per stage (same arithmetic).
+  void run_chain(const std::vector<int>& kinds, const std::vector<double>& om, const double* xin,
+                 const double* r, double* out_t, double* out_mid, double* out) {
+    chain_run(op, kinds, om, xin, r, out_t, out_mid, out, za, zb);
+  }
+
   // Jacobi sweeps 2..sweeps+1 (the first sweep's output is in za):
   // z <- z + w_l D^-1 (r - A z) (sweeps-1 times), then dst = z + w_g D^-1 (r - A z).
   void sweeps(const double* r, double* dst, double* red) {
     const rk_precond& pc = cfg.pc;
+    if (!red) {
+      std::vector<int> k(pc.sweeps, CK_SWEEP);
+      std::vector<double> w(pc.sweeps, pc.omega_local);
+      w.back() = pc.omega_global;
+      run_chain(k, w, za, r, nullptr, nullptr, dst);
+      return;
+    }
     double *zin = za, *zout = zb;
     for (int q = 1; q < pc.sweeps; ++q) {
       stencil(op, SM_SWEEP, zin, r, zout, nullptr, pc.omega_local, nullptr);
       std::swap(zin, zout);
     }
-    stencil(op, red ? SM_SWEEP_NORM : SM_SWEEP, zin, r, dst, nullptr, pc.omega_global, red);
+    stencil(op, SM_SWEEP_NORM, zin, r, dst, nullptr, pc.omega_global, red);
   }
   bool jac() const { return cfg.pc.kind == 1; }
 
-  // dst = M^-1 A v  (left-preconditioned operator, Alg. 3 line 6)
+  // dst = M^-1 A v  (left-preconditioned operator, Alg. 3 line 6):
+  // stages [t = A v, z1 = w_l t/D], sweeps 2..5 (w_l), sweep 6 (w_g)
   void apply_ahat(const double* v, double* dst) {
     if (jac()) {
-      stencil(op, SM_SPMV_SWEEP1, v, nullptr, t, za, cfg.pc.omega_local, nullptr);
-      sweeps(t, dst, nullptr);
+      std::vector<int> k(cfg.pc.sweeps + 1, CK_SWEEP);
+      std::vector<double> w(cfg.pc.sweeps + 1, cfg.pc.omega_local);
+      k[0] = CK_SPMV1;
+      w.back() = cfg.pc.omega_global;
+      run_chain(k, w, v, nullptr, t, nullptr, dst);
     } else {
       stencil(op, SM_SPMV, v, nullptr, dst, nullptr, 0.0, nullptr);
     }
+  }
+  // rBiCGStab: (z1 in za) -> p_hat = M^-1 p (out_mid) and v = A p_hat (out)
+  void apply_right(const double* rhs, double* phat, double* v) {
+    std::vector<int> k(cfg.pc.sweeps + 1, CK_SWEEP);
+    std::vector<double> w(cfg.pc.sweeps + 1, cfg.pc.omega_local);
+    w[cfg.pc.sweeps - 1] = cfg.pc.omega_global;
+    k.back() = CK_SPMV;
+    w.back() = 0.0;
+    run_chain(k, w, za, rhs, nullptr, phat, v);
   }
   // dst = M^-1 r (r need not be padded), optional ||dst||^2
   void apply_minv(const double* r, double* dst, double* red) {
@@ -563,11 +594,11 @@ struct rk_solver {
         // line 6 + p_hat = M^-1 p (right preconditioning) ; line 7: v = A p_hat
         if (jac()) {
           bicg_p(op, r, p, v, za, wl, true, cur, i ? bi(i - 1) : cur, i == 0);
-          sweeps(p, ph, nullptr);
+          apply_right(p, ph, v);               // p_hat = M^-1 p ; v = A p_hat
         } else {
           bicg_p(op, r, p, v, ph, 1.0, false, cur, i ? bi(i - 1) : cur, i == 0);
+          stencil(op, SM_SPMV, ph, nullptr, v, nullptr, 0.0, nullptr);
         }
-        stencil(op, SM_SPMV, ph, nullptr, v, nullptr, 0.0, nullptr);
         rep.krylov_matvecs += 1;
         // line 7a: eta1 = C^T v ; v -= C eta1 ; sigma = r~^T v
         if (k > 0) {
@@ -578,8 +609,8 @@ struct rk_solver {
         }
         // line 8: alpha = rho / sigma ; s = r - alpha v (+ first sweep of s_hat)
         bicg_s(op, r, v, s, jac() ? za : sh, wl, jac(), cur);
-        if (jac()) sweeps(s, sh, nullptr);
-        stencil(op, SM_SPMV, sh, nullptr, tt, nullptr, 0.0, nullptr);   // line 12
+        if (jac()) apply_right(s, sh, tt);      // s_hat = M^-1 s ; t = A s_hat (line 12)
+        else stencil(op, SM_SPMV, sh, nullptr, tt, nullptr, 0.0, nullptr);
         rep.krylov_matvecs += 1;
         if (k > 0) {                                              // line 12a
           bdot(ctx, C, tt, N, eta(1));
@@ -779,6 +810,7 @@ rk_status rk_op_create(rk_ctx* ctx, const rk_grid* g, int nbands, const int8_t* 
                  "bands violate truncation (S:39) or have a zero diagonal: " +
                      std::to_string(bad) + " bad coefficients");
       op->user_offsets.assign(offsets, offsets + 3 * nbands);
+      op->no_chain = std::getenv("RK_NO_CHAIN") != nullptr;
     } catch (...) {
       cudaFree(op->bands);
       delete op;
@@ -836,11 +868,10 @@ rk_status rk_precond_apply(rk_op* op, const rk_precond* pc, const double* r, dou
       op_scratch(op);
       double *za = op->scratch[0], *zb = op->scratch[1];
       stencil(op, SM_SCALE, nullptr, r, za, nullptr, pc->omega_local, nullptr);
-      for (int q = 1; q < pc->sweeps; ++q) {
-        stencil(op, SM_SWEEP, za, r, zb, nullptr, pc->omega_local, nullptr);
-        std::swap(za, zb);
-      }
-      stencil(op, SM_SWEEP, za, r, z, nullptr, pc->omega_global, nullptr);
+      std::vector<int> k(pc->sweeps, CK_SWEEP);
+      std::vector<double> w(pc->sweeps, pc->omega_local);
+      w.back() = pc->omega_global;
+      chain_run(op, k, w, za, r, nullptr, nullptr, z, za, zb);
     }
     RK_CUDA(cudaStreamSynchronize(op->ctx->stream));
   });

@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <cstdio>
+#include <cstring>
 #include <map>
 #include <stdexcept>
 #include <unordered_map>
@@ -80,6 +81,27 @@ struct LcOut {
   int acc[MAXOUT];
 };
 
+// Stage kinds of the fused preconditioned-operator chain (chain.cu)
+enum ChainKind {
+  CK_SPMV1 = 0,   // t = A x (kept as the sweeps' right-hand side); z = w t / D
+  CK_SWEEP = 1,   // z' = z + w (r - A z) / D
+  CK_SPMV = 2,    // y = A z
+};
+
+struct ChainParams {
+  const double* bands;
+  int64_t N, P;
+  int nx, ny, nz;
+  int px, py, pz;
+  const double* xin;    // stage-0 input (padded vector)
+  const double* r;      // sweep right-hand side (unused when stage 0 is CK_SPMV1)
+  double* out_t;        // CK_SPMV1: t (nullable)
+  double* out_mid;      // output of stage NST-2 (nullable)
+  double* out;          // output of the last stage
+  double omega[3];
+  int zc;               // z planes per CTA
+};
+
 // Per-iteration device scalars of rBiCGStab (one 64-byte record per iteration).
 struct BiIter {
   double rho;    // r~^T r_i            (written by iteration i-1 or the setup)
@@ -139,9 +161,55 @@ struct rk_op {
   double* scratch[2] = {nullptr, nullptr};
   int wrapz = 0;
   std::vector<int8_t> user_offsets;   // caller's band order (for rk_op_update_bands)
+  bool no_chain = false;              // env RK_NO_CHAIN: disable the fused TMA chain
 };
 
 namespace rk {
+
+// Every librk launch goes through a Launch: it counts the launch and, with
+// profiling on, brackets it with CUDA events on the context stream.
+struct Launch {
+  rk_ctx* ctx;
+  bool on = false;
+  size_t idx = 0;
+  Launch(rk_ctx* c, const char* cls, double bytes) : ctx(c) {
+    ++ctx->launches;
+    if (ctx->prof_on && (ctx->prof_filter.empty() || strstr(cls, ctx->prof_filter.c_str()))) {
+      on = true;
+      rk_ctx::Pending p;
+      p.cls = cls;
+      p.bytes = bytes;
+      if (ctx->pool.size() < 2) {
+        cudaEvent_t e;
+        for (int q = 0; q < 64; ++q) {
+          RK_CUDA(cudaEventCreate(&e));
+          ctx->pool.push_back(e);
+        }
+      }
+      p.a = ctx->pool.back();
+      ctx->pool.pop_back();
+      p.b = ctx->pool.back();
+      ctx->pool.pop_back();
+      RK_CUDA(cudaEventRecord(p.a, ctx->stream));
+      ctx->pending.push_back(p);
+      idx = ctx->pending.size() - 1;
+    }
+  }
+  void done() {
+    RK_CUDA(cudaGetLastError());
+    if (on) RK_CUDA(cudaEventRecord(ctx->pending[idx].b, ctx->stream));
+  }
+};
+
+// fused chain (chain.cu): max stages per launch for this operator (0 = unavailable)
+int chain_max_stages(const rk_op* op);
+void chain_launch(rk_op* op, int nst, const int* kinds, const double* omegas, const double* xin,
+                  const double* r, double* out_t, double* out_mid, double* out);
+// Runs n chained stencil stages; fused (TMA) launches of up to chain_max_stages()
+// stages when available, else one stencil launch per stage.  za/zb: padded scratch.
+void chain_run(rk_op* op, const std::vector<int>& kinds, const std::vector<double>& om,
+               const double* xin, const double* r, double* out_t, double* out_mid, double* out,
+               double* za, double* zb);
 
 // ------------------------------------------------------------ launch layer
 // All kernels are launched through these wrappers (kernels.cu).  Each
