@@ -25,14 +25,18 @@ def have_nccl():
     return os.path.exists("/usr/include/nccl.h")
 
 
-def command(out=LIB, extra=()):
-    cmd = [nvcc_path(), "-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC",
-           "-Xcompiler", "-Wall", "-shared", "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-           "-Xptxas", "-warn-spills"]
+def flags(extra=()):
+    f = [nvcc_path(), "-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC",
+         "-Xcompiler", "-Wall", "-I", os.path.join(ROOT, "include"), "-I", CSRC,
+         "-Xptxas", "-warn-spills"]
     if have_nccl():
-        cmd += ["-DRK_WITH_NCCL"]
-    cmd += list(extra)
-    cmd += [os.path.join(CSRC, s) for s in SOURCES]
+        f += ["-DRK_WITH_NCCL"]
+    return f + list(extra)
+
+
+def command(out=LIB, extra=()):
+    """Single-invocation build command (documentation / manual builds)."""
+    cmd = flags(extra) + ["-shared"] + [os.path.join(CSRC, s) for s in SOURCES]
     cmd += ["-o", out, "-lcudart"]
     if have_nccl():
         cmd += ["-lnccl"]
@@ -52,12 +56,26 @@ def up_to_date():
 def build(force=False, verbose=True):
     if not force and up_to_date():
         return LIB
-    cmd = command()
+    # one nvcc per translation unit, in parallel, then one link
+    from concurrent.futures import ThreadPoolExecutor
+    odir = os.path.join(HERE, "build_obj")
+    os.makedirs(odir, exist_ok=True)
+    objs = [os.path.join(odir, s + ".o") for s in SOURCES]
+    cmds = [flags() + ["-c", os.path.join(CSRC, s), "-o", o] for s, o in zip(SOURCES, objs)]
     if verbose:
-        print(" ".join(cmd), flush=True)
+        for c in cmds:
+            print(" ".join(c), flush=True)
+    with ThreadPoolExecutor(len(cmds)) as ex:
+        for r in ex.map(lambda c: subprocess.run(c, capture_output=True, text=True), cmds):
+            sys.stdout.write(r.stdout)
+            sys.stderr.write(r.stderr)
+            if r.returncode != 0:
+                raise subprocess.CalledProcessError(r.returncode, r.args)
     tmp = LIB + ".tmp"
-    cmd[cmd.index("-o") + 1] = tmp
-    subprocess.run(cmd, check=True)
+    link = [nvcc_path(), *ARCH, "-shared", *objs, "-o", tmp, "-lcudart"]
+    if have_nccl():
+        link += ["-lnccl"]
+    subprocess.run(link, check=True)
     os.replace(tmp, LIB)
     return LIB
 
