@@ -147,6 +147,16 @@ def cpu_sample(workload, seconds, gpu_mv=None):
             "sample": sample, "setup_s": setup}
 
 
+def oracle_counts(workload):
+    """[(tag, krylov matvecs)] of the oracle's full sequence, if stored."""
+    p = os.path.join(ROOT, "tests", "golden", f"oracle_seq_{workload}.json")
+    if not os.path.exists(p):
+        return None, None
+    d = json.load(open(p))
+    return ([[r["tag"], r["krylov_matvecs"]] for r in d["systems"]],
+            f"the oracle's own full-sequence counts ({os.path.relpath(p, ROOT)})")
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle, timed per step on a bounded sample."""
     rank = int(os.environ.get("RANK", "0"))
@@ -154,8 +164,7 @@ def run_reference(args):
         return
     from problems import get_workload
     w = get_workload(args.workload)
-    # typical per-system counts from the oracle's own c3 behaviour are not known
-    # without a full run; each step times one rGCROT cycle + rBiCGStab iterations
+    # each step times one rGCROT cycle + rBiCGStab iterations of the oracle
     ms = []
     info = None
     for i in range(args.warmup + args.steps):
@@ -165,15 +174,14 @@ def run_reference(args):
     mrg = float(np.mean([m["ms_per_mv_rgcrot"] for m in ms]))
     mbi = [m["ms_per_mv_rbicgstab"] for m in ms if m["ms_per_mv_rbicgstab"]]
     mbi = float(np.mean(mbi)) if mbi else mrg
-    # ms/system for a sequence with the hybrid's structure: n_sw rGCROT systems and
-    # the rest rBiCGStab, at the GPU-measured average matvecs per system stored by
-    # the last rk bench (profiles/last_counts.json) when present, else 100 / system.
-    counts = None
-    cp = os.path.join(ROOT, "profiles", "last_counts.json")
-    if os.path.exists(cp):
-        counts = json.load(open(cp)).get(args.workload)
+    # ms/system for the sequence with the oracle's OWN per-system Krylov
+    # matvec counts (tests/golden/oracle_seq_<workload>.json, written by
+    # scripts/oracle_counts.py from oracle/ alone); without that file, the
+    # hybrid's structure at 100 matvecs per system.
+    counts, src = oracle_counts(args.workload)
     if not counts:
         counts = [["rgcrot" if t < w.params.n_sw else "rbicgstab", 100] for t in range(w.n_systems)]
+        src = "100 matvecs/system assumed"
     value = sum(mv * (mbi if tag == "rbicgstab" else mrg) for tag, mv in counts) / len(counts)
     cores = os.cpu_count()
     line = {
@@ -185,6 +193,7 @@ def run_reference(args):
                    "systems": w.n_systems, "l2": "inputs larger than L2"},
         "cpu_baseline": {"value": round(value, 3), "unit": "ms/system", "cores": cores,
                          "kind": "oracle", "sample": ms[-1]["sample"] +
+                         f"; per-system matvecs: {src}"
                          " (NumPy; stencil and elementwise work single-threaded)"},
         "e2e": {"value": round(value, 3), "unit": "ms/system", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -291,11 +300,14 @@ def run_rk(args):
         Xh = [torch.zeros(Nl, dtype=torch.float64).pin_memory() for _ in range(T)]
         step(True, Bh, Xh)
         barrier()
-        t0 = time.perf_counter()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
         for _ in range(args.steps):
             step(True, Bh, Xh)
+        e1.record(stream)
         barrier()
-        wall = (time.perf_counter() - t0) * 1e3
+        wall = e0.elapsed_time(e1)   # device time on the library stream; copies included
         if world > 1:
             t = torch.tensor([wall], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -338,20 +350,16 @@ def run_rk(args):
         "clocks": clk,
         "e2e": e2e,
     }
-    if args.breakdown or True:
+    if True:   # per-kernel-class breakdown of the untimed profiling pass
         line["kernel_breakdown"] = {k: {"ms": round(v["ms"], 3), "launches": v["launches"],
                                         "gbs": round(v["bytes"] / (v["ms"] * 1e-3) / 1e9, 1) if v["ms"] else None}
                                     for k, v in sorted(prof_all.items(), key=lambda kv: -kv[1]["ms"])}
-    try:
-        os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
-        cp = os.path.join(ROOT, "profiles", "last_counts.json")
-        d = json.load(open(cp)) if os.path.exists(cp) else {}
-        d[args.workload] = [[r["tag"], r["krylov_matvecs"]] for r in reps]
-        json.dump(d, open(cp, "w"))
-    except OSError:
-        pass
     if world == 1 and not args.no_cpu_baseline:
-        cb = cpu_sample(args.workload, args.cpu_sample_seconds, [(r["tag"], r["krylov_matvecs"]) for r in reps])
+        counts, src = oracle_counts(args.workload)
+        if not counts:
+            counts, src = [(r["tag"], r["krylov_matvecs"]) for r in reps], "the GPU run's per-system counts"
+        cb = cpu_sample(args.workload, args.cpu_sample_seconds, counts)
+        cb["sample"] = cb["sample"].replace("the GPU run's per-system matvec counts", src)
         line["cpu_baseline"] = {"value": round(cb["ms_per_system"], 1), "unit": "ms/system",
                                 "cores": os.cpu_count(), "kind": "oracle", "sample": cb["sample"]}
     print(json.dumps(line), flush=True)

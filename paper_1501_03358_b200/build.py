@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "librk.so")
-SOURCES = ["kernels.cu", "chain.cu", "librk.cpp", "comm.cpp"]
+SOURCES = ["stencil.cu", "blockops.cu", "bicg.cu", "chain.cu", "librk.cpp", "comm.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

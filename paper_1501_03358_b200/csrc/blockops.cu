@@ -1,0 +1,548 @@
+// sm_100a block kernels of librk: K3 block dot, K4 block update, normalise,
+// K5 linear combinations, projection, K8 rotation (tall-skinny, HBM-bound).
+#include "kcommon.cuh"
+
+namespace rk {
+
+
+// ----------------------------------------------------------------- K3
+// g_c = Q_c^T w for c < ncol (block dot, "[C V_j]^T w").  NC accumulators
+// per thread; every column is streamed once, w once.
+template <int NC, int VEC>
+__global__ void __launch_bounds__(256) bdot_kernel(ColPtrs Q, int ncol, const double* __restrict__ w,
+                                                   int64_t N, RedArgs ra) {
+  double acc[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) acc[c] = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t NE = N / VEC;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < NE; e += stride) {
+    const int64_t r = e * VEC;
+    const Vec<VEC> wv = ldv_ro<VEC>(w + r);
+#pragma unroll
+    for (int g = 0; g < NC / GRP; ++g) {
+      if (g * GRP < ncol) {
+        Vec<VEC> q[GRP];
+#pragma unroll
+        for (int u = 0; u < GRP; ++u) q[u] = ldv_stream<VEC>(Q.p[g * GRP + u] + r);
+#pragma unroll
+        for (int u = 0; u < GRP; ++u)
+#pragma unroll
+          for (int t = 0; t < VEC; ++t) acc[g * GRP + u] = fma(q[u].v[t], wv.v[t], acc[g * GRP + u]);
+      }
+    }
+  }
+  block_reduce_store<NC>(acc, ncol, ra);
+}
+
+// ----------------------------------------------------------------- K4
+// w <- w - sum_c Q_c gs*g_c, then optional dots of the new w with up to 3
+// vectors (nullptr = w itself).
+template <int NC, int ND, int VEC>
+__global__ void __launch_bounds__(256) bupd_kernel(ColPtrs Q, int ncol, const double* __restrict__ g,
+                                                   double gs, double* __restrict__ w, int64_t N,
+                                                   const double* d0, const double* d1,
+                                                   const double* d2, RedArgs ra) {
+  __shared__ double gsh[NC];
+  for (int c = threadIdx.x; c < NC; c += blockDim.x) gsh[c] = c < ncol ? gs * g[c] : 0.0;
+  __syncthreads();
+  double acc[ND > 0 ? ND : 1];
+#pragma unroll
+  for (int q = 0; q < (ND > 0 ? ND : 1); ++q) acc[q] = 0.0;
+  const double* dv[3] = {d0, d1, d2};
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t NE = N / VEC;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < NE; e += stride) {
+    const int64_t r = e * VEC;
+    Vec<VEC> wv = ldv<VEC>(w + r);
+#pragma unroll
+    for (int gi = 0; gi < NC / GRP; ++gi) {
+      if (gi * GRP < ncol) {
+        Vec<VEC> q[GRP];
+#pragma unroll
+        for (int u = 0; u < GRP; ++u) q[u] = ldv_stream<VEC>(Q.p[gi * GRP + u] + r);
+#pragma unroll
+        for (int u = 0; u < GRP; ++u)
+#pragma unroll
+          for (int t = 0; t < VEC; ++t) wv.v[t] = fma(-gsh[gi * GRP + u], q[u].v[t], wv.v[t]);
+      }
+    }
+    stv<VEC>(w + r, wv);
+#pragma unroll
+    for (int q = 0; q < ND; ++q) {
+      Vec<VEC> o = wv;
+      if (dv[q]) o = ldv_ro<VEC>(dv[q] + r);
+#pragma unroll
+      for (int t = 0; t < VEC; ++t) acc[q] = fma(o.v[t], wv.v[t], acc[q]);
+    }
+  }
+  if constexpr (ND > 0) block_reduce_store<(ND > 0 ? ND : 1)>(acc, ND, ra);
+}
+
+// ------------------------------------------------ K3 / K4, tiled (VEC = 2)
+// Column-chunk order: a CTA owns a tile of TILE = 512 RV rows; each thread
+// holds its RV double2 of w in registers and streams the columns through
+// the tile G at a time (G x RV independent 16-byte loads in flight).  Every
+// warp reads 512-byte runs of one column at a time, which keeps DRAM pages
+// open far better than interleaving all columns per row (measured at c3:
+// 4.8 -> 7.0 TB/s for the block dot, 5.4 -> 6.8 TB/s for the update;
+// scripts/micro/bdot_bench.cu).  The rows past the last whole tile are
+// handled by a row-interleaved tail loop.  Columns are padded to a
+// multiple of GRP by the host (duplicate pointers: surplus dot accumulators
+// are never stored, surplus update coefficients are 0), so every group is
+// loaded whole -- one basic block per group keeps all G x RV loads in flight
+// ahead of the FMAs (a remainder branch let the compiler sink them).
+constexpr int TRV = 2, TG = 4, TILE_ROWS = 512 * TRV;
+
+constexpr int DRV = 4, DG = 2, DTILE_ROWS = 512 * DRV;
+
+template <int NC>
+__global__ void __launch_bounds__(256) bdot_tile_kernel(ColPtrs Q, int ncol, const double* __restrict__ w,
+                                                        int64_t N, RedArgs ra) {
+  constexpr int RV = DRV, G = DG, TILE_ROWS = DTILE_ROWS;
+  double acc[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) acc[c] = 0.0;
+  const int64_t ntile = N / TILE_ROWS;
+#pragma unroll 1
+  for (int64_t t = blockIdx.x; t < ntile; t += gridDim.x) {
+    const int64_t r0 = t * TILE_ROWS + 2 * threadIdx.x;
+    double2 wv[RV];
+#pragma unroll
+    for (int v = 0; v < RV; ++v) wv[v] = __ldg(reinterpret_cast<const double2*>(w + r0 + 512 * v));
+#pragma unroll
+    for (int c = 0; c < NC; c += G) {
+      if (c < ncol) {
+        double2 q[G][RV];
+#pragma unroll
+        for (int u = 0; u < G; ++u)
+#pragma unroll
+          for (int v = 0; v < RV; ++v) {
+            const Vec<2> a = ldv_stream<2>(Q.p[c + u] + r0 + 512 * v);
+            q[u][v] = make_double2(a.v[0], a.v[1]);
+          }
+#pragma unroll
+        for (int u = 0; u < G; ++u)
+#pragma unroll
+          for (int v = 0; v < RV; ++v) {
+            acc[c + u] = fma(q[u][v].x, wv[v].x, acc[c + u]);
+            acc[c + u] = fma(q[u][v].y, wv[v].y, acc[c + u]);
+          }
+      }
+    }
+  }
+  // tail rows (N even: VEC = 2 is only chosen for even N)
+  for (int64_t r = ntile * TILE_ROWS + 2 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x); r < N;
+       r += 2 * (int64_t)gridDim.x * blockDim.x) {
+    const Vec<2> wv = ldv_ro<2>(w + r);
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+      if (c < ncol) {
+        const Vec<2> a = ldv_stream<2>(Q.p[c] + r);
+        acc[c] = fma(a.v[0], wv.v[0], acc[c]);
+        acc[c] = fma(a.v[1], wv.v[1], acc[c]);
+      }
+  }
+  block_reduce_store<NC>(acc, ncol, ra);
+}
+
+template <int NC, int ND>
+__global__ void __launch_bounds__(256) bupd_tile_kernel(ColPtrs Q, int ncol, const double* __restrict__ g,
+                                                        double gs, double* __restrict__ w, int64_t N,
+                                                        const double* d0, const double* d1,
+                                                        const double* d2, RedArgs ra) {
+  constexpr int RV = TRV, G = TG;
+  __shared__ double gsh[NC];
+  for (int c = threadIdx.x; c < NC; c += blockDim.x) gsh[c] = c < ncol ? gs * g[c] : 0.0;
+  __syncthreads();
+  double acc[ND > 0 ? ND : 1];
+#pragma unroll
+  for (int q = 0; q < (ND > 0 ? ND : 1); ++q) acc[q] = 0.0;
+  const double* dv[3] = {d0, d1, d2};
+  auto dots = [&](const double* row, const double2& wn) {
+#pragma unroll
+    for (int q = 0; q < ND; ++q) {
+      double2 o = wn;
+      if (dv[q]) {
+        const Vec<2> a = ldv_ro<2>(dv[q] + (row - w));
+        o = make_double2(a.v[0], a.v[1]);
+      }
+      acc[q] = fma(o.x, wn.x, acc[q]);
+      acc[q] = fma(o.y, wn.y, acc[q]);
+    }
+  };
+  const int64_t ntile = N / TILE_ROWS;
+#pragma unroll 1
+  for (int64_t t = blockIdx.x; t < ntile; t += gridDim.x) {
+    const int64_t r0 = t * TILE_ROWS + 2 * threadIdx.x;
+    double2 wv[RV];
+#pragma unroll
+    for (int v = 0; v < RV; ++v) wv[v] = *reinterpret_cast<const double2*>(w + r0 + 512 * v);
+    // padded columns (host duplicates, coefficient 0) are loaded whole
+#pragma unroll
+    for (int c = 0; c < NC; c += G) {
+      if (c < ncol) {
+        double2 q[G][RV];
+#pragma unroll
+        for (int u = 0; u < G; ++u)
+#pragma unroll
+          for (int v = 0; v < RV; ++v) {
+            const Vec<2> a = ldv_stream<2>(Q.p[c + u] + r0 + 512 * v);
+            q[u][v] = make_double2(a.v[0], a.v[1]);
+          }
+#pragma unroll
+        for (int u = 0; u < G; ++u)
+#pragma unroll
+          for (int v = 0; v < RV; ++v) {
+            wv[v].x = fma(-gsh[c + u], q[u][v].x, wv[v].x);
+            wv[v].y = fma(-gsh[c + u], q[u][v].y, wv[v].y);
+          }
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < RV; ++v) {
+      *reinterpret_cast<double2*>(w + r0 + 512 * v) = wv[v];
+      dots(w + r0 + 512 * v, wv[v]);
+    }
+  }
+  for (int64_t r = ntile * TILE_ROWS + 2 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x); r < N;
+       r += 2 * (int64_t)gridDim.x * blockDim.x) {
+    double2 wn = *reinterpret_cast<const double2*>(w + r);
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+      if (c < ncol) {
+        const Vec<2> a = ldv_stream<2>(Q.p[c] + r);
+        wn.x = fma(-gsh[c], a.v[0], wn.x);
+        wn.y = fma(-gsh[c], a.v[1], wn.y);
+      }
+    *reinterpret_cast<double2*>(w + r) = wn;
+    dots(w + r, wn);
+  }
+  if constexpr (ND > 0) block_reduce_store<(ND > 0 ? ND : 1)>(acc, ND, ra);
+}
+
+// v_{j+1} = w / h_{j+1,j}, with the happy-breakdown test h <= 1e-14 ||A_hat v_j||
+// (reading D18): on breakdown v_{j+1} = 0 and *flag = 1.
+template <int VEC>
+__global__ void __launch_bounds__(256) normalize_kernel(double* __restrict__ w, int64_t N,
+                                                        const double* nrm2, const double* nin2,
+                                                        double* flag) {
+  const double h = sqrt(*nrm2);
+  bool brk = false;
+  if (nin2) brk = !(h > 1e-14 * sqrt(*nin2));
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t NE = N / VEC;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < NE; e += stride) {
+    Vec<VEC> v = ldv<VEC>(w + e * VEC);
+#pragma unroll
+    for (int t = 0; t < VEC; ++t) v.v[t] = brk ? 0.0 : v.v[t] / h;
+    stv<VEC>(w + e * VEC, v);
+  }
+  if (flag && blockIdx.x == 0 && threadIdx.x == 0) *flag = brk ? 1.0 : 0.0;
+}
+
+// ----------------------------------------------------------------- K5
+// out_o = scale_o * sum_c Q_c coef[o][c]  (+ out_o if acc_o), o < nout.
+template <int NC, int VEC>
+__global__ void __launch_bounds__(256) lincomb_kernel(ColPtrs Q, int ncol, const double* __restrict__ coef,
+                                                      int nout, LcOut lo, int64_t N) {
+  __shared__ double cs[MAXOUT][NC];
+  for (int t = threadIdx.x; t < MAXOUT * NC; t += blockDim.x) {
+    const int o = t / NC, c = t % NC;
+    cs[o][c] = (o < nout && c < ncol) ? coef[o * ncol + c] : 0.0;
+  }
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t NE = N / VEC;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < NE; e += stride) {
+    const int64_t r = e * VEC;
+    double s[MAXOUT][VEC];
+#pragma unroll
+    for (int o = 0; o < MAXOUT; ++o)
+#pragma unroll
+      for (int t = 0; t < VEC; ++t) s[o][t] = 0.0;
+#pragma unroll
+    for (int gi = 0; gi < NC / GRP; ++gi) {
+      if (gi * GRP < ncol) {
+        Vec<VEC> q[GRP];
+#pragma unroll
+        for (int u = 0; u < GRP; ++u) q[u] = ldv_stream<VEC>(Q.p[gi * GRP + u] + r);
+#pragma unroll
+        for (int o = 0; o < MAXOUT; ++o) {
+          if (o < nout) {
+#pragma unroll
+            for (int u = 0; u < GRP; ++u)
+#pragma unroll
+              for (int t = 0; t < VEC; ++t) s[o][t] = fma(q[u].v[t], cs[o][gi * GRP + u], s[o][t]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 0; o < MAXOUT; ++o) {
+      if (o < nout) {
+        Vec<VEC> v;
+#pragma unroll
+        for (int t = 0; t < VEC; ++t) v.v[t] = lo.scale[o] * s[o][t];
+        if (lo.acc[o]) {
+          const Vec<VEC> old = ldv<VEC>(lo.out[o] + r);
+#pragma unroll
+          for (int t = 0; t < VEC; ++t) v.v[t] = old.v[t] + v.v[t];
+        }
+        stv<VEC>(lo.out[o] + r, v);
+      }
+    }
+  }
+}
+
+// Projection (Alg. 3 line 1b, Alg. 4 line 1c, reading D20):
+// r <- r - C xi ; x <- x + U xi (x may be null) ; red ||r||^2.
+template <int NC, int VEC>
+__global__ void __launch_bounds__(256) proj_kernel(ColPtrs C, ColPtrs U, int k, const double* __restrict__ xi,
+                                                   double* __restrict__ r, double* __restrict__ x,
+                                                   int64_t N, RedArgs ra) {
+  __shared__ double xs[NC];
+  for (int c = threadIdx.x; c < NC; c += blockDim.x) xs[c] = c < k ? xi[c] : 0.0;
+  __syncthreads();
+  double acc[1] = {0.0};
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t NE = N / VEC;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < NE; e += stride) {
+    const int64_t n = e * VEC;
+    Vec<VEC> cr, ux;
+#pragma unroll
+    for (int t = 0; t < VEC; ++t) cr.v[t] = ux.v[t] = 0.0;
+#pragma unroll
+    for (int gi = 0; gi < NC / GRP; ++gi) {
+      if (gi * GRP < k) {
+        Vec<VEC> q[GRP];
+#pragma unroll
+        for (int u = 0; u < GRP; ++u) q[u] = ldv_stream<VEC>(C.p[gi * GRP + u] + n);
+#pragma unroll
+        for (int u = 0; u < GRP; ++u)
+#pragma unroll
+          for (int t = 0; t < VEC; ++t) cr.v[t] = fma(q[u].v[t], xs[gi * GRP + u], cr.v[t]);
+        if (x) {
+#pragma unroll
+          for (int u = 0; u < GRP; ++u) q[u] = ldv_stream<VEC>(U.p[gi * GRP + u] + n);
+#pragma unroll
+          for (int u = 0; u < GRP; ++u)
+#pragma unroll
+            for (int t = 0; t < VEC; ++t) ux.v[t] = fma(q[u].v[t], xs[gi * GRP + u], ux.v[t]);
+        }
+      }
+    }
+    Vec<VEC> rv = ldv<VEC>(r + n);
+#pragma unroll
+    for (int t = 0; t < VEC; ++t) {
+      rv.v[t] = rv.v[t] - cr.v[t];
+      acc[0] = fma(rv.v[t], rv.v[t], acc[0]);
+    }
+    stv<VEC>(r + n, rv);
+    if (x) {
+      Vec<VEC> xv = ldv<VEC>(x + n);
+#pragma unroll
+      for (int t = 0; t < VEC; ++t) xv.v[t] = xv.v[t] + ux.v[t];
+      stv<VEC>(x + n, xv);
+    }
+  }
+  block_reduce_store<1>(acc, 1, ra);
+}
+
+// In-place column rotation  [q_0 .. q_{k-1}] <- [q_0 .. q_{k-1}] T  (T k x k,
+// column-major): the QR refresh C <- C~ R^-1, U <- U R^-1 (K8).  Each thread
+// owns whole rows, so in-place is race free.
+template <int NC>
+__global__ void __launch_bounds__(256) rotate_kernel(ColPtrs Qc, int k, const double* __restrict__ T,
+                                                     int64_t N) {
+  __shared__ double ts[NC * NC];
+  for (int t = threadIdx.x; t < k * k; t += blockDim.x) ts[t] = T[t];
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; n < N; n += stride) {
+    double in[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+      if (c < k) in[c] = Qc.p[c][n];
+#pragma unroll
+    for (int o = 0; o < NC; ++o) {
+      if (o < k) {
+        double s = 0.0;
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+          if (c < k) s = fma(in[c], ts[o * k + c], s);
+        const_cast<double*>(Qc.p[o])[n] = s;
+      }
+    }
+  }
+}
+
+
+// =================================================================== host
+// bdot launches cover <= 40 columns each (register budget: 40 accumulators).
+void bdot(rk_ctx* ctx, const std::vector<const double*>& cols_all, const double* w, int64_t N,
+          double* out) {
+  const int total = (int)cols_all.size();
+  RK_REQUIRE(total <= MAXCOL, RK_EINVAL, "too many columns in a block product");
+  for (int off = 0; off < total; off += 40) {
+    std::vector<const double*> cols(cols_all.begin() + off,
+                                    cols_all.begin() + std::min(total, off + 40));
+    const int ncol = (int)cols.size();
+    const int nc = nc_round(ncol);
+    const int vec = pick_vec(N, {w}, cols);
+    RedArgs ra = red_args(ctx, out + off);
+    ColPtrs Q = make_cols_padded(cols, nc);
+    const int64_t work = N / vec;
+    Launch L(ctx, "bdot", 8.0 * N * (ncol + 1));
+#define RK_BDOT(NCV)                                                                          \
+  if (vec == 2) launch_k(ctx, bdot_tile_kernel<NCV>, work / DRV, dim3(256), Q, ncol, w, N, ra); \
+  else launch_k(ctx, bdot_kernel<NCV, 1>, work, dim3(256), Q, ncol, w, N, ra);
+    switch (nc) {
+      case 8: RK_BDOT(8); break;
+      case 16: RK_BDOT(16); break;
+      case 24: RK_BDOT(24); break;
+      case 32: RK_BDOT(32); break;
+      default: RK_BDOT(40); break;
+    }
+#undef RK_BDOT
+    L.done();
+    allreduce(ctx, out + off, ncol);
+  }
+}
+
+void bupd(rk_ctx* ctx, const std::vector<const double*>& cols, const double* g, double gscale,
+          double* w, int64_t N, const std::vector<const double*>& dots, double* red_out) {
+  const int ncol = (int)cols.size();
+  const int nd = (int)dots.size();
+  RK_REQUIRE(nd <= 3, RK_EINVAL, "bupd: at most 3 dots");
+  RK_REQUIRE(ncol <= MAXCOL, RK_EINVAL, "too many columns in a block product");
+  const int nc = nc_round(ncol);
+  const int vec = pick_vec(N, {w, nd > 0 ? dots[0] : nullptr, nd > 1 ? dots[1] : nullptr,
+                               nd > 2 ? dots[2] : nullptr}, cols);
+  RedArgs ra = nd ? red_args(ctx, red_out) : RedArgs{nullptr, nullptr, nullptr};
+  ColPtrs Q = make_cols_padded(cols, nc);
+  const double* d[3] = {nullptr, nullptr, nullptr};
+  for (int q = 0; q < nd; ++q) d[q] = dots[q];
+  double words = ncol + 2;
+  for (int q = 0; q < nd; ++q) words += dots[q] ? 1 : 0;
+  const int64_t work = N / vec;
+  Launch L(ctx, "bupd", 8.0 * N * words);
+#define RK_BUPD(NCV, NDV)                                                                      \
+  if (vec == 2)                                                                                \
+    launch_k(ctx, bupd_tile_kernel<NCV, NDV>, work / TRV, dim3(256), Q, ncol, g, gscale, w, N,  \
+             d[0], d[1], d[2], ra);                                                            \
+  else                                                                                         \
+    launch_k(ctx, bupd_kernel<NCV, NDV, 1>, work, dim3(256), Q, ncol, g, gscale, w, N, d[0],   \
+             d[1], d[2], ra);
+#define RK_BUPD_NC(NCV)               \
+  switch (nd) {                       \
+    case 0: RK_BUPD(NCV, 0); break;   \
+    case 1: RK_BUPD(NCV, 1); break;   \
+    case 2: RK_BUPD(NCV, 2); break;   \
+    default: RK_BUPD(NCV, 3); break;  \
+  }
+  switch (nc) {
+    case 8: RK_BUPD_NC(8); break;
+    case 16: RK_BUPD_NC(16); break;
+    case 24: RK_BUPD_NC(24); break;
+    case 32: RK_BUPD_NC(32); break;
+    case 40: RK_BUPD_NC(40); break;
+    case 48: RK_BUPD_NC(48); break;
+    case 56: RK_BUPD_NC(56); break;
+    case 64: RK_BUPD_NC(64); break;
+    case 72: RK_BUPD_NC(72); break;
+    default: RK_BUPD_NC(80); break;
+  }
+#undef RK_BUPD_NC
+#undef RK_BUPD
+  L.done();
+  if (nd) allreduce(ctx, red_out, nd);
+}
+
+void normalize(rk_ctx* ctx, double* w, int64_t N, const double* nrm2, const double* nin2,
+               double* flag) {
+  const int vec = pick_vec(N, {w});
+  Launch L(ctx, "normalize", 16.0 * N);
+  if (vec == 2) launch_k(ctx, normalize_kernel<2>, N / 2, dim3(256), w, N, nrm2, nin2, flag);
+  else launch_k(ctx, normalize_kernel<1>, N, dim3(256), w, N, nrm2, nin2, flag);
+  L.done();
+}
+
+void lincomb(rk_ctx* ctx, const std::vector<const double*>& cols, const double* coef, int nout,
+             const LcOut& lo, int64_t N) {
+  const int ncol = (int)cols.size();
+  RK_REQUIRE(nout >= 1 && nout <= MAXOUT, RK_EINVAL, "lincomb: 1..5 outputs");
+  RK_REQUIRE(ncol >= 1 && ncol <= MAXCOL, RK_EINVAL, "lincomb: 1..80 columns");
+  const int nc = nc_round(ncol);
+  ColPtrs Q = make_cols_padded(cols, nc);
+  int vec = pick_vec(N, {}, cols);
+  for (int o = 0; o < nout; ++o)
+    if (!aligned16(lo.out[o])) vec = 1;
+  double words = ncol;
+  for (int o = 0; o < nout; ++o) words += lo.acc[o] ? 2 : 1;
+  const int64_t work = N / vec;
+  Launch L(ctx, "lincomb", 8.0 * N * words);
+#define RK_LC(NCV)                                                                              \
+  if (vec == 2) launch_k(ctx, lincomb_kernel<NCV, 2>, work, dim3(256), Q, ncol, coef, nout, lo, N); \
+  else launch_k(ctx, lincomb_kernel<NCV, 1>, work, dim3(256), Q, ncol, coef, nout, lo, N);
+  switch (nc) {
+    case 8: RK_LC(8); break;
+    case 16: RK_LC(16); break;
+    case 24: RK_LC(24); break;
+    case 32: RK_LC(32); break;
+    case 40: RK_LC(40); break;
+    case 48: RK_LC(48); break;
+    case 56: RK_LC(56); break;
+    case 64: RK_LC(64); break;
+    case 72: RK_LC(72); break;
+    default: RK_LC(80); break;
+  }
+#undef RK_LC
+  L.done();
+}
+
+void proj(rk_ctx* ctx, const std::vector<const double*>& C, const std::vector<const double*>& U,
+          const double* xi, double* r, double* x, int64_t N, double* red_out) {
+  const int k = (int)C.size();
+  RK_REQUIRE(k >= 1 && k <= 48, RK_EINVAL, "projection supports 1 <= k <= 48");
+  const int nc = nc_round(k);
+  RedArgs ra = red_args(ctx, red_out);
+  ColPtrs Cp = make_cols_padded(C, nc), Up = make_cols_padded(U, nc);
+  int vec = pick_vec(N, {r, x}, C);
+  if (x && pick_vec(N, {}, U) == 1) vec = 1;
+  const int64_t work = N / vec;
+  Launch L(ctx, "proj", 8.0 * N * (k * (x ? 2 : 1) + 2 + (x ? 2 : 0)));
+#define RK_PJ(NCV)                                                                               \
+  if (vec == 2) launch_k(ctx, proj_kernel<NCV, 2>, work, dim3(256), Cp, Up, k, xi, r, x, N, ra); \
+  else launch_k(ctx, proj_kernel<NCV, 1>, work, dim3(256), Cp, Up, k, xi, r, x, N, ra);
+  switch (nc) {
+    case 8: RK_PJ(8); break;
+    case 16: RK_PJ(16); break;
+    case 24: RK_PJ(24); break;
+    case 32: RK_PJ(32); break;
+    case 40: RK_PJ(40); break;
+    default: RK_PJ(48); break;
+  }
+#undef RK_PJ
+  L.done();
+  allreduce(ctx, red_out, 1);
+}
+
+void rotate(rk_ctx* ctx, const std::vector<double*>& cols, const double* T, int64_t N) {
+  const int k = (int)cols.size();
+  if (k == 0) return;
+  const int nc = nc_bucket(k);
+  ColPtrs Q;
+  memset(&Q, 0, sizeof(Q));
+  for (int c = 0; c < k; ++c) Q.p[c] = cols[c];
+  Launch L(ctx, "rotate", 16.0 * N * k);
+  switch (nc) {
+    case 8: launch_k(ctx, rotate_kernel<8>, N, dim3(256), Q, k, T, N); break;
+    case 16: launch_k(ctx, rotate_kernel<16>, N, dim3(256), Q, k, T, N); break;
+    case 32: launch_k(ctx, rotate_kernel<32>, N, dim3(256), Q, k, T, N); break;
+    default: launch_k(ctx, rotate_kernel<48>, N, dim3(256), Q, k, T, N); break;
+  }
+  L.done();
+}
+
+}  // namespace rk

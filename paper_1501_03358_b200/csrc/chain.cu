@@ -6,7 +6,7 @@
 // v = A p_hat) are chains of 6 stencil stages over the SAME bands.  One stage
 // per launch streams the S bands from HBM six times (~(S+3) W per stage).
 // Here NST consecutive stages run in one launch:
-//  * the grid tiles x-y (CTX x CTY interior + an (NST-1)-cell halo that is
+//  * the grid tiles x-y (TX x TY interior + an (NST-1)-cell halo that is
 //    recomputed) and chunks z; each CTA marches through its z range;
 //  * stage s computes plane tau - s at step tau (a wavefront in z) and keeps
 //    the three most recent planes of its output in a shared-memory ring that
@@ -27,6 +27,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "rk_internal.h"
@@ -43,24 +44,26 @@ __host__ __device__ constexpr void coffs(int d, int& dx, int& dy, int& dz) {
   dz = DZ[d];
 }
 
-constexpr int CTX = 32, CTY = 16;  // interior tile of a chain CTA
-
+// Tile geometry.  TX x TY interior cells per CTA plus an (NST-1)-cell halo
+// that is recomputed; PD = TMA prefetch distance in planes (plane tau + PD is
+// issued at step tau, so the data of plane tau + 1 -- waited for at step tau
+// -- was issued PD - 1 steps earlier).
 // TMA box starts must be 16-byte aligned in the innermost (x) dimension, so
 // every box starts at an even x and the shared-memory rows carry PAD cells.
-// Shared memory: NB = 3 band/rhs buffers (plane phase (q - tau0) mod 3; a
-// plane's bands are read into registers by stage 0 and the buffer is free
-// after that step), NXB = 4 input-tile buffers (planes tau-1 .. tau+2, one
-// mbarrier each), and the (NST-1) x 3-plane stage rings.
-template <int ST, int NST>
+// Shared memory: NB = PD + 1 band/rhs buffers (plane q's bands are read into
+// registers by stage 0 at step q), NXB = PD + 2 input-tile buffers (plane q's
+// tile is read at steps q-1 .. q+1; one mbarrier each, which also carries
+// the band/rhs bytes of that plane), and the (NST-1) x 3-plane stage rings.
+template <int ST, int NST, int TX, int TY, int PD>
 struct ChainGeom {
-  static constexpr int CTY_ = CTY;
   static constexpr int HALO = NST - 1;
-  static constexpr int EX = CTX + 2 * HALO, EY = CTY + 2 * HALO;     // stage tile (threads)
+  static constexpr int EX = TX + 2 * HALO, EY = TY + 2 * HALO;        // stage tile (threads)
+  static constexpr int NTHR = EX * EY;
   static constexpr int PADB = HALO % 2;                               // band/rhs box starts at gx0 - PADB
   static constexpr int SX = (EX + PADB + 1) / 2 * 2;                  // band/rhs smem row (even)
   static constexpr int PADX = (HALO + 1) % 2;                         // input box starts at gx0 - 1 - PADX
   static constexpr int XX = (EX + 2 + PADX + 1) / 2 * 2, XY = EY + 2; // input tile (+1 halo)
-  static constexpr int NB = 3, NXB = 4;
+  static constexpr int NB = PD + 1, NXB = PD + 2;
   static constexpr int B_BYTES = ST * EY * SX * 8;
   static constexpr int R_BYTES = EY * SX * 8;
   static constexpr int X_BYTES = XY * XX * 8;
@@ -75,7 +78,7 @@ struct ChainGeom {
   static constexpr int RING_BASE = X_BASE + NXB * XSLOT + GUARD;
   static constexpr int RING = (NST > 1 ? NST - 1 : 1) * 3 * EY * EX * 8;
   static constexpr int BAR_BASE = RING_BASE + al(RING) + GUARD;
-  static constexpr int SMEM = BAR_BASE + 128;
+  static constexpr int SMEM = BAR_BASE + 8 * NXB + 128;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -96,10 +99,10 @@ __device__ __forceinline__ bool mbar_try(uint64_t* b, uint32_t parity) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
       "selp.u32 %0, 1, 0, P1;\n\t}"
       : "=r"(ok)
-      : "r"(smem_u32(b)), "r"(parity), "r"(1000000u)
+      : "r"(smem_u32(b)), "r"(parity)
       : "memory");
   return ok != 0;
 }
@@ -108,7 +111,7 @@ __device__ __forceinline__ bool mbar_try(uint64_t* b, uint32_t parity) {
 // (a reported launch failure) instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   for (uint32_t it = 0; !mbar_try(b, parity); ++it)
-    if (it > (1u << 22)) __trap();
+    if (it > (1u << 26)) __trap();
 }
 
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
@@ -130,32 +133,30 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, u
 }
 
 // One z-step of the chain for loop phase PH = (tau - tau0) mod 3: register
-// sets (bands / rhs / 1/D of the planes stages 0..NST-1 work on), band
-// buffers and ring slots all rotate with PH at compile time.  The code is
-// branch-free per cell: TMA zero-fills every band and input value outside the
-// grid (x/y) and outside [0, nz) (non-periodic z), and the guarded reciprocal
-// 1/D = 0 there, so such cells evaluate to exactly 0 -- the zero-ghost value
-// -- without tests.  Threads outside a stage's shrinking valid region compute
+// sets (bands / rhs / 1/D of the planes stages 0..NST-1 work on) and ring
+// slots rotate with PH at compile time.  The code is branch-free per cell:
+// TMA zero-fills every band and input value outside the grid (x/y) and
+// outside [0, nz) (non-periodic z), and the guarded reciprocal 1/D = 0
+// there, so such cells evaluate to exactly 0 -- the zero-ghost value --
+// without tests.  Threads outside a stage's shrinking valid region compute
 // values nobody reads.
-template <int ST, int NST, int K0, int K1, int K2, int PH>
+template <int ST, int NST, int TX, int TY, int PD, int K0, int K1, int K2, int PH>
 struct ChainStep {
-  using G = ChainGeom<ST, NST>;
+  using G = ChainGeom<ST, NST, TX, TY, PD>;
   static constexpr int EX = G::EX, EY = G::EY, XX = G::XX, SX = G::SX, RPL = EY * EX;
-  static constexpr int HALO = G::HALO;
-  static __device__ __forceinline__ void stage0(int tau, bool st_ok, int pl_tau,
-                                                const unsigned char* smem, int x_m1, int x_0, int x_p1,
-                                                double* ring, double (&bnd)[3][ST], double (&rr)[3],
-                                                double (&inv)[3], int64_t cxy, int xoff, int boff,
-                                                int roff, const ChainParams& cp) {
+  // stage 0 at plane tau: bands / rhs from the band slot `sb`, input
+  // neighbours from the x tiles of planes tau-1, tau, tau+1
+  static __device__ __forceinline__ double stage0(bool st_ok, int pl_tau, const unsigned char* sb,
+                                                  const double* xm, const double* x0,
+                                                  const double* xp, double* ring,
+                                                  double (&bnd)[3][ST], double (&rr)[3],
+                                                  double (&inv)[3], int64_t cxy, int boff, int roff,
+                                                  const ChainParams& cp) {
     constexpr bool LOAD_R = (K0 != CK_SPMV1);
-    const unsigned char* sb = smem + PH * G::BSLOT;
     const double* bs = reinterpret_cast<const double*>(sb) + boff;
 #pragma unroll
     for (int d = 0; d < ST; ++d) bnd[PH][d] = bs[d * EY * SX];
     if (LOAD_R) rr[PH] = reinterpret_cast<const double*>(sb + G::R_OFF)[boff];
-    const double* xm = reinterpret_cast<const double*>(smem + G::X_BASE + x_m1 * G::XSLOT) + xoff;
-    const double* x0 = reinterpret_cast<const double*>(smem + G::X_BASE + x_0 * G::XSLOT) + xoff;
-    const double* xp = reinterpret_cast<const double*>(smem + G::X_BASE + x_p1 * G::XSLOT) + xoff;
     inv[PH] = bnd[PH][0] != 0.0 ? 1.0 / bnd[PH][0] : 0.0;
     double ya = 0.0, yb = 0.0, xc = 0.0;
 #pragma unroll
@@ -185,27 +186,32 @@ struct ChainStep {
       if (NST == 2 && cp.out_mid) cp.out_mid[n] = val;
     }
     if (NST > 1) ring[PH * RPL + roff] = val;
+    return val;
   }
 
-  // stage s at plane q = tau - s (register set / ring slot R of plane q)
+  // stage s at plane q = tau - s (register set / ring slot R of plane q).
+  // `up` is stage s-1's value at plane q+1 for this thread's own cell,
+  // computed earlier in the SAME step; every other input (planes q and q-1)
+  // was written to the ring in earlier steps.  A 7-point stencil reaches
+  // plane q+1 only through its centre (0,0,+1), so a step needs a single
+  // __syncthreads at its end.
   template <int S>
-  static __device__ __forceinline__ void stage(bool st_ok, int pl_q, double* ring,
-                                               double (&bnd)[3][ST], double (&rr)[3],
-                                               double (&inv)[3], int64_t cxy, int roff,
-                                               const ChainParams& cp) {
+  static __device__ __forceinline__ double stage(bool st_ok, int pl_q, double* ring,
+                                                 double (&bnd)[3][ST], double (&rr)[3],
+                                                 double (&inv)[3], int64_t cxy, int roff, double up,
+                                                 const ChainParams& cp) {
+    static_assert(ST == 7, "single-barrier chain steps need a 7-point stencil");
     constexpr int KIND[3] = {K0, K1, K2};
     constexpr int R = (PH - S + 3) % 3;
     const double* rb = ring + (S - 1) * 3 * RPL + roff;
     const double* rm = rb + ((R + 2) % 3) * RPL;
     const double* r0 = rb + R * RPL;
-    const double* rp = rb + ((R + 1) % 3) * RPL;
     double ya = 0.0, yb = 0.0, zc = 0.0;
 #pragma unroll
     for (int d = 0; d < ST; ++d) {
       int dx = 0, dy = 0, dz = 0;
       coffs<ST>(d, dx, dy, dz);
-      const double* rt = dz < 0 ? rm : (dz > 0 ? rp : r0);
-      const double zv = rt[dy * EX + dx];
+      const double zv = dz > 0 ? up : (dz < 0 ? rm[0] : r0[dy * EX + dx]);
       if (d == 0) zc = zv;
       if (d % 2 == 0) ya = fma(bnd[R][d], zv, ya);
       else yb = fma(bnd[R][d], zv, yb);
@@ -218,15 +224,16 @@ struct ChainStep {
       else if (S == NST - 2 && cp.out_mid) cp.out_mid[nq] = val;
     }
     if (S < NST - 1) ring[(S * 3 + R) * RPL + roff] = val;
+    return val;
   }
 };
 
-template <int ST, int NST, int K0, int K1, int K2>
-__global__ void __launch_bounds__((CTX + 2 * (NST - 1)) * (CTY + 2 * (NST - 1)), 1)
+template <int ST, int NST, int TX, int TY, int PD, int K0, int K1, int K2>
+__global__ void __launch_bounds__((TX + 2 * (NST - 1)) * (TY + 2 * (NST - 1)), 1)
 chain_kernel(const __grid_constant__ CUtensorMap map_b, const __grid_constant__ CUtensorMap map_r,
              const __grid_constant__ CUtensorMap map_x, ChainParams cp) {
-  using G = ChainGeom<ST, NST>;
-  constexpr int HALO = G::HALO, EX = G::EX, XX = G::XX, NXB = G::NXB;
+  using G = ChainGeom<ST, NST, TX, TY, PD>;
+  constexpr int HALO = G::HALO, EX = G::EX, XX = G::XX, NXB = G::NXB, NB = G::NB;
   constexpr int SX = G::SX, PADB = G::PADB, PADX = G::PADX;
   constexpr bool LOAD_R = (K0 != CK_SPMV1);
   extern __shared__ __align__(128) unsigned char smem[];
@@ -237,10 +244,10 @@ chain_kernel(const __grid_constant__ CUtensorMap map_b, const __grid_constant__ 
   const int tid = ty * EX + tx;
   const int nx = cp.nx, ny = cp.ny, nz = cp.nz;
   const bool pz = cp.pz != 0;
-  const int gx0 = (int)blockIdx.x * CTX - HALO, gy0 = (int)blockIdx.y * CTY - HALO;
+  const int gx0 = (int)blockIdx.x * TX - HALO, gy0 = (int)blockIdx.y * TY - HALO;
   const int gx = gx0 + tx, gy = gy0 + ty;
   const bool inside = gx >= 0 && gx < nx && gy >= 0 && gy < ny;
-  const bool interior = tx >= HALO && tx < HALO + CTX && ty >= HALO && ty < HALO + CTY;
+  const bool interior = tx >= HALO && tx < HALO + TX && ty >= HALO && ty < HALO + TY;
   const int64_t cxy = inside ? (int64_t)gy * nx + gx : 0;
   const int z0 = (int)blockIdx.z * cp.zc;
   const int z1 = min(nz, z0 + cp.zc);
@@ -251,13 +258,20 @@ chain_kernel(const __grid_constant__ CUtensorMap map_b, const __grid_constant__ 
   const int xoff = (ty + 1) * XX + tx + 1 + PADX;    // own cell in an input tile
   const int boff = ty * SX + tx + PADB;              // own cell in a band / rhs tile
   const int roff = ty * EX + tx;                     // own cell in a ring plane
+  auto pl_of = [&](int q) { return pz ? ((q % nz) + nz) % nz : q; };  // out of range -> TMA zero fill
+  auto xslot = [&](int q) { return (q - qfirst) % NXB; };
+  auto bslot = [&](int q) { return (q - qfirst) % NB; };
+  auto xtile = [&](int q) {
+    return reinterpret_cast<const double*>(smem + G::X_BASE + xslot(q) * G::XSLOT) + xoff;
+  };
 
-  // thread 0: plane q -> band buffer (q - tau0) mod 3, input buffer xs, barrier xs
-  auto issue = [&](int q, int xs) {
-    const int bb = ((q - tau0) % 3 + 3) % 3;
-    unsigned char* bbase = smem + bb * G::BSLOT;
+  // thread 0: all bytes of plane q (bands, rhs, input tile) land on the
+  // mbarrier of q's input-tile slot
+  auto issue = [&](int q) {
+    const int xs = xslot(q);
+    unsigned char* bbase = smem + bslot(q) * G::BSLOT;
     unsigned char* xbase = smem + G::X_BASE + xs * G::XSLOT;
-    const int pl = pz ? ((q % nz) + nz) % nz : q;   // out of range -> TMA zero fill
+    const int pl = pl_of(q);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_expect_tx(&bars[xs], tx_bytes);
     tma_load_4d(bbase, &map_b, &bars[xs], gx0 - PADB, gy0, pl, 0);
@@ -265,21 +279,19 @@ chain_kernel(const __grid_constant__ CUtensorMap map_b, const __grid_constant__ 
     // the input vector is padded: plane pl lives at z-coordinate pl + 1
     tma_load_3d(xbase, &map_x, &bars[xs], gx0 - 1 - PADX, gy0 - 1, pl + 1);
   };
+  auto wait_plane = [&](int q) { mbar_wait(&bars[xslot(q)], (uint32_t)(((q - qfirst) / NXB) & 1)); };
 
   if (tid == 0) {
     for (int s = 0; s < NXB; ++s) mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  // prologue: planes tau0-1, tau0, tau0+1 (input buffers 0, 1, 2)
+  // prologue: planes qfirst .. qfirst + PD (step tau0 issues tau0 + PD)
   if (tid == 0)
-    for (int q = qfirst; q <= min(qfirst + 2, qlast); ++q) issue(q, q - qfirst);
-  mbar_wait(&bars[0], 0);
-  if (qfirst + 1 <= qlast) mbar_wait(&bars[1], 0);
+    for (int q = qfirst; q <= min(qfirst + PD, qlast); ++q) issue(q);
+  wait_plane(qfirst);
+  if (qfirst + 1 <= qlast) wait_plane(qfirst + 1);
 
-  // running input-buffer indices of planes tau-1, tau, tau+1, tau+2 and parity of tau+1
-  int x_m1 = 0, x_0 = 1, x_p1 = 2, x_p2 = 3;
-  uint32_t par_p1 = 0;
   double bnd[3][ST], rr[3], inv[3];
 #pragma unroll
   for (int s = 0; s < 3; ++s) {
@@ -289,40 +301,32 @@ chain_kernel(const __grid_constant__ CUtensorMap map_b, const __grid_constant__ 
     for (int d = 0; d < ST; ++d) bnd[s][d] = 0.0;
   }
   const int tau_end = z1 + HALO;
-  auto pl_of = [&](int q) { return pz ? ((q % nz) + nz) % nz : q; };
 #define RK_CHAIN_STEP(PHV)                                                                         \
   {                                                                                                \
     if (tau >= tau_end) break;                                                                     \
-    if (tid == 0 && tau + 2 <= qlast) issue(tau + 2, x_p2);                                       \
-    if (tau + 1 <= qlast) mbar_wait(&bars[x_p1], par_p1);                                         \
-    using SP = ChainStep<ST, NST, K0, K1, K2, PHV>;                                               \
-    SP::stage0(tau, interior && tau >= z0 && tau < z1 && (pz || tau < nz), pl_of(tau), smem,      \
-               x_m1, x_0, x_p1, ring, bnd, rr, inv, cxy, xoff, boff, roff, cp);                   \
-    __syncthreads();                                                                               \
+    if (tid == 0 && tau + PD <= qlast) issue(tau + PD);                                            \
+    if (tau + 1 <= qlast) wait_plane(tau + 1);                                                     \
+    using SP = ChainStep<ST, NST, TX, TY, PD, K0, K1, K2, PHV>;                                    \
+    const double v0 = SP::stage0(interior && tau >= z0 && tau < z1 && (pz || tau < nz),           \
+                                 pl_of(tau), smem + bslot(tau) * G::BSLOT, xtile(tau - 1),         \
+                                 xtile(tau), xtile(tau + 1), ring, bnd, rr, inv, cxy, boff, roff,  \
+                                 cp);                                                              \
     if constexpr (NST >= 2) {                                                                      \
+      double v1 = 0.0;                                                                             \
       if (tau >= tau0 + 2) {                                                                       \
         const int q = tau - 1;                                                                     \
-        SP::template stage<1>(interior && q >= z0 && q < z1, pl_of(q), ring, bnd, rr, inv, cxy,   \
-                              roff, cp);                                                          \
+        v1 = SP::template stage<1>(interior && q >= z0 && q < z1, pl_of(q), ring, bnd, rr, inv,    \
+                                   cxy, roff, v0, cp);                                             \
       }                                                                                            \
-      __syncthreads();                                                                             \
-    }                                                                                              \
-    if constexpr (NST >= 3) {                                                                      \
-      if (tau >= tau0 + 4) {                                                                       \
-        const int q = tau - 2;                                                                     \
-        SP::template stage<2>(interior && q >= z0 && q < z1, pl_of(q), ring, bnd, rr, inv, cxy,   \
-                              roff, cp);                                                          \
+      if constexpr (NST >= 3) {                                                                    \
+        if (tau >= tau0 + 4) {                                                                     \
+          const int q = tau - 2;                                                                   \
+          SP::template stage<2>(interior && q >= z0 && q < z1, pl_of(q), ring, bnd, rr, inv, cxy, \
+                                roff, v1, cp);                                                     \
+        }                                                                                          \
       }                                                                                            \
-      __syncthreads();                                                                             \
     }                                                                                              \
-    {                                                                                              \
-      const int t = x_m1;                                                                          \
-      x_m1 = x_0;                                                                                  \
-      x_0 = x_p1;                                                                                  \
-      x_p1 = x_p2;                                                                                 \
-      x_p2 = t;                                                                                    \
-      if (x_p1 == 0) par_p1 ^= 1u;                                                                 \
-    }                                                                                              \
+    __syncthreads();                                                                               \
     ++tau;                                                                                         \
   }
   for (int tau = tau0; tau < tau_end;) {
@@ -358,10 +362,11 @@ void encode(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims,
   RK_REQUIRE(r == CUDA_SUCCESS, RK_ECUDA, "cuTensorMapEncodeTiled failed");
 }
 
-template <int ST, int NST, int K0, int K1, int K2>
+template <int ST, int NST, int TX, int TY, int PD, int K0, int K1, int K2>
 void launch_one(rk_op* op, const ChainParams& cp, dim3 grid) {
-  using G = ChainGeom<ST, NST>;
-  auto kern = chain_kernel<ST, NST, K0, K1, K2>;
+  using G = ChainGeom<ST, NST, TX, TY, PD>;
+  static_assert(G::SMEM <= 232448, "chain tile exceeds 227 KB of shared memory");
+  auto kern = chain_kernel<ST, NST, TX, TY, PD, K0, K1, K2>;
   static bool attr = false;
   if (!attr) {
     RK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
@@ -391,28 +396,55 @@ void launch_one(rk_op* op, const ChainParams& cp, dim3 grid) {
   kern<<<grid, blk, G::SMEM, op->ctx->stream>>>(mb, mr, mx, cp);
 }
 
-template <int NST>
+template <int NST, int TX, int TY, int PD>
 void chain_dispatch(rk_op* op, const int* k, const ChainParams& cp, dim3 grid) {
   if constexpr (NST == 3) {
     if (k[0] == CK_SPMV1 && k[1] == CK_SWEEP && k[2] == CK_SWEEP)
-      return launch_one<7, 3, CK_SPMV1, CK_SWEEP, CK_SWEEP>(op, cp, grid);
+      return launch_one<7, 3, TX, TY, PD, CK_SPMV1, CK_SWEEP, CK_SWEEP>(op, cp, grid);
     if (k[0] == CK_SWEEP && k[1] == CK_SWEEP && k[2] == CK_SWEEP)
-      return launch_one<7, 3, CK_SWEEP, CK_SWEEP, CK_SWEEP>(op, cp, grid);
+      return launch_one<7, 3, TX, TY, PD, CK_SWEEP, CK_SWEEP, CK_SWEEP>(op, cp, grid);
     if (k[0] == CK_SWEEP && k[1] == CK_SWEEP && k[2] == CK_SPMV)
-      return launch_one<7, 3, CK_SWEEP, CK_SWEEP, CK_SPMV>(op, cp, grid);
+      return launch_one<7, 3, TX, TY, PD, CK_SWEEP, CK_SWEEP, CK_SPMV>(op, cp, grid);
   } else if constexpr (NST == 2) {
     if (k[0] == CK_SPMV1 && k[1] == CK_SWEEP)
-      return launch_one<7, 2, CK_SPMV1, CK_SWEEP, 0>(op, cp, grid);
+      return launch_one<7, 2, TX, TY, PD, CK_SPMV1, CK_SWEEP, 0>(op, cp, grid);
     if (k[0] == CK_SWEEP && k[1] == CK_SWEEP)
-      return launch_one<7, 2, CK_SWEEP, CK_SWEEP, 0>(op, cp, grid);
+      return launch_one<7, 2, TX, TY, PD, CK_SWEEP, CK_SWEEP, 0>(op, cp, grid);
     if (k[0] == CK_SWEEP && k[1] == CK_SPMV)
-      return launch_one<7, 2, CK_SWEEP, CK_SPMV, 0>(op, cp, grid);
+      return launch_one<7, 2, TX, TY, PD, CK_SWEEP, CK_SPMV, 0>(op, cp, grid);
   } else {
-    if (k[0] == CK_SPMV1) return launch_one<7, 1, CK_SPMV1, 0, 0>(op, cp, grid);
-    if (k[0] == CK_SWEEP) return launch_one<7, 1, CK_SWEEP, 0, 0>(op, cp, grid);
-    return launch_one<7, 1, CK_SPMV, 0, 0>(op, cp, grid);
+    if (k[0] == CK_SPMV1) return launch_one<7, 1, TX, TY, PD, CK_SPMV1, 0, 0>(op, cp, grid);
+    if (k[0] == CK_SWEEP) return launch_one<7, 1, TX, TY, PD, CK_SWEEP, 0, 0>(op, cp, grid);
+    return launch_one<7, 1, TX, TY, PD, CK_SPMV, 0, 0>(op, cp, grid);
   }
   throw Error(RK_EINVAL, "unsupported chain stage combination");
+}
+
+// Tile configurations (interior TX x TY, prefetch distance PD).  RK_CHAIN_CFG
+// (read per launch; experiments only) selects one by index.
+struct TileCfg {
+  int tx, ty, pd;
+};
+constexpr TileCfg CFGS[] = {{32, 16, 2}, {32, 8, 3}, {32, 8, 4}, {16, 16, 3}, {16, 16, 4}, {64, 8, 2}};
+constexpr int NCFG = sizeof(CFGS) / sizeof(CFGS[0]);
+constexpr int DEFAULT_CFG = 0;
+
+int cfg_index() {
+  const char* e = std::getenv("RK_CHAIN_CFG");
+  const int i = e ? std::atoi(e) : DEFAULT_CFG;
+  return (i >= 0 && i < NCFG) ? i : DEFAULT_CFG;
+}
+
+template <int NST>
+void chain_dispatch_cfg(int ci, rk_op* op, const int* k, const ChainParams& cp, dim3 grid) {
+  switch (ci) {
+    case 0: return chain_dispatch<NST, 32, 16, 2>(op, k, cp, grid);
+    case 1: return chain_dispatch<NST, 32, 8, 3>(op, k, cp, grid);
+    case 2: return chain_dispatch<NST, 32, 8, 4>(op, k, cp, grid);
+    case 3: return chain_dispatch<NST, 16, 16, 3>(op, k, cp, grid);
+    case 4: return chain_dispatch<NST, 16, 16, 4>(op, k, cp, grid);
+    default: return chain_dispatch<NST, 64, 8, 2>(op, k, cp, grid);
+  }
 }
 
 }  // namespace
@@ -421,14 +453,22 @@ int chain_max_stages(const rk_op* op) {
   if (op->ctx->nranks != 1 || op->no_chain) return 0;      // deep halos not exchanged (yet)
   if (op->S != 7) return 0;
   if (op->g.periodic_mask & 3) return 0;                    // TMA boxes do not wrap in x/y
-  if (op->g.nx % CTX != 0 || op->g.ny % CTY != 0 || op->g.nx % 2 != 0) return 0;
+  const TileCfg tc = CFGS[cfg_index()];
+  if (op->g.nx % tc.tx != 0 || op->g.ny % tc.ty != 0 || op->g.nx % 2 != 0) return 0;
   if (op->g.nz_local < 16) return 0;
+  // While the bands and the sweep vectors fit in L2 the one-stage-per-launch
+  // path re-reads them from L2, not HBM, and wins (64^3: 46 vs 63 us per
+  // M^-1); the chain pays off once a stage's traffic exceeds L2.
+  if (!op->force_chain && (double)(op->S + 3) * 8.0 * (double)op->N <= (double)op->ctx->l2_bytes)
+    return 0;
   return 3;
 }
 
 void chain_launch(rk_op* op, int nst, const int* kinds, const double* omegas, const double* xin,
                   const double* r, double* out_t, double* out_mid, double* out) {
   rk_ctx* ctx = op->ctx;
+  const int ci = cfg_index();
+  const TileCfg tc = CFGS[ci];
   ChainParams cp;
   std::memset(&cp, 0, sizeof(cp));
   cp.bands = op->bands;
@@ -446,8 +486,8 @@ void chain_launch(rk_op* op, int nst, const int* kinds, const double* omegas, co
   cp.out_mid = out_mid;
   cp.out = out;
   for (int s = 0; s < nst; ++s) cp.omega[s] = omegas[s];
-  const int tiles = (int)((op->g.nx / CTX) * (op->g.ny / CTY));
-  // z chunks: one resident CTA per SM (the slot ring uses ~200 KB of shared
+  const int tiles = (int)((op->g.nx / tc.tx) * (op->g.ny / tc.ty));
+  // z chunks: one resident CTA per SM (the slot rings use most of the shared
   // memory), so aim for a single wave -- chunks = SMs / tiles (>= 1), long
   // chunks to amortise the 2 (NST-1)-plane wavefront prologue
   const int nz = (int)op->g.nz_local;
@@ -455,14 +495,14 @@ void chain_launch(rk_op* op, int nst, const int* kinds, const double* omegas, co
   int zc = (nz + chunks - 1) / chunks;
   zc = std::max(1, std::min(zc, nz));
   cp.zc = zc;
-  dim3 grid((unsigned)(op->g.nx / CTX), (unsigned)(op->g.ny / CTY), (unsigned)((nz + zc - 1) / zc));
+  dim3 grid((unsigned)(op->g.nx / tc.tx), (unsigned)(op->g.ny / tc.ty), (unsigned)((nz + zc - 1) / zc));
   // algorithmic bytes: bands once + stage-0 input + rhs (if any) + outputs
   const double words = op->S + 1 + ((kinds[0] != CK_SPMV1) ? 1 : 0) + 1 + (out_t ? 1 : 0) +
                        (out_mid ? 1 : 0);
   Launch L(ctx, "chain", 8.0 * op->N * words);
-  if (nst == 3) chain_dispatch<3>(op, kinds, cp, grid);
-  else if (nst == 2) chain_dispatch<2>(op, kinds, cp, grid);
-  else chain_dispatch<1>(op, kinds, cp, grid);
+  if (nst == 3) chain_dispatch_cfg<3>(ci, op, kinds, cp, grid);
+  else if (nst == 2) chain_dispatch_cfg<2>(ci, op, kinds, cp, grid);
+  else chain_dispatch_cfg<1>(ci, op, kinds, cp, grid);
   L.done();
 }
 

@@ -1,0 +1,223 @@
+// Shared device helpers and launch utilities of the librk kernel translation
+// units (stencil.cu, blockops.cu, bicg.cu).  Not part of the ABI.
+//
+// Every librk kernel is HBM-bound fp64 work on the CUDA cores (0.1-0.3
+// flop/B, SURVEY §8(a) "Tensor cores"):
+//  * coalesced x-fastest rows, 16-byte loads wherever the data allows;
+//  * streaming (ld.global.nc.L1::no_allocate) loads for data read once per
+//    launch (bands, basis columns);
+//  * grids sized from each instantiation's occupancy: SMs x resident CTAs,
+//    grid-stride loops;
+//  * deterministic two-stage reductions (per-CTA partials + fixed-order
+//    finalisation by the last CTA; no floating-point atomics).
+#pragma once
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <initializer_list>
+
+#include "rk_internal.h"
+
+namespace rk {
+
+
+// ------------------------------------------------------------------ helpers
+template <int VEC>
+struct Vec {
+  double v[VEC];
+};
+
+template <int VEC>
+__device__ __forceinline__ Vec<VEC> ldv_stream(const double* p) {
+  Vec<VEC> r;
+  if constexpr (VEC == 2) {
+    asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(r.v[0]), "=d"(r.v[1]) : "l"(p));
+  } else {
+    asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r.v[0]) : "l"(p));
+  }
+  return r;
+}
+
+// read-only (non-coherent) path: data not written by the same launch
+template <int VEC>
+__device__ __forceinline__ Vec<VEC> ldv_ro(const double* p) {
+  Vec<VEC> r;
+  if constexpr (VEC == 2) {
+    const double2 t = __ldg(reinterpret_cast<const double2*>(p));
+    r.v[0] = t.x;
+    r.v[1] = t.y;
+  } else {
+    r.v[0] = __ldg(p);
+  }
+  return r;
+}
+
+template <int VEC>
+__device__ __forceinline__ Vec<VEC> ldv(const double* p) {
+  Vec<VEC> r;
+  if constexpr (VEC == 2) {
+    const double2 t = *reinterpret_cast<const double2*>(p);
+    r.v[0] = t.x;
+    r.v[1] = t.y;
+  } else {
+    r.v[0] = *p;
+  }
+  return r;
+}
+
+template <int VEC>
+__device__ __forceinline__ void stv(double* p, const Vec<VEC>& a) {
+  if constexpr (VEC == 2) {
+    *reinterpret_cast<double2*>(p) = make_double2(a.v[0], a.v[1]);
+  } else {
+    *p = a.v[0];
+  }
+}
+
+// Canonical stencil layouts.  Band 0 is the diagonal.
+//  7: 0, -x, +x, -y, +y, -z, +z
+// 19: 7-point + xy edges (-1,-1)(1,-1)(-1,1)(1,1), yz edges (y,z) = (-1,-1)(1,-1)(-1,1)(1,1),
+//     xz edges (x,z) = (-1,-1)(1,-1)(-1,1)(1,1)
+// 27: centre, then the other 26 offsets in lexicographic (dz, dy, dx) order.
+template <int ST>
+__host__ __device__ constexpr void offs(int d, int& dx, int& dy, int& dz) {
+  if (ST == 27) {
+    const int e = d == 0 ? 13 : (d <= 13 ? d - 1 : d);
+    dx = e % 3 - 1;
+    dy = (e / 3) % 3 - 1;
+    dz = e / 9 - 1;
+    return;
+  }
+  constexpr int DX[19] = {0, -1, 1, 0, 0, 0, 0, -1, 1, -1, 1, 0, 0, 0, 0, -1, 1, -1, 1};
+  constexpr int DY[19] = {0, 0, 0, -1, 1, 0, 0, -1, -1, 1, 1, -1, 1, -1, 1, 0, 0, 0, 0};
+  constexpr int DZ[19] = {0, 0, 0, 0, 0, -1, 1, 0, 0, 0, 0, -1, -1, 1, 1, -1, -1, 1, 1};
+  dx = DX[d];
+  dy = DY[d];
+  dz = DZ[d];
+}
+
+template <int ST>
+__host__ __device__ constexpr bool uses(int dx, int dy, int dz) {
+  for (int d = 0; d < ST; ++d) {
+    int a = 0, b = 0, c = 0;
+    offs<ST>(d, a, b, c);
+    if (a == dx && b == dy && c == dz) return true;
+  }
+  return false;
+}
+
+// Block reduction of NV per-thread values -> per-CTA partials -> the last CTA
+// to finish sums the partials of every value in a fixed order (deterministic).
+template <int NV>
+__device__ __forceinline__ void block_reduce_store(const double (&v)[NV], int nv,
+                                                   const RedArgs& ra) {
+  __shared__ double sm[NV][33];
+  __shared__ bool last;
+  const int tid = threadIdx.x + threadIdx.y * blockDim.x;
+  const int nthreads = blockDim.x * blockDim.y;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = (nthreads + 31) >> 5;
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    if (q < nv) {
+      double s = v[q];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+      if (lane == 0) sm[q][warp] = s;
+    }
+  }
+  __syncthreads();
+  const int G = gridDim.x;
+  for (int q = warp; q < nv; q += nwarps) {
+    double s = lane < nwarps ? sm[q][lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if (lane == 0) ra.partials[(int64_t)q * G + blockIdx.x] = s;
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) last = (atomicAdd(ra.counter, 1u) == (unsigned)(G - 1));
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    for (int q = warp; q < nv; q += nwarps) {
+      double s = 0.0;
+      for (int c = lane; c < G; c += 32) s += __ldcg(ra.partials + (int64_t)q * G + c);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+      if (lane == 0) ra.out[q] = s;
+    }
+    if (tid == 0) atomicExch(ra.counter, 0u);
+  }
+}
+
+
+// Columns are processed in groups of 8 with unguarded loads (the host pads
+// the last group with a duplicate pointer and zero coefficients), so every
+// thread keeps 8 x VEC loads in flight per group.
+constexpr int GRP = 8;
+
+// =================================================================== host
+namespace {
+
+
+// Grid = min(work / CTA, SMs x resident CTAs of this instantiation).
+template <typename... KArgs, typename... Args>
+void launch_k(rk_ctx* ctx, void (*kern)(KArgs...), int64_t work_threads, dim3 blk,
+              Args&&... args) {
+  const int threads = (int)(blk.x * blk.y);
+  auto it = ctx->occ_cache.find((const void*)kern);
+  int occ;
+  if (it == ctx->occ_cache.end()) {
+    RK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, 0));
+    occ = std::max(1, occ);
+    ctx->occ_cache[(const void*)kern] = occ;
+  } else {
+    occ = it->second;
+  }
+  const int64_t want = std::max<int64_t>(1, (work_threads + threads - 1) / threads);
+  const int grid = (int)std::min<int64_t>(want, (int64_t)ctx->sms * occ);
+  kern<<<grid, blk, 0, ctx->stream>>>(std::forward<Args>(args)...);
+}
+
+inline RedArgs red_args(rk_ctx* ctx, double* out) {
+  return RedArgs{ctx->partials, ctx->counter, out};
+}
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// VEC = 2 iff N is even and every pointer is 16-byte aligned.
+inline int pick_vec(int64_t N, std::initializer_list<const void*> ps,
+             const std::vector<const double*>& cols = {}) {
+  if (N & 1) return 1;
+  for (auto p : ps)
+    if (p && !aligned16(p)) return 1;
+  for (auto p : cols)
+    if (p && !aligned16(p)) return 1;
+  return 2;
+}
+
+// Pad to a multiple of GRP with the first column of the last group.
+inline ColPtrs make_cols_padded(const std::vector<const double*>& v, int nc) {
+  ColPtrs c;
+  memset(&c, 0, sizeof(c));
+  for (size_t i = 0; i < v.size(); ++i) c.p[i] = v[i];
+  for (int i = (int)v.size(); i < nc && !v.empty(); ++i) {
+    const int g0 = (i / GRP) * GRP;
+    c.p[i] = v[g0 < (int)v.size() ? g0 : 0];
+  }
+  return c;
+}
+
+inline int nc_round(int n) { return ((std::max(n, 1) + GRP - 1) / GRP) * GRP; }
+
+inline int nc_bucket(int n) {
+  if (n <= 8) return 8;
+  if (n <= 16) return 16;
+  if (n <= 32) return 32;
+  RK_REQUIRE(n <= 48, RK_EINVAL, "rotation supports k <= 48");
+  return 48;
+}
+
+}  // namespace
+
+}  // namespace rk

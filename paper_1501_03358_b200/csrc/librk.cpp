@@ -2,7 +2,7 @@
 // of rGCROT(m,k) (Alg. 3), rBiCGStab with one recycle space
 // (Alg. 4) and their k = 0 cases GMRES(m) / BiCGStab (Alg. 1 / 2).
 //
-// All N-length work runs in the sm_100a kernels of kernels.cu; this file
+// All N-length work runs in the sm_100a kernels (stencil.cu, chain.cu, blockops.cu, bicg.cu); this file
 // only sequences them, keeps the tiny dense algebra (Hessenberg least
 // squares, line-14a coefficient-space algebra, k x k Cholesky) on the host
 // and reads back a handful of scalars per rGCROT cycle / rBiCGStab
@@ -811,6 +811,7 @@ rk_status rk_op_create(rk_ctx* ctx, const rk_grid* g, int nbands, const int8_t* 
                      std::to_string(bad) + " bad coefficients");
       op->user_offsets.assign(offsets, offsets + 3 * nbands);
       op->no_chain = std::getenv("RK_NO_CHAIN") != nullptr;
+      op->force_chain = std::getenv("RK_FORCE_CHAIN") != nullptr;
     } catch (...) {
       cudaFree(op->bands);
       delete op;

@@ -125,6 +125,7 @@ struct ProfAgg {
 
 struct rk_ctx {
   int device = 0, rank = 0, nranks = 1, sms = 148;
+  int64_t l2_bytes = 0;         // L2 capacity (chain policy)
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   double* partials = nullptr;
@@ -162,6 +163,7 @@ struct rk_op {
   int wrapz = 0;
   std::vector<int8_t> user_offsets;   // caller's band order (for rk_op_update_bands)
   bool no_chain = false;              // env RK_NO_CHAIN: disable the fused TMA chain
+  bool force_chain = false;           // env RK_FORCE_CHAIN: use it below the L2 threshold (tests)
 };
 
 namespace rk {
@@ -212,7 +214,7 @@ void chain_run(rk_op* op, const std::vector<int>& kinds, const std::vector<doubl
                double* za, double* zb);
 
 // ------------------------------------------------------------ launch layer
-// All kernels are launched through these wrappers (kernels.cu).  Each
+// All kernels are launched through these wrappers (stencil.cu, blockops.cu, bicg.cu).  Each
 // increments ctx->launches and, when profiling, is bracketed by events.
 void init_ctx_kernels(rk_ctx* ctx);
 void stencil(rk_op* op, int mode, const double* x, const double* r, double* out0,

@@ -78,6 +78,8 @@ WORKLOADS = {
     "c1s": Workload("c1s", lambda: convection_diffusion_c1(8), _rg(10, 6, 1), 1),
     "c2s": Workload("c2s", lambda: channel19(16), _rg(12, 8, 1), 6),
     "c3s": Workload("c3s", lambda: porous7(24, 3), _hy(8, 8, 2), 8),
+    # 32^3: the smallest porous grid the fused TMA chain tiles (nx % 32, ny % 16)
+    "c3m": Workload("c3m", lambda: porous7(32, 3), _hy(8, 8, 2), 6),
     "c4s": Workload("c4s", lambda: channel19(16), _rg(12, 10, 1), 9, epoch_every=3),
     "c4hs": Workload("c4hs", lambda: channel19(16), _hy(12, 10, 1), 9, epoch_every=3),
 }

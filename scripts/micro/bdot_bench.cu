@@ -20,7 +20,10 @@ __device__ __forceinline__ void mbar_expect(uint64_t* b, uint32_t bytes) { asm v
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) { asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory"); }
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t par) {
   uint32_t ok = 0;
-  while (!ok) asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\tselp.u32 %0, 1, 0, P1;\n\t}" : "=r"(ok) : "r"(su32(b)), "r"(par) : "memory");
+  for (uint32_t n = 0; !ok; ++n) {
+    if (n > (1u << 26)) __trap();
+    asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\tselp.u32 %0, 1, 0, P1;\n\t}" : "=r"(ok) : "r"(su32(b)), "r"(par) : "memory");
+  }
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
@@ -248,6 +251,69 @@ __global__ void __launch_bounds__(288, 1) bupd_v3(ColPtrs Q, int ncol, const dou
   }
 }
 
+
+// ---------------- V4: column-chunk, w in registers, G columns per group
+template <int NC, int RV, int G>
+__global__ void __launch_bounds__(256) bdot_v4(ColPtrs Q, int ncol, const double* __restrict__ w, int64_t N, double* out) {
+  double acc[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) acc[c] = 0.0;
+  const int64_t tile = 256 * 2 * RV;
+  for (int64_t t0 = (int64_t)blockIdx.x * tile; t0 < N; t0 += (int64_t)gridDim.x * tile) {
+    double2 wv[RV];
+#pragma unroll
+    for (int v = 0; v < RV; ++v) wv[v] = __ldg(reinterpret_cast<const double2*>(w + t0 + (v * 256 + threadIdx.x) * 2));
+#pragma unroll
+    for (int c = 0; c < NC; c += G) {
+      if (c < ncol) {
+        double2 q[G][RV];
+#pragma unroll
+        for (int g = 0; g < G; ++g)
+#pragma unroll
+          for (int v = 0; v < RV; ++v) q[g][v] = ldst(Q.p[c + g] + t0 + (v * 256 + threadIdx.x) * 2);
+#pragma unroll
+        for (int g = 0; g < G; ++g)
+#pragma unroll
+          for (int v = 0; v < RV; ++v) { acc[c + g] = fma(q[g][v].x, wv[v].x, acc[c + g]); acc[c + g] = fma(q[g][v].y, wv[v].y, acc[c + g]); }
+      }
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) s += acc[c];
+  if (threadIdx.x == 0) out[blockIdx.x] = s;
+}
+
+// ---------------- bupd V2: column-chunk, w tile in registers, G columns per group
+template <int NC, int RV, int G>
+__global__ void __launch_bounds__(256) bupd_v2(ColPtrs Q, int ncol, const double* __restrict__ g, double* __restrict__ w, int64_t N) {
+  __shared__ double gsh[NC];
+  for (int c = threadIdx.x; c < NC; c += blockDim.x) gsh[c] = c < ncol ? g[c] : 0.0;
+  __syncthreads();
+  const int64_t tile = 256 * 2 * RV;
+  for (int64_t t0 = (int64_t)blockIdx.x * tile; t0 < N; t0 += (int64_t)gridDim.x * tile) {
+    double2 wv[RV];
+#pragma unroll
+    for (int v = 0; v < RV; ++v) wv[v] = *reinterpret_cast<const double2*>(w + t0 + (v * 256 + threadIdx.x) * 2);
+#pragma unroll
+    for (int c = 0; c < NC; c += G) {
+      if (c < ncol) {
+        double2 q[G][RV];
+#pragma unroll
+        for (int gg = 0; gg < G; ++gg)
+#pragma unroll
+          for (int v = 0; v < RV; ++v) q[gg][v] = ldst(Q.p[c + gg] + t0 + (v * 256 + threadIdx.x) * 2);
+#pragma unroll
+        for (int gg = 0; gg < G; ++gg)
+#pragma unroll
+          for (int v = 0; v < RV; ++v) { wv[v].x = fma(-gsh[c + gg], q[gg][v].x, wv[v].x); wv[v].y = fma(-gsh[c + gg], q[gg][v].y, wv[v].y); }
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < RV; ++v) *reinterpret_cast<double2*>(w + t0 + (v * 256 + threadIdx.x) * 2) = wv[v];
+  }
+}
+
 __global__ void rd_kernel(const double* __restrict__ a, int64_t N, double* out) {
   double s = 0;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < N / 2; e += (int64_t)gridDim.x * blockDim.x) {
@@ -276,6 +342,7 @@ float timeit(F f, int reps = 20) {
 }
 
 int main(int argc, char** argv) {
+  if (argc > 2 && atoi(argv[2]) > 24) { printf("ncol must be <= 24 (template NC)\n"); return 1; }
   const int64_t N = argc > 1 ? atoll(argv[1]) : (1 << 21);
   const int ncol = argc > 2 ? atoi(argv[2]) : 20;
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -334,6 +401,25 @@ int main(int argc, char** argv) {
     const int smem = ST * TR * 8 + 2 * ST * 8;
     CK(cudaFuncSetAttribute(bupd_v3<24, TR, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     rep("bupd_v3<24,512,24> tma 2/SM", timeit([&] { bupd_v3<24, TR, ST><<<sms * 2, 288, smem>>>(Q, ncol, g, w, N); }), ncol + 2);
+  }
+  for (int occ : {2, 3, 4, 6}) {
+    char nm[64];
+    snprintf(nm, 64, "bdot_v4<24,4,2> grid %dx", occ);
+    rep(nm, timeit([&] { bdot_v4<24, 4, 2><<<sms * occ, 256>>>(Q, ncol, w, N, out); }), ncol + 1);
+    snprintf(nm, 64, "bdot_v4<24,4,4> grid %dx", occ);
+    rep(nm, timeit([&] { bdot_v4<24, 4, 4><<<sms * occ, 256>>>(Q, ncol, w, N, out); }), ncol + 1);
+    snprintf(nm, 64, "bdot_v4<24,8,1> grid %dx", occ);
+    rep(nm, timeit([&] { bdot_v4<24, 8, 1><<<sms * occ, 256>>>(Q, ncol, w, N, out); }), ncol + 1);
+    snprintf(nm, 64, "bdot_v4<24,2,4> grid %dx", occ);
+    rep(nm, timeit([&] { bdot_v4<24, 2, 4><<<sms * occ, 256>>>(Q, ncol, w, N, out); }), ncol + 1);
+    snprintf(nm, 64, "bupd_v2<24,4,2> grid %dx", occ);
+    rep(nm, timeit([&] { bupd_v2<24, 4, 2><<<sms * occ, 256>>>(Q, ncol, g, w, N); }), ncol + 2);
+    snprintf(nm, 64, "bupd_v2<24,4,1> grid %dx", occ);
+    rep(nm, timeit([&] { bupd_v2<24, 4, 1><<<sms * occ, 256>>>(Q, ncol, g, w, N); }), ncol + 2);
+    snprintf(nm, 64, "bupd_v2<24,2,4> grid %dx", occ);
+    rep(nm, timeit([&] { bupd_v2<24, 2, 4><<<sms * occ, 256>>>(Q, ncol, g, w, N); }), ncol + 2);
+    snprintf(nm, 64, "bupd_v2<24,8,1> grid %dx", occ);
+    rep(nm, timeit([&] { bupd_v2<24, 8, 1><<<sms * occ, 256>>>(Q, ncol, g, w, N); }), ncol + 2);
   }
   printf("done\n");
   return 0;

@@ -126,6 +126,59 @@ def test_precond_parity(rk, ctx, name, mk):
     op.close()
 
 
+# Fused TMA chain (chain.cu): 3 stencil stages per launch.  It runs for
+# 7-point operators with non-periodic x/y, nx % 32 == 0, ny % 16 == 0 and
+# nz >= 16 on one rank; these cases span several x-y tiles, several z
+# chunks, a ragged last z chunk and a periodic z axis.
+CHAIN_CASES = [
+    ("porous_c3_full", lambda: porous7(128, 6)),
+    ("random_96x48x40", lambda: _random7(96, 48, 40, 0, 21)),
+    ("random_64x32x48_pz", lambda: _random7(64, 32, 48, 4, 22)),
+]
+
+
+def _random7(nx, ny, nz, periodic, seed):
+    from problems.stencils import StencilProblem
+    bands = random_op_problem(nx, ny, nz, periodic, OFFSETS7, seed)
+    return StencilProblem(name="random7", nx=nx, ny=ny, nz=nz, periodic=periodic,
+                          offsets=np.asarray(OFFSETS7), _band_fn=lambda z0, z1: bands[:, z0:z1].copy())
+
+
+@pytest.mark.parametrize("name,mk", CHAIN_CASES, ids=[c[0] for c in CHAIN_CASES])
+def test_precond_parity_chain(rk, ctx, name, mk, monkeypatch):
+    prob = mk()
+    monkeypatch.setenv("RK_FORCE_CHAIN", "1")      # below the L2 threshold too
+    op = make_op(rk, ctx, prob)
+    monkeypatch.delenv("RK_FORCE_CHAIN")
+    ref = Operator.from_problem(prob)
+    r = np.random.default_rng(5).uniform(-1, 1, prob.N)
+    z = op.precond(dev(r)).cpu().numpy()
+    zr = Jacobi(ref)(r)
+    assert np.max(np.abs(z - zr)) <= 1e-12 * np.max(np.abs(zr))
+    op.close()
+
+
+@pytest.mark.parametrize("shape,periodic", [((64, 32, 48), 4), ((32, 16, 17), 4), ((96, 48, 40), 0)])
+def test_chain_bitwise_equals_unfused(rk, ctx, shape, periodic, monkeypatch):
+    """The fused chain and the one-stage-per-launch stencil path share the
+    per-cell arithmetic (two FMA chains, 1/D), so M^-1 r and M^-1 A v agree
+    bit for bit; RK_NO_CHAIN (read at rk_op_create) selects the unfused path."""
+    nx, ny, nz = shape
+    bands = dev(random_op_problem(nx, ny, nz, periodic, OFFSETS7, 11))
+    mk = lambda: rk.GridOperator(ctx, nx, ny, nz, OFFSETS7, bands, periodic)
+    monkeypatch.setenv("RK_FORCE_CHAIN", "1")
+    fused = mk()
+    monkeypatch.delenv("RK_FORCE_CHAIN")
+    monkeypatch.setenv("RK_NO_CHAIN", "1")
+    plain = mk()
+    monkeypatch.delenv("RK_NO_CHAIN")
+    r = dev(np.random.default_rng(2).uniform(-1, 1, nx * ny * nz))
+    a, b = fused.precond(r), plain.precond(r)
+    assert torch.equal(a, b)
+    fused.close()
+    plain.close()
+
+
 # ------------------------------------------------------------ solves
 def gpu_sequence(rk, ctx, w, solver_name=None, host=False):
     prob = w.problem()
@@ -195,6 +248,17 @@ def test_sequence_parity(rk, ctx, name, solver):
     ora = run_sequence(w, solver=method)
     gpu, _ = gpu_sequence(rk, ctx, w, method)
     compare_sequences(w, gpu, ora, method)
+
+
+def test_sequence_parity_fused_chain(rk, ctx, monkeypatch):
+    """Hybrid sequence with every preconditioned operator application
+    through the fused TMA chain (forced below its L2 threshold)."""
+    w = get_workload("c3m")
+    ora = run_sequence(w)
+    monkeypatch.setenv("RK_FORCE_CHAIN", "1")
+    gpu, _ = gpu_sequence(rk, ctx, w)
+    monkeypatch.delenv("RK_FORCE_CHAIN")
+    compare_sequences(w, gpu, ora, w.params.method)
 
 
 def test_gmres_stagnation_parity(rk, ctx):
