@@ -83,7 +83,10 @@ typedef struct {
   int k_keep;          /* k_t: dimension after truncation       */
   int select_count;    /* p1: candidates added per cycle, 0..2  */
   int ortho;           /* 0 = CGS2 (block classical Gram-Schmidt, twice)    */
-  int trunc;           /* 0 = T1 (drop oldest)                              */
+  int trunc;           /* 0 = T1 (drop the oldest columns);     
+                        * 1 = T2 (keep the directions of range(C) with the 
+                        * smallest principal angles to the cycle's image  
+                        * space A_hat V_m; R13)       */
   rk_precond pc;
   double tol;          /* default tolerance (rk_solve's tol overrides)      */
   int64_t max_matvecs; /* Krylov matvec budget per solve (paper: 2000)      */

@@ -82,8 +82,9 @@ def gcrot_update(U, C, V, H, B, y, dx, rho, prm):
     smaller j), h* = H_(:, j*), u = v_j* - U B(:, j*) satisfies
     A_hat u = V_{m+1} h*; it is orthogonalised against c1 in coefficient
     space.  Truncation T1: if k + p > k_max keep the newest k_t - p old
-    columns (drop the oldest).  Columns are ordered oldest
-    first."""
+    columns (drop the oldest); T2 (prm.trunc == "T2"): keep the
+    k_t - p directions of range(C) with the smallest principal angles to the
+    cycle's image space (t2_directions).  Columns are ordered oldest first."""
     m_eff = len(y)
     k = U.shape[1]
     zeta = H @ y
@@ -112,11 +113,37 @@ def gcrot_update(U, C, V, H, B, y, dx, rho, prm):
         return U, C
     if k + p > prm.k_max:
         keep = max(0, prm.k_t - p)
-        U = U[:, k - keep:]
-        C = C[:, k - keep:]
+        if getattr(prm, "trunc", "T1") == "T2" and 0 < keep <= min(k, m_eff):
+            W = t2_directions(B, H, keep)
+            U = U @ W
+            C = C @ W
+        else:
+            U = U[:, k - keep:]
+            C = C[:, k - keep:]
     U = np.column_stack([U] + newU)
     C = np.column_stack([C] + newC)
     return U, C
+
+
+def t2_directions(B, H, keep):
+    """Truncation T2 (the GCROT angle criterion the
+    paper names at P:462-463): the cycle's image space is
+    A_hat V_m = [C V_{m+1}] [B; H_] (eq. (5)); with Q = qr([B; H_]) the
+    cosines of the principal angles between range(C) and that image are the
+    singular values of Q(1:k, :) = W S Z^T.  Keep the `keep` directions of
+    range(C) closest to the image (largest singular values): U <- U W,
+    C <- C W with W = W[:, :keep], each column sign-normalised so that its
+    largest-|.| entry is positive.  C W stays orthonormal and A_hat U W = C W.
+    Used when keep <= min(k, m_eff) (reading R13), else T1."""
+    k = B.shape[0]
+    Q, _ = np.linalg.qr(np.vstack([B, H]))
+    W, _, _ = np.linalg.svd(Q[:k, :])
+    W = W[:, :keep].copy()
+    for j in range(keep):
+        i = int(np.argmax(np.abs(W[:, j])))
+        if W[i, j] < 0:
+            W[:, j] = -W[:, j]
+    return W
 
 
 # --------------------------------------------------------------- O3 rGCROT

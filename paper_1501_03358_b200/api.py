@@ -116,10 +116,10 @@ class GridOperator:
 
 def make_config(method="rgcrot", m=20, k_max=10, k_keep=5, select_count=1, precond="jacobi",
                 sweeps=5, omega_l=0.8, omega_g=1.0, tol=1e-8, max_matvecs=2000,
-                divergence=1e4):
+                divergence=1e4, trunc="T1"):
     pc = L.rk_precond(1 if precond == "jacobi" else 0, sweeps, omega_l, omega_g)
-    return L.rk_config(L.METHODS[method], m, k_max, k_keep, select_count, 0, 0, pc, tol,
-                       max_matvecs, divergence)
+    return L.rk_config(L.METHODS[method], m, k_max, k_keep, select_count, 0,
+                       {"T1": 0, "T2": 1}[trunc], pc, tol, max_matvecs, divergence)
 
 
 def config_from_params(prm, method=None):
@@ -131,7 +131,8 @@ def config_from_params(prm, method=None):
     return make_config(method=meth, m=prm.m, k_max=k, k_keep=min(prm.k_t, k),
                        select_count=0 if k == 0 else prm.p1,
                        sweeps=prm.sweeps, omega_l=prm.omega_l, omega_g=prm.omega_g,
-                       tol=prm.tol, max_matvecs=prm.max_mv, divergence=prm.divergence)
+                       tol=prm.tol, max_matvecs=prm.max_mv, divergence=prm.divergence,
+                       trunc=getattr(prm, "trunc", "T1"))
 
 
 def _report(r):

@@ -155,6 +155,9 @@ __global__ void __launch_bounds__(256) bupd_tile_kernel(ColPtrs Q, int ncol, con
   __shared__ double gsh[NC];
   for (int c = threadIdx.x; c < NC; c += blockDim.x) gsh[c] = c < ncol ? gs * g[c] : 0.0;
   __syncthreads();
+  // volatile: re-read per group instead of hoisting NC coefficients into
+  // registers for the whole tile loop (which cost occupancy)
+  const volatile double* gshv = gsh;
   double acc[ND > 0 ? ND : 1];
 #pragma unroll
   for (int q = 0; q < (ND > 0 ? ND : 1); ++q) acc[q] = 0.0;
@@ -182,6 +185,9 @@ __global__ void __launch_bounds__(256) bupd_tile_kernel(ColPtrs Q, int ncol, con
 #pragma unroll
     for (int c = 0; c < NC; c += G) {
       if (c < ncol) {
+        double gc[G];
+#pragma unroll
+        for (int u = 0; u < G; ++u) gc[u] = gshv[c + u];
         double2 q[G][RV];
 #pragma unroll
         for (int u = 0; u < G; ++u)
@@ -191,12 +197,13 @@ __global__ void __launch_bounds__(256) bupd_tile_kernel(ColPtrs Q, int ncol, con
             q[u][v] = make_double2(a.v[0], a.v[1]);
           }
 #pragma unroll
-        for (int u = 0; u < G; ++u)
+        for (int u = 0; u < G; ++u) {
 #pragma unroll
           for (int v = 0; v < RV; ++v) {
-            wv[v].x = fma(-gsh[c + u], q[u][v].x, wv[v].x);
-            wv[v].y = fma(-gsh[c + u], q[u][v].y, wv[v].y);
+            wv[v].x = fma(-gc[u], q[u][v].x, wv[v].x);
+            wv[v].y = fma(-gc[u], q[u][v].y, wv[v].y);
           }
+        }
       }
     }
 #pragma unroll
@@ -208,13 +215,12 @@ __global__ void __launch_bounds__(256) bupd_tile_kernel(ColPtrs Q, int ncol, con
   for (int64_t r = ntile * TILE_ROWS + 2 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x); r < N;
        r += 2 * (int64_t)gridDim.x * blockDim.x) {
     double2 wn = *reinterpret_cast<const double2*>(w + r);
-#pragma unroll
-    for (int c = 0; c < NC; ++c)
-      if (c < ncol) {
-        const Vec<2> a = ldv_stream<2>(Q.p[c] + r);
-        wn.x = fma(-gsh[c], a.v[0], wn.x);
-        wn.y = fma(-gsh[c], a.v[1], wn.y);
-      }
+#pragma unroll 1
+    for (int c = 0; c < ncol; ++c) {   // rolled: keeps the tail out of the register budget
+      const Vec<2> a = ldv_stream<2>(Q.p[c] + r);
+      wn.x = fma(-gsh[c], a.v[0], wn.x);
+      wn.y = fma(-gsh[c], a.v[1], wn.y);
+    }
     *reinterpret_cast<double2*>(w + r) = wn;
     dots(w + r, wn);
   }
@@ -353,10 +359,10 @@ __global__ void __launch_bounds__(256) proj_kernel(ColPtrs C, ColPtrs U, int k, 
 // column-major): the QR refresh C <- C~ R^-1, U <- U R^-1 (K8).  Each thread
 // owns whole rows, so in-place is race free.
 template <int NC>
-__global__ void __launch_bounds__(256) rotate_kernel(ColPtrs Qc, int k, const double* __restrict__ T,
+__global__ void __launch_bounds__(256) rotate_kernel(ColPtrs Qc, int k, int kout, const double* __restrict__ T,
                                                      int64_t N) {
   __shared__ double ts[NC * NC];
-  for (int t = threadIdx.x; t < k * k; t += blockDim.x) ts[t] = T[t];
+  for (int t = threadIdx.x; t < k * kout; t += blockDim.x) ts[t] = T[t];
   __syncthreads();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; n < N; n += stride) {
@@ -366,7 +372,7 @@ __global__ void __launch_bounds__(256) rotate_kernel(ColPtrs Qc, int k, const do
       if (c < k) in[c] = Qc.p[c][n];
 #pragma unroll
     for (int o = 0; o < NC; ++o) {
-      if (o < k) {
+      if (o < kout) {
         double s = 0.0;
 #pragma unroll
         for (int c = 0; c < NC; ++c)
@@ -528,19 +534,21 @@ void proj(rk_ctx* ctx, const std::vector<const double*>& C, const std::vector<co
   allreduce(ctx, red_out, 1);
 }
 
-void rotate(rk_ctx* ctx, const std::vector<double*>& cols, const double* T, int64_t N) {
+void rotate(rk_ctx* ctx, const std::vector<double*>& cols, const double* T, int64_t N, int kout) {
   const int k = (int)cols.size();
   if (k == 0) return;
+  if (kout < 0) kout = k;
+  RK_REQUIRE(kout >= 1 && kout <= k, RK_EINVAL, "rotate: 1 <= kout <= k");
   const int nc = nc_bucket(k);
   ColPtrs Q;
   memset(&Q, 0, sizeof(Q));
   for (int c = 0; c < k; ++c) Q.p[c] = cols[c];
-  Launch L(ctx, "rotate", 16.0 * N * k);
+  Launch L(ctx, "rotate", 8.0 * N * (k + kout));
   switch (nc) {
-    case 8: launch_k(ctx, rotate_kernel<8>, N, dim3(256), Q, k, T, N); break;
-    case 16: launch_k(ctx, rotate_kernel<16>, N, dim3(256), Q, k, T, N); break;
-    case 32: launch_k(ctx, rotate_kernel<32>, N, dim3(256), Q, k, T, N); break;
-    default: launch_k(ctx, rotate_kernel<48>, N, dim3(256), Q, k, T, N); break;
+    case 8: launch_k(ctx, rotate_kernel<8>, N, dim3(256), Q, k, kout, T, N); break;
+    case 16: launch_k(ctx, rotate_kernel<16>, N, dim3(256), Q, k, kout, T, N); break;
+    case 32: launch_k(ctx, rotate_kernel<32>, N, dim3(256), Q, k, kout, T, N); break;
+    default: launch_k(ctx, rotate_kernel<48>, N, dim3(256), Q, k, kout, T, N); break;
   }
   L.done();
 }

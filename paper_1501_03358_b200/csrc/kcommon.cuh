@@ -139,9 +139,20 @@ __device__ __forceinline__ void block_reduce_store(const double (&v)[NV], int nv
   __syncthreads();
   if (last) {
     __threadfence();
+    // one warp per value, each lane with 4 independent partial sums (the
+    // tail of every reduction; its latency is on the critical path)
     for (int q = warp; q < nv; q += nwarps) {
-      double s = 0.0;
-      for (int c = lane; c < G; c += 32) s += __ldcg(ra.partials + (int64_t)q * G + c);
+      const double* p = ra.partials + (int64_t)q * G;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int c = lane;
+      for (; c + 96 < G; c += 128) {
+        s0 += __ldcg(p + c);
+        s1 += __ldcg(p + c + 32);
+        s2 += __ldcg(p + c + 64);
+        s3 += __ldcg(p + c + 96);
+      }
+      for (; c < G; c += 32) s0 += __ldcg(p + c);
+      double s = (s0 + s1) + (s2 + s3);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
       if (lane == 0) ra.out[q] = s;

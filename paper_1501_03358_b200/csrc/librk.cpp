@@ -106,6 +106,112 @@ double ls_givens(const std::vector<double>& H, int m, double rho, std::vector<do
   return std::fabs(g[m]);
 }
 
+// Truncation T2 (reading R13).  The cycle's image
+// space is A_hat V_m = [C V_{m+1}] M with M = [B; H_] ((k+m+1) x m, eq. (5)).
+// With M = Q R (Householder), the cosines of the principal angles between
+// range(C) and the image are the singular values of Q1 = Q(1:k, :); the left
+// singular vectors are the eigenvectors of Q1 Q1^T (cyclic Jacobi).  Returns
+// W (k x keep, column-major): the `keep` leading directions, each column
+// sign-normalised so that its largest-|.| entry is positive.
+std::vector<double> t2_directions(int k, int m, const std::vector<double>& B,
+                                  const std::vector<double>& H, int keep) {
+  const int n = k + m + 1;
+  std::vector<double> A((size_t)n * m, 0.0);  // column-major [B; H]
+  for (int j = 0; j < m; ++j) {
+    for (int i = 0; i < k; ++i) A[i + (size_t)j * n] = B[i + (size_t)j * k];
+    for (int i = 0; i <= m; ++i) A[k + i + (size_t)j * n] = H[i + (size_t)j * (m + 1)];
+  }
+  // Householder QR: reflectors v_j (stored below the diagonal, v_j[j] = 1)
+  std::vector<double> tau(m, 0.0);
+  for (int j = 0; j < m; ++j) {
+    double nrm = 0.0;
+    for (int i = j; i < n; ++i) nrm += A[i + (size_t)j * n] * A[i + (size_t)j * n];
+    nrm = std::sqrt(nrm);
+    const double a = A[j + (size_t)j * n];
+    if (nrm == 0.0) continue;
+    const double beta = a >= 0 ? -nrm : nrm;
+    const double v0 = a - beta;
+    for (int i = j + 1; i < n; ++i) A[i + (size_t)j * n] /= v0;
+    tau[j] = (beta - a) / beta;
+    A[j + (size_t)j * n] = beta;
+    for (int l = j + 1; l < m; ++l) {
+      double d = A[j + (size_t)l * n];
+      for (int i = j + 1; i < n; ++i) d += A[i + (size_t)j * n] * A[i + (size_t)l * n];
+      d *= tau[j];
+      A[j + (size_t)l * n] -= d;
+      for (int i = j + 1; i < n; ++i) A[i + (size_t)l * n] -= d * A[i + (size_t)j * n];
+    }
+  }
+  // Q (n x m) = H_0 H_1 ... H_{m-1} [I; 0]
+  std::vector<double> Q((size_t)n * m, 0.0);
+  for (int j = 0; j < m; ++j) Q[j + (size_t)j * n] = 1.0;
+  for (int j = m - 1; j >= 0; --j)
+    for (int l = 0; l < m; ++l) {
+      double d = Q[j + (size_t)l * n];
+      for (int i = j + 1; i < n; ++i) d += A[i + (size_t)j * n] * Q[i + (size_t)l * n];
+      d *= tau[j];
+      Q[j + (size_t)l * n] -= d;
+      for (int i = j + 1; i < n; ++i) Q[i + (size_t)l * n] -= d * A[i + (size_t)j * n];
+    }
+  // K = Q1 Q1^T (k x k), cyclic Jacobi eigen-decomposition K = V diag(e) V^T
+  std::vector<double> K((size_t)k * k, 0.0), V((size_t)k * k, 0.0);
+  for (int a = 0; a < k; ++a)
+    for (int b = 0; b < k; ++b) {
+      double d = 0.0;
+      for (int l = 0; l < m; ++l) d += Q[a + (size_t)l * n] * Q[b + (size_t)l * n];
+      K[a + (size_t)b * k] = d;
+    }
+  for (int a = 0; a < k; ++a) V[a + (size_t)a * k] = 1.0;
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0.0, tot = 0.0;
+    for (int a = 0; a < k; ++a)
+      for (int b = 0; b < k; ++b) {
+        const double v = K[a + (size_t)b * k] * K[a + (size_t)b * k];
+        tot += v;
+        if (a != b) off += v;
+      }
+    if (off <= 1e-30 * tot || off == 0.0) break;
+    for (int p = 0; p < k - 1; ++p)
+      for (int q = p + 1; q < k; ++q) {
+        const double apq = K[p + (size_t)q * k];
+        if (apq == 0.0) continue;
+        const double app = K[p + (size_t)p * k], aqq = K[q + (size_t)q * k];
+        const double theta = (aqq - app) / (2.0 * apq);
+        const double t = (theta >= 0 ? 1.0 : -1.0) / (std::fabs(theta) + std::sqrt(theta * theta + 1.0));
+        const double c = 1.0 / std::sqrt(t * t + 1.0), sn = t * c;
+        for (int r = 0; r < k; ++r) {  // K <- K J
+          const double kp = K[r + (size_t)p * k], kq = K[r + (size_t)q * k];
+          K[r + (size_t)p * k] = c * kp - sn * kq;
+          K[r + (size_t)q * k] = sn * kp + c * kq;
+        }
+        for (int r = 0; r < k; ++r) {  // K <- J^T K
+          const double kp = K[p + (size_t)r * k], kq = K[q + (size_t)r * k];
+          K[p + (size_t)r * k] = c * kp - sn * kq;
+          K[q + (size_t)r * k] = sn * kp + c * kq;
+        }
+        for (int r = 0; r < k; ++r) {  // V <- V J
+          const double vp = V[r + (size_t)p * k], vq = V[r + (size_t)q * k];
+          V[r + (size_t)p * k] = c * vp - sn * vq;
+          V[r + (size_t)q * k] = sn * vp + c * vq;
+        }
+      }
+  }
+  std::vector<int> idx(k);
+  std::iota(idx.begin(), idx.end(), 0);
+  std::stable_sort(idx.begin(), idx.end(),
+                   [&](int a, int b) { return K[a + (size_t)a * k] > K[b + (size_t)b * k]; });
+  std::vector<double> W((size_t)k * keep, 0.0);
+  for (int j = 0; j < keep; ++j) {
+    const int e = idx[j];
+    int im = 0;
+    for (int i = 1; i < k; ++i)
+      if (std::fabs(V[i + (size_t)e * k]) > std::fabs(V[im + (size_t)e * k])) im = i;
+    const double sg = V[im + (size_t)e * k] < 0 ? -1.0 : 1.0;
+    for (int i = 0; i < k; ++i) W[i + (size_t)j * k] = sg * V[i + (size_t)e * k];
+  }
+  return W;
+}
+
 }  // namespace
 
 // --------------------------------------------------------------- solver
@@ -514,7 +620,24 @@ struct rk_solver {
       if (p > 0) {
         if (k + p > cfg.k_max) {
           const int keep = std::max(0, cfg.k_keep - p);
-          order.erase(order.begin(), order.begin() + (k - keep));
+          if (cfg.trunc == 1 && keep > 0 && keep <= std::min(k, m_eff)) {
+            // T2: [U C] <- [U C] W in place, the first `keep` slots of order
+            const std::vector<double> W = t2_directions(k, m_eff, B, H, keep);
+            std::memcpy(hsc + o_T, W.data(), sizeof(double) * W.size());
+            RK_CUDA(cudaMemcpyAsync(dsc + o_T, hsc + o_T, sizeof(double) * W.size(),
+                                    cudaMemcpyHostToDevice, ctx->stream));
+            std::vector<double*> Uw, Cw;
+            for (int s : order) {
+              Uw.push_back(Us[s]);
+              Cw.push_back(Cs[s]);
+            }
+            rotate(ctx, Uw, dsc + o_T, N, keep);
+            rotate(ctx, Cw, dsc + o_T, N, keep);
+            order.resize(keep);
+            sync();  // the pinned W buffer is reused
+          } else {
+            order.erase(order.begin(), order.begin() + (k - keep));   // T1
+          }
         }
         for (int s : newslots) order.push_back(s);
       }
@@ -887,7 +1010,8 @@ rk_status rk_solver_create(rk_op* op, const rk_config* cfg, rk_solver** out) {
     RK_REQUIRE(cfg->k_max <= 46, RK_EINVAL, "k_max <= 46");
     RK_REQUIRE(cfg->select_count >= 0 && cfg->select_count <= 2, RK_EINVAL, "select_count 0..2");
     RK_REQUIRE(cfg->k_keep >= 0 && cfg->k_keep <= cfg->k_max, RK_EINVAL, "0 <= k_keep <= k_max");
-    RK_REQUIRE(cfg->ortho == 0 && cfg->trunc == 0, RK_EUNSUPPORTED, "only CGS2 and T1");
+    RK_REQUIRE(cfg->ortho == 0, RK_EUNSUPPORTED, "only CGS2");
+    RK_REQUIRE(cfg->trunc == 0 || cfg->trunc == 1, RK_EINVAL, "trunc: 0 (T1) or 1 (T2)");
     RK_REQUIRE(cfg->pc.kind == 0 || (cfg->pc.kind == 1 && cfg->pc.sweeps >= 1), RK_EINVAL,
                "bad preconditioner");
     RK_REQUIRE(cfg->max_matvecs >= 1, RK_EINVAL, "max_matvecs >= 1");

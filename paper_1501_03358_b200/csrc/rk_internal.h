@@ -229,7 +229,9 @@ void lincomb(rk_ctx* ctx, const std::vector<const double*>& cols, const double* 
              const LcOut& lo, int64_t N);
 void proj(rk_ctx* ctx, const std::vector<const double*>& C, const std::vector<const double*>& U,
           const double* xi, double* r, double* x, int64_t N, double* red_out);
-void rotate(rk_ctx* ctx, const std::vector<double*>& cols, const double* T, int64_t N);
+// [q_0 .. q_{k-1}] <- [q_0 .. q_{k-1}] T in place, T k x kout (column-major),
+// outputs into the first kout columns (kout = -1: square).
+void rotate(rk_ctx* ctx, const std::vector<double*>& cols, const double* T, int64_t N, int kout = -1);
 void bicg_p(rk_op* op, const double* r, double* p, const double* v, double* z, double wl,
             bool jacobi, const BiIter* cur, const BiIter* prev, int first);
 void bicg_s(rk_op* op, const double* r, const double* v, double* s, double* z, double wl,

@@ -250,6 +250,20 @@ def test_sequence_parity(rk, ctx, name, solver):
     compare_sequences(w, gpu, ora, method)
 
 
+@pytest.mark.parametrize("name", ["c2s", "c3s", "c4s"])
+def test_sequence_parity_T2(rk, ctx, name):
+    """Truncation T2 (principal angles, reading R13): host Householder QR +
+    Jacobi eigen-solve in librk vs numpy QR + SVD in the oracle."""
+    from dataclasses import replace
+    from problems.workloads import Workload
+    w0 = get_workload(name)
+    w = Workload(w0.name, w0.make_problem, replace(w0.params, trunc="T2"), w0.n_systems,
+                 w0.epoch_every, w0.description)
+    ora = run_sequence(w)
+    gpu, _ = gpu_sequence(rk, ctx, w)
+    compare_sequences(w, gpu, ora, w.params.method)
+
+
 def test_sequence_parity_fused_chain(rk, ctx, monkeypatch):
     """Hybrid sequence with every preconditioned operator application
     through the fused TMA chain (forced below its L2 threshold)."""
@@ -438,3 +452,46 @@ def test_c2_full_size_sequence_properties(rk, ctx):
     assert np.mean(mv[1:]) < mv[0]
     k = U.shape[0]
     assert np.linalg.norm(C @ C.T - np.eye(k)) <= 1e-12 * k
+
+
+@pytest.mark.parametrize("name", ["c3", "c2"])
+def test_full_size_sequence_vs_stored_oracle(rk, ctx, name):
+    """BASELINE configs at FULL size, in the launch configuration bench.py
+    times (c3 = the bench workload), against the oracle's own full-sequence
+    run stored by scripts/oracle_counts.py (tests/golden/oracle_seq_<name>.json,
+    written from oracle/ alone): per-system Krylov matvecs within one cycle
+    (rGCROT) / 10 % (rBiCGStab), sequence total within 10 %, the true
+    relative residual <= tol, and the solution through ||x||, 4 seeded probe
+    projections and 64 sampled entries (|x_gpu - x_or| <= 1e-6 ||x_or||
+    componentwise in those measures)."""
+    import json
+    import os
+    path = os.path.join(os.path.dirname(__file__), "..", "golden", f"oracle_seq_{name}.json")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated yet (scripts/oracle_counts.py {name})")
+    gold = json.load(open(path))
+    w = get_workload(name)
+    prob = w.problem()
+    from problems.rng import uniform
+    idx = np.arange(prob.N, dtype=np.uint64)
+    probes = [uniform(s, idx) for s in gold["probe_seeds"]]
+    gpu, _ = gpu_sequence(rk, ctx, w)
+    tot_g = tot_o = 0
+    for t, ((rg, x), go) in enumerate(zip(gpu, gold["systems"])):
+        assert rg["tag"] == go["tag"]
+        assert rg["outcome"] == "CONVERGED"
+        assert rg["final_true_res"] <= w.params.tol * rg["bnorm"]
+        ng, no = rg["krylov_matvecs"], go["krylov_matvecs"]
+        tot_g += ng
+        tot_o += no
+        if rg["tag"] == "rbicgstab":
+            assert abs(ng - no) <= max(0.1 * no, 2), (t, ng, no)
+        else:
+            assert abs(ng - no) <= w.params.m, (t, ng, no)
+        xn = go["xnorm"]
+        assert abs(np.linalg.norm(x) - xn) <= 1e-6 * xn, t
+        for g, pv in zip(probes, go["xproj"]):
+            assert abs(g @ x - pv) <= 1e-6 * xn * np.linalg.norm(g), t
+        xsamp = x[gold["sample_idx"]]
+        assert np.max(np.abs(xsamp - np.array(go["xsample"]))) <= 1e-6 * xn, t
+    assert abs(tot_g - tot_o) <= 0.1 * tot_o, (tot_g, tot_o)

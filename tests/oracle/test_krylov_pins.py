@@ -315,3 +315,53 @@ def test_gcrot_update_truncation_T1():
     zeta = H @ y
     assert np.allclose(C2[:, 1], V @ zeta / np.linalg.norm(zeta))
     assert abs(C2[:, 1] @ C2[:, 2]) <= 1e-14
+
+
+def test_t2_directions_are_principal_vectors():
+    """T2 (reading R13): the kept directions C W are the principal vectors
+    of range(C) w.r.t. the cycle's image space [C V_{m+1}] [B; H_]
+    (eq. (5)).  Pinned against scipy.linalg.subspace_angles (an
+    independent principal-angle routine): the cosines of the angles of
+    each kept direction to the image equal the `keep` largest cosines of
+    the principal angles, in order; W has orthonormal columns and the
+    sign rule holds."""
+    import scipy.linalg as sla
+    from oracle.krylov import t2_directions
+    rng = np.random.default_rng(4)
+    N, m, k, keep = 60, 6, 8, 5
+    CV = _orth(rng.standard_normal((N, k + m + 1)))
+    C, V = CV[:, :k], CV[:, k:]
+    H = np.triu(rng.standard_normal((m + 1, m)), -1)
+    B = rng.standard_normal((k, m))
+    W = t2_directions(B, H, keep)
+    assert np.allclose(W.T @ W, np.eye(keep), atol=1e-13)
+    img = _orth(CV @ np.vstack([B, H]))
+    cos_ref = np.sort(np.cos(sla.subspace_angles(C, img)))[::-1][:keep]
+    cos_kept = np.linalg.norm(img.T @ (C @ W), axis=0)
+    assert np.allclose(cos_kept, cos_ref, atol=1e-12)
+    for j in range(keep):
+        assert W[np.argmax(np.abs(W[:, j])), j] > 0
+
+
+def test_rgcrot_T2_invariants_and_solution():
+    """rGCROT with T2 truncation keeps A_hat U = C, C^T C = I and solves
+    the shrunken channel sequence to tol (the invariants of S:275-282)."""
+    w = get_workload("c2s")
+    prob = w.problem()
+    op, pc, _ = _setup(prob)
+    prm = replace(w.params, trunc="T2")
+    U = np.zeros((op.N, 0))
+    C = np.zeros((op.N, 0))
+    truncated = 0
+    for t in range(4):
+        b = prob.rhs(t).reshape(-1)
+        k_before = U.shape[1]
+        x, U, C, rep = rgcrot(op, pc, b, U, C, prm)
+        truncated += rep.cycles > 0 and k_before + rep.cycles * prm.p1 > prm.k_max
+        assert rep.outcome == CONVERGED
+        assert U.shape[1] <= prm.k_max
+        assert np.linalg.norm(C.T @ C - np.eye(C.shape[1])) <= 1e-12
+        AU = np.column_stack([pc(op.apply(U[:, i])) for i in range(U.shape[1])])
+        assert np.linalg.norm(AU - C) <= 1e-11 * np.linalg.norm(U)
+        assert np.linalg.norm(b - op.apply(x)) <= prm.tol * np.linalg.norm(b)
+    assert truncated
