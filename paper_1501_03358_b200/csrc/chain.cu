@@ -258,18 +258,17 @@ chain_kernel(const __grid_constant__ CUtensorMap map_b, const __grid_constant__ 
   const int xoff = (ty + 1) * XX + tx + 1 + PADX;    // own cell in an input tile
   const int boff = ty * SX + tx + PADB;              // own cell in a band / rhs tile
   const int roff = ty * EX + tx;                     // own cell in a ring plane
-  auto pl_of = [&](int q) { return pz ? ((q % nz) + nz) % nz : q; };  // out of range -> TMA zero fill
-  auto xslot = [&](int q) { return (q - qfirst) % NXB; };
-  auto bslot = [&](int q) { return (q - qfirst) % NB; };
-  auto xtile = [&](int q) {
-    return reinterpret_cast<const double*>(smem + G::X_BASE + xslot(q) * G::XSLOT) + xoff;
+  // planes outside [0, nz) wrap on a periodic z axis (|overhang| <= HALO + 1
+  // < nz) and are zero-filled by TMA otherwise
+  auto pl_of = [&](int q) { return pz ? (q < 0 ? q + nz : (q >= nz ? q - nz : q)) : q; };
+  auto xtile = [&](int xs) {
+    return reinterpret_cast<const double*>(smem + G::X_BASE + xs * G::XSLOT) + xoff;
   };
 
   // thread 0: all bytes of plane q (bands, rhs, input tile) land on the
-  // mbarrier of q's input-tile slot
-  auto issue = [&](int q) {
-    const int xs = xslot(q);
-    unsigned char* bbase = smem + bslot(q) * G::BSLOT;
+  // mbarrier of q's input-tile slot xs; the bands / rhs go to band slot bs
+  auto issue = [&](int q, int xs, int bs) {
+    unsigned char* bbase = smem + bs * G::BSLOT;
     unsigned char* xbase = smem + G::X_BASE + xs * G::XSLOT;
     const int pl = pl_of(q);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -279,18 +278,25 @@ chain_kernel(const __grid_constant__ CUtensorMap map_b, const __grid_constant__ 
     // the input vector is padded: plane pl lives at z-coordinate pl + 1
     tma_load_3d(xbase, &map_x, &bars[xs], gx0 - 1 - PADX, gy0 - 1, pl + 1);
   };
-  auto wait_plane = [&](int q) { mbar_wait(&bars[xslot(q)], (uint32_t)(((q - qfirst) / NXB) & 1)); };
 
   if (tid == 0) {
     for (int s = 0; s < NXB; ++s) mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  // prologue: planes qfirst .. qfirst + PD (step tau0 issues tau0 + PD)
+  // prologue: planes qfirst .. qfirst + PD (step tau0 issues tau0 + PD);
+  // plane q uses x slot (q - qfirst) % NXB, band slot (q - qfirst) % NB and
+  // barrier parity ((q - qfirst) / NXB) & 1
   if (tid == 0)
-    for (int q = qfirst; q <= min(qfirst + PD, qlast); ++q) issue(q);
-  wait_plane(qfirst);
-  if (qfirst + 1 <= qlast) wait_plane(qfirst + 1);
+    for (int q = qfirst; q <= min(qfirst + PD, qlast); ++q) issue(q, (q - qfirst) % NXB, (q - qfirst) % NB);
+  mbar_wait(&bars[0], 0);
+  if (qfirst + 1 <= qlast) mbar_wait(&bars[1], 0);
+  // running slot state (advanced once per step; no divisions in the loop)
+  int xsm = 0, xs0 = 1, xsp = 2 % NXB;          // x slots of planes tau-1, tau, tau+1
+  uint32_t parp = 0;                             // barrier parity of plane tau+1
+  int bs0 = 1 % NB;                              // band slot of plane tau
+  int xsi = (PD + 1) % NXB, bsi = (PD + 1) % NB; // slots of plane tau + PD
+  auto adv = [](int& v, int n) { v = (v + 1 == n) ? 0 : v + 1; };
 
   double bnd[3][ST], rr[3], inv[3];
 #pragma unroll
@@ -304,13 +310,12 @@ chain_kernel(const __grid_constant__ CUtensorMap map_b, const __grid_constant__ 
 #define RK_CHAIN_STEP(PHV)                                                                         \
   {                                                                                                \
     if (tau >= tau_end) break;                                                                     \
-    if (tid == 0 && tau + PD <= qlast) issue(tau + PD);                                            \
-    if (tau + 1 <= qlast) wait_plane(tau + 1);                                                     \
+    if (tid == 0 && tau + PD <= qlast) issue(tau + PD, xsi, bsi);                                  \
+    if (tau + 1 <= qlast) mbar_wait(&bars[xsp], parp);                                             \
     using SP = ChainStep<ST, NST, TX, TY, PD, K0, K1, K2, PHV>;                                    \
     const double v0 = SP::stage0(interior && tau >= z0 && tau < z1 && (pz || tau < nz),           \
-                                 pl_of(tau), smem + bslot(tau) * G::BSLOT, xtile(tau - 1),         \
-                                 xtile(tau), xtile(tau + 1), ring, bnd, rr, inv, cxy, boff, roff,  \
-                                 cp);                                                              \
+                                 pl_of(tau), smem + bs0 * G::BSLOT, xtile(xsm), xtile(xs0),        \
+                                 xtile(xsp), ring, bnd, rr, inv, cxy, boff, roff, cp);             \
     if constexpr (NST >= 2) {                                                                      \
       double v1 = 0.0;                                                                             \
       if (tau >= tau0 + 2) {                                                                       \
@@ -327,6 +332,13 @@ chain_kernel(const __grid_constant__ CUtensorMap map_b, const __grid_constant__ 
       }                                                                                            \
     }                                                                                              \
     __syncthreads();                                                                               \
+    xsm = xs0;                                                                                     \
+    xs0 = xsp;                                                                                     \
+    adv(xsp, NXB);                                                                                 \
+    if (xsp == 0) parp ^= 1u;                                                                      \
+    adv(bs0, NB);                                                                                  \
+    adv(xsi, NXB);                                                                                 \
+    adv(bsi, NB);                                                                                  \
     ++tau;                                                                                         \
   }
   for (int tau = tau0; tau < tau_end;) {
