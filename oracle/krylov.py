@@ -375,51 +375,86 @@ def bicgstab(op, pc, b, prm):
 
 
 # ------------------------------------------------------- O7 hybrid / sequence
-def run_sequence(workload, systems=None, solver=None, callback=None):
+def run_sequence(workload, systems=None, solver=None, callback=None, switchback=False,
+                 refresh_on_epoch=False, refresh_every=0):
     """Solve workload.n_systems systems A_e x_t = b_t in order, carrying the
     recycle space.  method 'rgcrot' | 'gmres' | 'bicgstab' | 'hybrid'.
     Hybrid: systems t < n_sw by rGCROT, then rBiCGStab with the
     space frozen; at the switch and at each A epoch C is invalidated and
-    rebuilt against the operator of the method in use [D3]."""
+    rebuilt against the operator of the method in use [D3].
+
+    Hybrid policy options (SPEC hybrid module, reading R16):
+      switchback       -- "if convergence is poor ... switch back to rGCROT":
+                          an rBiCGStab solve that does not converge (UNSTABLE,
+                          BREAKDOWN, MAX_MATVECS, DRIFT) is re-solved from
+                          x = 0 by rGCROT, which updates the space; rBiCGStab
+                          resumes with the next system.  Both attempts count.
+      refresh_on_epoch -- "intermittent solves with rGCROT to update the
+                          recycle space ... when the system matrix changes":
+                          the first system of every new A epoch after the
+                          switch is solved by rGCROT.
+      refresh_every    -- n > 0: every n-th system after the switch is solved
+                          by rGCROT (SPEC refresh_every_n).
+    Returns [(tag, x, report)]; a switched-back system has tag
+    'rbicgstab+rgcrot' and a report with the summed counts."""
     from .stencil import Operator, Jacobi
     prm = workload.params
     method = solver or prm.method
     prob = workload.problem()
     T = workload.n_systems if systems is None else systems
     U = C = None
-    valid = True
+    c_kind = "ahat"            # C spans M^-1 A U (rGCROT) or A U (rBiCGStab) [D3]
+    c_epoch = 0
     epoch = -1
     out = []
     op = pc = None
     for t in range(T):
         e = workload.epoch(t)
-        if e != epoch:
+        new_epoch = e != epoch
+        if new_epoch:
             op = Operator.from_problem(prob, epoch=e)
             pc = Jacobi(op, prm.sweeps, prm.omega_l, prm.omega_g)
-            if epoch >= 0:
-                valid = False
             epoch = e
         if U is None:
             U = np.zeros((op.N, 0))
             C = np.zeros((op.N, 0))
+            c_epoch = e
         b = prob.rhs(t).reshape(-1)
+        use_rg = method == "rgcrot" or (method == "hybrid" and hybrid_uses_rgcrot(
+            t, prm.n_sw, new_epoch and t > 0, refresh_on_epoch, refresh_every))
         if method == "gmres":
             x, rep = gmres(op, pc, b, prm)
             tag = "gmres"
         elif method == "bicgstab":
             x, rep = bicgstab(op, pc, b, prm)
             tag = "bicgstab"
-        elif method == "rgcrot" or (method == "hybrid" and t < prm.n_sw):
-            x, U, C, rep = rgcrot(op, pc, b, U, C, prm, valid=valid)
-            valid = True
+        elif use_rg:
+            x, U, C, rep = rgcrot(op, pc, b, U, C, prm, valid=(c_kind == "ahat" and c_epoch == e))
+            c_kind, c_epoch = "ahat", e
             tag = "rgcrot"
         else:
-            if method == "hybrid" and t == prm.n_sw:
-                valid = False                              # switch: C R = qr(A U) [D3]
-            x, U, C, rep = rbicgstab(op, pc, b, U, C, prm, valid=valid)
-            valid = True
+            x, U, C, rep = rbicgstab(op, pc, b, U, C, prm, valid=(c_kind == "a" and c_epoch == e))
+            c_kind, c_epoch = "a", e
             tag = "rbicgstab"
+            if switchback and rep.outcome != CONVERGED:
+                x, U, C, rep2 = rgcrot(op, pc, b, U, C, prm, valid=False)
+                c_kind = "ahat"
+                rep2.krylov_mv += rep.krylov_mv
+                rep2.op_apps += rep.op_apps
+                rep = rep2
+                tag = "rbicgstab+rgcrot"
         out.append((tag, x, rep))
         if callback:
             callback(t, tag, x, U, C, rep)
     return out
+
+
+def hybrid_uses_rgcrot(t, n_sw, epoch_changed, refresh_on_epoch, refresh_every):
+    """Hybrid schedule (R16): rGCROT for t < n_sw, and after the
+    switch on the first system of a new A epoch (refresh_on_epoch) or every
+    refresh_every-th system; rBiCGStab otherwise."""
+    if t < n_sw:
+        return True
+    if refresh_on_epoch and epoch_changed:
+        return True
+    return bool(refresh_every) and (t - n_sw) % refresh_every == refresh_every - 1

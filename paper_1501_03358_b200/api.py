@@ -216,30 +216,56 @@ class Solver:
 
 
 def solve_sequence(solver, rhs, n, method, n_sw=0, epoch_of=None, bands_for_epoch=None,
-                   tol=0.0, host=False, x_out=None):
+                   tol=0.0, host=False, x_out=None, switchback=False, refresh_on_epoch=False,
+                   refresh_every=0):
     """Sequence controller (reading D3): for the hybrid,
     systems t < n_sw use rGCROT and later ones rBiCGStab with the recycle
     space frozen; a new A epoch uploads its bands (librk then invalidates C
-    and rebuilds it by QR of op(U) in the next solve).  rhs(t) -> b_t (device
-    tensor, or pinned host tensor if host=True).  Returns the reports;
-    solutions go to x_out[t] when given.  The operator must hold the bands of
-    epoch_of(0) on entry."""
+    and rebuilds it by QR of op(U) in the next solve).  Policy options
+    (reading R16): `switchback` re-solves a non-converged
+    rBiCGStab system by rGCROT; `refresh_on_epoch` solves the first system
+    of each new A epoch after the switch by rGCROT ("intermittent solves");
+    `refresh_every` = n solves every n-th post-switch system by rGCROT.
+    rhs(t) -> b_t (device tensor, or pinned host tensor if host=True).
+    Returns the reports; solutions go to x_out[t] when given.  The operator
+    must hold the bands of epoch_of(0) on entry."""
     reps = []
     cur = epoch_of(0) if epoch_of else 0
     for t in range(n):
         e = epoch_of(t) if epoch_of else 0
-        if e != cur:
+        changed = e != cur
+        if changed:
             solver.op.update_bands(bands_for_epoch(e))
             cur = e
+        tag = method
         if method == "hybrid":
-            solver.set_method("rgcrot" if t < n_sw else "rbicgstab")
+            tag = "rgcrot" if _hybrid_uses_rgcrot(t, n_sw, changed, refresh_on_epoch,
+                                                  refresh_every) else "rbicgstab"
+            solver.set_method(tag)
         b = rhs(t)
         x = x_out[t] if x_out is not None else torch.zeros_like(b)
         x.zero_()
-        if host:
-            _, r = solver.solve_host(b, x, tol)
-        else:
-            _, r = solver.solve(b, x, tol)
-        r["tag"] = ("rgcrot" if t < n_sw else "rbicgstab") if method == "hybrid" else method
+        solve = solver.solve_host if host else solver.solve
+        _, r = solve(b, x, tol)
+        if method == "hybrid" and tag == "rbicgstab" and switchback and r["outcome"] != "CONVERGED":
+            solver.set_method("rgcrot")
+            x.zero_()
+            _, r2 = solve(b, x, tol)
+            for key in ("krylov_matvecs", "operator_applications", "seconds"):
+                r2[key] += r[key]
+            r = r2
+            tag = "rbicgstab+rgcrot"
+        r["tag"] = tag
         reps.append(r)
     return reps
+
+
+def _hybrid_uses_rgcrot(t, n_sw, epoch_changed, refresh_on_epoch, refresh_every):
+    """Hybrid schedule (R16): rGCROT for t < n_sw, and after the
+    switch on the first system of a new A epoch (refresh_on_epoch) or on
+    every refresh_every-th system; rBiCGStab otherwise."""
+    if t < n_sw:
+        return True
+    if refresh_on_epoch and epoch_changed:
+        return True
+    return bool(refresh_every) and (t - n_sw) % refresh_every == refresh_every - 1

@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(256) bicg_p_kernel(const double* __restrict__ 
     if (D) {
       const Vec<VEC> dn = ldv_stream<VEC>(D + n);
 #pragma unroll
-      for (int t = 0; t < VEC; ++t) zn.v[t] = (wl * pn.v[t]) * (1.0 / dn.v[t]);
+      for (int t = 0; t < VEC; ++t) zn.v[t] = (wl * pn.v[t]) * dn.v[t];
     }
     stv<VEC>(z + n, zn);
   }
@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(256) bicg_s_kernel(const double* __restrict__ 
     if (D) {
       const Vec<VEC> dn = ldv_stream<VEC>(D + n);
 #pragma unroll
-      for (int t = 0; t < VEC; ++t) zn.v[t] = (wl * sn.v[t]) * (1.0 / dn.v[t]);
+      for (int t = 0; t < VEC; ++t) zn.v[t] = (wl * sn.v[t]) * dn.v[t];
     }
     stv<VEC>(z + n, zn);
   }
@@ -151,7 +151,7 @@ __global__ void bicg_setup_kernel(double* xi, const double* eta0, int k, BiIter*
 void bicg_p(rk_op* op, const double* r, double* p, const double* v, double* z, double wl,
             bool jacobi, const BiIter* cur, const BiIter* prev, int first) {
   rk_ctx* ctx = op->ctx;
-  const double* D = jacobi ? op->bands : nullptr;
+  const double* D = jacobi ? op->invd() : nullptr;   // 1 / D
   const int vec = pick_vec(op->N, {r, p, v, z, D});
   Launch L(ctx, "bicg_p", 8.0 * op->N * ((first ? 3 : 5) + (jacobi ? 1 : 0)));
   if (vec == 2)
@@ -164,7 +164,7 @@ void bicg_p(rk_op* op, const double* r, double* p, const double* v, double* z, d
 void bicg_s(rk_op* op, const double* r, const double* v, double* s, double* z, double wl,
             bool jacobi, BiIter* cur) {
   rk_ctx* ctx = op->ctx;
-  const double* D = jacobi ? op->bands : nullptr;
+  const double* D = jacobi ? op->invd() : nullptr;   // 1 / D
   RedArgs ra = red_args(ctx, &cur->ss);
   const int vec = pick_vec(op->N, {r, v, s, z, D});
   Launch L(ctx, "bicg_s", 8.0 * op->N * (jacobi ? 5 : 4));

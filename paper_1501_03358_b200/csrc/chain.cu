@@ -32,6 +32,10 @@
 
 #include "rk_internal.h"
 
+#ifndef RK_CHAIN_LOADONLY
+#define RK_CHAIN_LOADONLY 0   // experiments: 1 = TMA traffic only, no stage arithmetic
+#endif
+
 namespace rk {
 
 template <int ST>
@@ -64,7 +68,7 @@ struct ChainGeom {
   static constexpr int PADX = (HALO + 1) % 2;                         // input box starts at gx0 - 1 - PADX
   static constexpr int XX = (EX + 2 + PADX + 1) / 2 * 2, XY = EY + 2; // input tile (+1 halo)
   static constexpr int NB = PD + 1, NXB = PD + 2;
-  static constexpr int B_BYTES = ST * EY * SX * 8;
+  static constexpr int B_BYTES = (ST + 1) * EY * SX * 8;           // bands + 1/D
   static constexpr int R_BYTES = EY * SX * 8;
   static constexpr int X_BYTES = XY * XX * 8;
   __host__ __device__ static constexpr int al(int b) { return (b + 127) / 128 * 128; }
@@ -157,7 +161,7 @@ struct ChainStep {
 #pragma unroll
     for (int d = 0; d < ST; ++d) bnd[PH][d] = bs[d * EY * SX];
     if (LOAD_R) rr[PH] = reinterpret_cast<const double*>(sb + G::R_OFF)[boff];
-    inv[PH] = bnd[PH][0] != 0.0 ? 1.0 / bnd[PH][0] : 0.0;
+    inv[PH] = bs[ST * EY * SX];   // 1/D (0 outside the grid: TMA zero fill)
     double ya = 0.0, yb = 0.0, xc = 0.0;
 #pragma unroll
     for (int d = 0; d < ST; ++d) {
@@ -313,6 +317,18 @@ chain_kernel(const __grid_constant__ CUtensorMap map_b, const __grid_constant__ 
     if (tid == 0 && tau + PD <= qlast) issue(tau + PD, xsi, bsi);                                  \
     if (tau + 1 <= qlast) mbar_wait(&bars[xsp], parp);                                             \
     using SP = ChainStep<ST, NST, TX, TY, PD, K0, K1, K2, PHV>;                                    \
+    if (RK_CHAIN_LOADONLY) {                                                                       \
+      __syncthreads();                                                                             \
+      xsm = xs0;                                                                                   \
+      xs0 = xsp;                                                                                   \
+      adv(xsp, NXB);                                                                               \
+      if (xsp == 0) parp ^= 1u;                                                                    \
+      adv(bs0, NB);                                                                                \
+      adv(xsi, NXB);                                                                               \
+      adv(bsi, NB);                                                                                \
+      ++tau;                                                                                       \
+      continue;                                                                                    \
+    }                                                                                              \
     const double v0 = SP::stage0(interior && tau >= z0 && tau < z1 && (pz || tau < nz),           \
                                  pl_of(tau), smem + bs0 * G::BSLOT, xtile(xsm), xtile(xs0),        \
                                  xtile(xsp), ring, bnd, rr, inv, cxy, boff, roff, cp);             \
@@ -375,21 +391,31 @@ void encode(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims,
 }
 
 template <int ST, int NST, int TX, int TY, int PD, int K0, int K1, int K2>
-void launch_one(rk_op* op, const ChainParams& cp, dim3 grid) {
+void launch_one(rk_op* op, ChainParams cp, dim3 grid) {
   using G = ChainGeom<ST, NST, TX, TY, PD>;
   static_assert(G::SMEM <= 232448, "chain tile exceeds 227 KB of shared memory");
   auto kern = chain_kernel<ST, NST, TX, TY, PD, K0, K1, K2>;
-  static bool attr = false;
-  if (!attr) {
+  static int occ = 0;   // resident CTAs per SM of this instantiation
+  if (!occ) {
     RK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
-    attr = true;
+    RK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, G::NTHR, G::SMEM));
+    occ = std::max(1, occ);
   }
+  // z chunks: a single wave of SMs x occ CTAs -- chunks = resident slots /
+  // tiles (>= 1), long chunks (>= 16 planes) to amortise the 2 (NST-1)-plane
+  // wavefront prologue
+  const int nzl = (int)op->g.nz_local;
+  const int tiles = (int)(grid.x * grid.y);
+  const int chunks = std::max(1, std::min(op->ctx->sms * occ / std::max(1, tiles), nzl / 16));
+  const int zc = std::max(1, std::min((nzl + chunks - 1) / chunks, nzl));
+  cp.zc = zc;
+  grid.z = (unsigned)((nzl + zc - 1) / zc);
   const cuuint64_t nx = op->g.nx, ny = op->g.ny, nz = op->g.nz_local;
   CUtensorMap mb, mr, mx;
   {
-    cuuint64_t dims[4] = {nx, ny, nz, (cuuint64_t)ST};
+    cuuint64_t dims[4] = {nx, ny, nz, (cuuint64_t)ST + 1};          // bands, then 1/D
     cuuint64_t str[3] = {nx * 8, nx * ny * 8, (cuuint64_t)op->N * 8};
-    cuuint32_t box[4] = {(cuuint32_t)G::SX, (cuuint32_t)G::EY, 1, (cuuint32_t)ST};
+    cuuint32_t box[4] = {(cuuint32_t)G::SX, (cuuint32_t)G::EY, 1, (cuuint32_t)ST + 1};
     encode(&mb, cp.bands, 4, dims, str, box);
   }
   {
@@ -433,11 +459,14 @@ void chain_dispatch(rk_op* op, const int* k, const ChainParams& cp, dim3 grid) {
 }
 
 // Tile configurations (interior TX x TY, prefetch distance PD).  RK_CHAIN_CFG
-// (read per launch; experiments only) selects one by index.
+// (read per launch; experiments only) selects one by index.  Measured at
+// 128^3 / 256^3 (scripts/micro/chain_bench.cu, r01): 32x16 pd2 is fastest;
+// smaller tiles (more CTAs per SM, deeper prefetch) lose to their larger
+// recomputed halo.
 struct TileCfg {
   int tx, ty, pd;
 };
-constexpr TileCfg CFGS[] = {{32, 16, 2}, {32, 8, 3}, {32, 8, 4}, {16, 16, 3}, {16, 16, 4}, {64, 8, 2}};
+constexpr TileCfg CFGS[] = {{32, 16, 2}, {32, 8, 2}, {16, 8, 2}, {16, 8, 3}, {16, 16, 2}};
 constexpr int NCFG = sizeof(CFGS) / sizeof(CFGS[0]);
 constexpr int DEFAULT_CFG = 0;
 
@@ -451,11 +480,10 @@ template <int NST>
 void chain_dispatch_cfg(int ci, rk_op* op, const int* k, const ChainParams& cp, dim3 grid) {
   switch (ci) {
     case 0: return chain_dispatch<NST, 32, 16, 2>(op, k, cp, grid);
-    case 1: return chain_dispatch<NST, 32, 8, 3>(op, k, cp, grid);
-    case 2: return chain_dispatch<NST, 32, 8, 4>(op, k, cp, grid);
-    case 3: return chain_dispatch<NST, 16, 16, 3>(op, k, cp, grid);
-    case 4: return chain_dispatch<NST, 16, 16, 4>(op, k, cp, grid);
-    default: return chain_dispatch<NST, 64, 8, 2>(op, k, cp, grid);
+    case 1: return chain_dispatch<NST, 32, 8, 2>(op, k, cp, grid);
+    case 2: return chain_dispatch<NST, 16, 8, 2>(op, k, cp, grid);
+    case 3: return chain_dispatch<NST, 16, 8, 3>(op, k, cp, grid);
+    default: return chain_dispatch<NST, 16, 16, 2>(op, k, cp, grid);
   }
 }
 
@@ -498,17 +526,9 @@ void chain_launch(rk_op* op, int nst, const int* kinds, const double* omegas, co
   cp.out_mid = out_mid;
   cp.out = out;
   for (int s = 0; s < nst; ++s) cp.omega[s] = omegas[s];
-  const int tiles = (int)((op->g.nx / tc.tx) * (op->g.ny / tc.ty));
-  // z chunks: one resident CTA per SM (the slot rings use most of the shared
-  // memory), so aim for a single wave -- chunks = SMs / tiles (>= 1), long
-  // chunks to amortise the 2 (NST-1)-plane wavefront prologue
-  const int nz = (int)op->g.nz_local;
-  const int chunks = std::max(1, std::min(ctx->sms / std::max(1, tiles), nz / 16));
-  int zc = (nz + chunks - 1) / chunks;
-  zc = std::max(1, std::min(zc, nz));
-  cp.zc = zc;
-  dim3 grid((unsigned)(op->g.nx / tc.tx), (unsigned)(op->g.ny / tc.ty), (unsigned)((nz + zc - 1) / zc));
-  // algorithmic bytes: bands once + stage-0 input + rhs (if any) + outputs
+  dim3 grid((unsigned)(op->g.nx / tc.tx), (unsigned)(op->g.ny / tc.ty), 1);   // z: launch_one
+  // algorithmic bytes: bands once + stage-0 input + rhs (if any) + outputs (the
+  // 1/D array is an implementation choice -- flops for bytes -- and not counted)
   const double words = op->S + 1 + ((kinds[0] != CK_SPMV1) ? 1 : 0) + 1 + (out_t ? 1 : 0) +
                        (out_mid ? 1 : 0);
   Launch L(ctx, "chain", 8.0 * op->N * words);

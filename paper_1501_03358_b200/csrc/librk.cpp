@@ -922,7 +922,8 @@ rk_status rk_op_create(rk_ctx* ctx, const rk_grid* g, int nbands, const int8_t* 
       op->P = g->nx * g->ny;
       op->N = op->P * g->nz_local;
       op->wrapz = ((g->periodic_mask & 4) && ctx->nranks == 1) ? 1 : 0;
-      cudaError_t e = cudaMalloc(&op->bands, sizeof(double) * op->S * op->N);
+      // [S][N] bands + [N] inverse diagonal (band S, see compute_invdiag)
+      cudaError_t e = cudaMalloc(&op->bands, sizeof(double) * (op->S + 1) * op->N);
       if (e != cudaSuccess) {
         cudaGetLastError();
         throw Error(RK_ENOMEM, "cudaMalloc of the bands failed");
@@ -932,6 +933,7 @@ rk_status rk_op_create(rk_ctx* ctx, const rk_grid* g, int nbands, const int8_t* 
       RK_REQUIRE(bad == 0, RK_EINVAL,
                  "bands violate truncation (S:39) or have a zero diagonal: " +
                      std::to_string(bad) + " bad coefficients");
+      compute_invdiag(op);
       op->user_offsets.assign(offsets, offsets + 3 * nbands);
       op->no_chain = std::getenv("RK_NO_CHAIN") != nullptr;
       op->force_chain = std::getenv("RK_FORCE_CHAIN") != nullptr;
@@ -950,6 +952,7 @@ rk_status rk_op_update_bands(rk_op* op, const double* bands) {
     copy_bands(op, op->user_offsets.data(), (int)op->user_offsets.size() / 3, bands);
     const int bad = validate_bands(op);
     RK_REQUIRE(bad == 0, RK_EINVAL, "bands violate truncation (S:39) or have a zero diagonal");
+    compute_invdiag(op);
     ++op->epoch;
   });
 }

@@ -64,6 +64,7 @@ enum StencilMode {
 
 struct StencilParams {
   const double* bands;  // [S][N] canonical order, band 0 = diagonal
+  const double* invd;   // [N] 1 / D
   int64_t N, P;
   int nx, ny, nzl;
   int px, py, wrapz;
@@ -89,7 +90,7 @@ enum ChainKind {
 };
 
 struct ChainParams {
-  const double* bands;
+  const double* bands;  // [S + 1][N]: bands, then 1 / D
   int64_t N, P;
   int nx, ny, nz;
   int px, py, pz;
@@ -155,7 +156,8 @@ struct rk_op {
   rk_grid g{};
   int S = 7;                    // 7, 19 or 27 (canonical layout)
   int64_t N = 0, P = 0;
-  double* bands = nullptr;      // [S][N]
+  double* bands = nullptr;      // [S][N] canonical bands, then [N] 1/D (invd())
+  const double* invd() const { return bands + (int64_t)S * N; }
   int64_t epoch = 0;
   // scratch (padded) for rk_op_apply / rk_precond_apply
   double* scratch_base[2] = {nullptr, nullptr};
@@ -241,6 +243,9 @@ void bicg_xr(rk_ctx* ctx, double* x, double* r, const double* s, const double* t
              const double* eta1, const double* eta2, int k);
 void bicg_setup(rk_ctx* ctx, double* xi, const double* eta0, int k, BiIter* it0);
 int validate_bands(rk_op* op);
+// band S := 1 / D (the Jacobi sweeps' reciprocal, computed once per matrix
+// epoch; 1.0 / D is correctly rounded, so every kernel sees the same bits)
+void compute_invdiag(rk_op* op);
 
 // communication (comm.cpp): no-ops for one rank
 void halo(rk_op* op, const double* v);

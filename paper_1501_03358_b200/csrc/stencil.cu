@@ -27,11 +27,11 @@ __global__ void __launch_bounds__(256) stencil_kernel(StencilParams sp) {
     if constexpr (MODE == SM_SCALE) {
       for (int iv = tx; iv < nxv; iv += BX) {
         const int64_t n = base + (int64_t)iv * VEC;
-        const Vec<VEC> D = ldv_stream<VEC>(sp.bands + n);
+        const Vec<VEC> iD = ldv_stream<VEC>(sp.invd + n);
         const Vec<VEC> r = ldv_ro<VEC>(sp.r + n);
         Vec<VEC> o;
 #pragma unroll
-        for (int t = 0; t < VEC; ++t) o.v[t] = (sp.omega * r.v[t]) * (1.0 / D.v[t]);
+        for (int t = 0; t < VEC; ++t) o.v[t] = (sp.omega * r.v[t]) * iD.v[t];
         stv<VEC>(sp.out0 + n, o);
       }
       continue;
@@ -110,7 +110,10 @@ __global__ void __launch_bounds__(256) stencil_kernel(StencilParams sp) {
 #pragma unroll
       for (int t = 0; t < VEC; ++t) y[t] = ya[t] + yb[t];
       const Vec<VEC>& x0 = xc[1][1];
-      Vec<VEC> o0, o1;
+      Vec<VEC> o0, o1, iD;
+      if constexpr (MODE == SM_SPMV_SWEEP1 || MODE == SM_SWEEP || MODE == SM_SWEEP_NORM ||
+                    MODE == SM_RESID_SWEEP1)
+        iD = ldv_stream<VEC>(sp.invd + n);
       if constexpr (MODE == SM_SPMV) {
 #pragma unroll
         for (int t = 0; t < VEC; ++t) o0.v[t] = y[t];
@@ -119,7 +122,7 @@ __global__ void __launch_bounds__(256) stencil_kernel(StencilParams sp) {
 #pragma unroll
         for (int t = 0; t < VEC; ++t) {
           o0.v[t] = y[t];
-          o1.v[t] = (sp.omega * y[t]) * (1.0 / a0[t]);
+          o1.v[t] = (sp.omega * y[t]) * iD.v[t];
         }
         stv<VEC>(sp.out0 + n, o0);
         stv<VEC>(sp.out1 + n, o1);
@@ -127,7 +130,7 @@ __global__ void __launch_bounds__(256) stencil_kernel(StencilParams sp) {
         const Vec<VEC> r = ldv_ro<VEC>(sp.r + n);
 #pragma unroll
         for (int t = 0; t < VEC; ++t) {
-          o0.v[t] = fma(sp.omega * (r.v[t] - y[t]), 1.0 / a0[t], x0.v[t]);
+          o0.v[t] = fma(sp.omega * (r.v[t] - y[t]), iD.v[t], x0.v[t]);
           if constexpr (MODE == SM_SWEEP_NORM) red[0] = fma(o0.v[t], o0.v[t], red[0]);
         }
         stv<VEC>(sp.out0 + n, o0);
@@ -137,7 +140,7 @@ __global__ void __launch_bounds__(256) stencil_kernel(StencilParams sp) {
         for (int t = 0; t < VEC; ++t) {
           o0.v[t] = r.v[t] - y[t];
           red[0] = fma(o0.v[t], o0.v[t], red[0]);
-          if constexpr (MODE == SM_RESID_SWEEP1) o1.v[t] = (sp.omega * o0.v[t]) * (1.0 / a0[t]);
+          if constexpr (MODE == SM_RESID_SWEEP1) o1.v[t] = (sp.omega * o0.v[t]) * iD.v[t];
         }
         stv<VEC>(sp.out0 + n, o0);
         if constexpr (MODE == SM_RESID_SWEEP1) stv<VEC>(sp.out1 + n, o1);
@@ -243,6 +246,7 @@ void stencil(rk_op* op, int mode, const double* x, const double* r, double* out0
   if (mode != SM_SCALE) halo(op, x);
   StencilParams sp;
   sp.bands = op->bands;
+  sp.invd = op->invd();
   sp.N = op->N;
   sp.P = op->P;
   sp.nx = (int)op->g.nx;
@@ -259,7 +263,7 @@ void stencil(rk_op* op, int mode, const double* x, const double* r, double* out0
   const bool red = (mode == SM_SWEEP_NORM || mode == SM_RESID || mode == SM_RESID_SWEEP1);
   sp.red = red ? red_args(ctx, red_out) : RedArgs{nullptr, nullptr, nullptr};
   // VEC = 2 needs even rows and 16-byte aligned rows of every array
-  int vec = (sp.nx % 2 == 0 && op->P % 2 == 0) ? pick_vec(op->N, {op->bands, x, r, out0, out1}) : 1;
+  int vec = (sp.nx % 2 == 0 && op->P % 2 == 0) ? pick_vec(op->N, {op->bands, op->invd(), x, r, out0, out1}) : 1;
   const int nxv = sp.nx / vec;
   const int bx = nxv >= 128 ? 128 : ((nxv + 31) / 32) * 32;
   dim3 blk(bx, 256 / bx);
@@ -274,6 +278,19 @@ void stencil(rk_op* op, int mode, const double* x, const double* r, double* out0
   }
   L.done();
   if (red) allreduce(ctx, red_out, 1);
+}
+
+__global__ void invdiag_kernel(const double* __restrict__ D, double* __restrict__ inv, int64_t N) {
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < N; n += (int64_t)gridDim.x * blockDim.x)
+    inv[n] = 1.0 / D[n];
+}
+
+void compute_invdiag(rk_op* op) {
+  rk_ctx* ctx = op->ctx;
+  Launch L(ctx, "invdiag", 16.0 * op->N);
+  invdiag_kernel<<<ctx->sms * 4, 256, 0, ctx->stream>>>(op->bands, op->bands + (int64_t)op->S * op->N,
+                                                       op->N);
+  L.done();
 }
 
 int validate_bands(rk_op* op) {

@@ -47,8 +47,8 @@ int main(int argc, char** argv) {
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  const char* names[] = {"32x16 pd2", "32x8 pd3", "32x8 pd4", "16x16 pd3", "16x16 pd4", "64x8 pd2"};
-  for (int ci = 0; ci < 6; ++ci) {
+  const char* names[] = {"32x16 pd2", "32x8 pd2", "16x8 pd2", "16x8 pd3", "16x16 pd2"};
+  for (int ci = 0; ci < 5; ++ci) {
   char buf[8];
   snprintf(buf, 8, "%d", ci);
   setenv("RK_CHAIN_CFG", buf, 1);
@@ -70,6 +70,30 @@ int main(int argc, char** argv) {
     printf("%-28s %8.1f us  %7.0f GB/s (alg %.0f W)  %s\n", c.name, us, c.words * 8.0 * op.N / (us * 1e-6) / 1e9,
            c.words, cudaGetErrorString(e));
   }
+  }
+  // two-stage launches (halo 1) for comparison, default tile config
+  setenv("RK_CHAIN_CFG", "0", 1);
+  {
+    int k2[2] = {rk::CK_SWEEP, rk::CK_SWEEP};
+    auto run = [&] { rk::chain_launch(&op, 2, k2, om, xb + op.P, r, nullptr, nullptr, out + op.P); };
+    for (int i = 0; i < 3; ++i) run();
+    cudaEventRecord(a, ctx.stream);
+    for (int i = 0; i < reps; ++i) run();
+    cudaEventRecord(b, ctx.stream);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    const double us = 1e3 * ms / reps;
+    printf("NST=2 SWEEP,SWEEP %8.1f us (%.1f us/stage)  %s\n", us, us / 2, cudaGetErrorString(cudaGetLastError()));
+    int k1[1] = {rk::CK_SWEEP};
+    auto run1 = [&] { rk::chain_launch(&op, 1, k1, om, xb + op.P, r, nullptr, nullptr, out + op.P); };
+    for (int i = 0; i < 3; ++i) run1();
+    cudaEventRecord(a, ctx.stream);
+    for (int i = 0; i < reps; ++i) run1();
+    cudaEventRecord(b, ctx.stream);
+    cudaEventSynchronize(b);
+    cudaEventElapsedTime(&ms, a, b);
+    printf("NST=1 SWEEP       %8.1f us  %s\n", 1e3 * ms / reps, cudaGetErrorString(cudaGetLastError()));
   }
   return 0;
 }
