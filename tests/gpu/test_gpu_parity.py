@@ -180,7 +180,7 @@ def test_chain_bitwise_equals_unfused(rk, ctx, shape, periodic, monkeypatch):
 
 
 # ------------------------------------------------------------ solves
-def gpu_sequence(rk, ctx, w, solver_name=None, host=False):
+def gpu_sequence(rk, ctx, w, solver_name=None, host=False, **policy):
     prob = w.problem()
     prm = w.params
     method = solver_name or prm.method
@@ -192,7 +192,8 @@ def gpu_sequence(rk, ctx, w, solver_name=None, host=False):
     rhs = (lambda t: torch.from_numpy(prob.rhs(t).reshape(-1)).pin_memory()) if host else \
         (lambda t: dev(prob.rhs(t).reshape(-1)))
     reps = rk.solve_sequence(s, rhs, w.n_systems, method, n_sw=prm.n_sw, epoch_of=w.epoch,
-                             bands_for_epoch=lambda e: dev(prob.bands(epoch=e)), host=host, x_out=xs)
+                             bands_for_epoch=lambda e: dev(prob.bands(epoch=e)), host=host, x_out=xs,
+                             **policy)
     out = [(r, x.cpu().numpy()) for r, x in zip(reps, xs)]
     U, C, R = s.recycle_export()
     s.close()
@@ -261,6 +262,27 @@ def test_sequence_parity_T2(rk, ctx, name):
                  w0.epoch_every, w0.description)
     ora = run_sequence(w)
     gpu, _ = gpu_sequence(rk, ctx, w)
+    compare_sequences(w, gpu, ora, w.params.method)
+
+
+@pytest.mark.parametrize("name,policy,kw", [
+    ("c3s", {"switchback": True}, {"divergence": 0.15}),
+    ("c4hs", {"refresh_on_epoch": True}, {}),
+    ("c4hs", {"refresh_every": 2}, {}),
+])
+def test_sequence_parity_hybrid_policies(rk, ctx, name, policy, kw):
+    """Hybrid policy options (R16) through the GPU controller vs the oracle:
+    switch-back of an unstable rBiCGStab system to rGCROT, and intermittent
+    rGCROT solves at A epochs / every n systems.  Same method schedule (tags)
+    on both sides, then the usual per-system parity."""
+    from dataclasses import replace
+    from problems.workloads import Workload
+    w0 = get_workload(name)
+    w = Workload(w0.name, w0.make_problem, replace(w0.params, **kw), w0.n_systems, w0.epoch_every,
+                 w0.description)
+    ora = run_sequence(w, **policy)
+    gpu, _ = gpu_sequence(rk, ctx, w, **policy)
+    assert [r["tag"] for r, _ in gpu] == [t for t, _, _ in ora]
     compare_sequences(w, gpu, ora, w.params.method)
 
 

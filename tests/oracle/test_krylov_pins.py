@@ -365,3 +365,42 @@ def test_rgcrot_T2_invariants_and_solution():
         assert np.linalg.norm(AU - C) <= 1e-11 * np.linalg.norm(U)
         assert np.linalg.norm(b - op.apply(x)) <= prm.tol * np.linalg.norm(b)
     assert truncated
+
+
+def _with(w0, **kw):
+    from problems.workloads import Workload
+    return Workload(w0.name, w0.make_problem, replace(w0.params, **kw), w0.n_systems,
+                    w0.epoch_every, w0.description)
+
+
+def test_hybrid_switchback_policy():
+    """P:668-669 / SPEC hybrid allow_switchback (reading R16): an rBiCGStab
+    solve that does not converge is re-solved by rGCROT from x = 0 and the
+    run continues with rBiCGStab.  Instability threshold 0.15 ||r0|| makes
+    exactly system 5 of c3s unstable (its residual peaks at 0.26 ||r0||, the
+    others stay below 0.095 ||r0||); counts are conserved."""
+    from oracle.krylov import OUTCOME_NAMES
+    w = _with(get_workload("c3s"), divergence=0.15)
+    plain = run_sequence(w)
+    assert [OUTCOME_NAMES[r.outcome] for _, _, r in plain][5] == "UNSTABLE"
+    out = run_sequence(w, switchback=True)
+    tags = [t for t, _, _ in out]
+    assert tags == ["rgcrot"] * 3 + ["rbicgstab", "rbicgstab", "rbicgstab+rgcrot", "rbicgstab", "rbicgstab"]
+    assert all(rep.outcome == CONVERGED for _, _, rep in out)
+    rep5 = out[5][2]
+    failed = plain[5][2].krylov_mv
+    assert rep5.krylov_mv > failed and rep5.cycles >= 1
+
+
+def test_hybrid_refresh_on_epoch_policy():
+    """P:666-667 "intermittent solves with rGCROT to update the recycle space
+    ... when the system matrix changes" (R16): with A epochs every 3 systems
+    and the switch after 3, systems 3 and 6 (first of a new epoch) are solved
+    by rGCROT, the others by rBiCGStab; every system converges.  With
+    refresh_every = 2 every second post-switch system is an rGCROT solve."""
+    w = get_workload("c4hs")
+    out = run_sequence(w, refresh_on_epoch=True)
+    assert [t for t, _, _ in out] == ["rgcrot"] * 4 + ["rbicgstab"] * 2 + ["rgcrot"] + ["rbicgstab"] * 2
+    assert all(r.outcome == CONVERGED for _, _, r in out)
+    every = run_sequence(w, refresh_every=2)
+    assert [t for t, _, _ in every] == ["rgcrot"] * 3 + ["rbicgstab", "rgcrot"] * 3
