@@ -68,12 +68,18 @@ typedef struct {
 } rk_grid;
 
 /* Jacobi(5+1) preconditioner: z = w_l D^-1 r; (sweeps-1) x
- * z += w_l D^-1 (r - A z); then z += w_g D^-1 (r - A z).  kind 0 = none. */
+ * z += w_l D^-1 (r - A_l z); then z += w_g D^-1 (r - A z).  kind 0 = none.
+ * zblocks <= 1: A_l = A (every sweep global, reading D9).  zblocks = P > 1:
+ * the paper's "sweeps ... on the local sub-domains" -- A_l drops every
+ * coupling between the P equal z-blocks (R17); requires P | nz and,
+ * on several ranks, that every rank owns whole blocks (those sweeps then
+ * exchange no halo).  RK_EINVAL otherwise. */
 typedef struct {
   int kind;            /* 0 none, 1 jacobi                          */
   int sweeps;          /* local relaxed sweeps (paper: 5)           */
   double omega_local;  /* 0.8 (reading D9)                          */
   double omega_global; /* 1.0 (reading D9)                          */
+  int zblocks;         /* block-Jacobi z-blocks (0/1 = global)      */
 } rk_precond;
 
 typedef struct {

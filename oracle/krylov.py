@@ -413,7 +413,7 @@ def run_sequence(workload, systems=None, solver=None, callback=None, switchback=
         new_epoch = e != epoch
         if new_epoch:
             op = Operator.from_problem(prob, epoch=e)
-            pc = Jacobi(op, prm.sweeps, prm.omega_l, prm.omega_g)
+            pc = Jacobi(op, prm.sweeps, prm.omega_l, prm.omega_g, getattr(prm, "zblocks", 1))
             epoch = e
         if U is None:
             U = np.zeros((op.N, 0))

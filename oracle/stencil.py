@@ -132,14 +132,39 @@ def to_dense(op, cap=8192):
     return Ad
 
 
-def jacobi(op, r, sweeps=5, omega_l=0.8, omega_g=1.0):
+def local_operator(op, zblocks):
+    """A_loc: A with every coupling between different z-blocks removed.  The
+    z axis is cut into `zblocks` equal slabs (planes [b nz/P, (b+1) nz/P),
+    the rank decomposition of SURVEY §8(e)); a band reaching across a slab
+    boundary (including the periodic wrap) gets a zero coefficient there, so
+    A_loc is block diagonal with the diagonal blocks of A (overlapping
+    Schwarz with zero overlap)."""
+    assert op.nz % zblocks == 0, "z-blocks must divide nz"
+    zb = op.nz // zblocks
+    bands = op.bands.copy()
+    k = np.arange(op.nz)
+    for d, (dx, dy, dz) in enumerate(op.offsets):
+        if dz == 0:
+            continue
+        cross = ((k + dz) // zb != k // zb) | (k + dz < 0) | (k + dz >= op.nz)
+        bands[d][cross] = 0.0
+    per = op.periodic & ~4 if zblocks > 1 else op.periodic
+    return Operator(op.nx, op.ny, op.nz, per, op.offsets, bands)
+
+
+def jacobi(op, r, sweeps=5, omega_l=0.8, omega_g=1.0, zblocks=1):
     """O2: z ~= M^-1 r by `sweeps` under-relaxed Jacobi sweeps from z = 0
-    followed by one point-Jacobi sweep with omega_g."""
+    followed by one point-Jacobi sweep with omega_g.  With
+    zblocks > 1 the `sweeps` relaxed sweeps are the paper's "sweeps on the
+    local sub-domains" -- they use A_loc (local_operator: no coupling between
+    z-blocks, so no communication between ranks owning whole blocks) -- and
+    the last sweep is the global one (reading R17)."""
     D = op.diag()
     r = np.asarray(r, dtype=np.float64)
+    A_l = op if zblocks <= 1 else local_operator(op, zblocks)
     z = omega_l * r / D                              # first sweep from z = 0
     for _ in range(sweeps - 1):
-        z = z + omega_l * (r - op.apply(z)) / D
+        z = z + omega_l * (r - A_l.apply(z)) / D
     z = z + omega_g * (r - op.apply(z)) / D          # global point-Jacobi sweep
     return z
 
@@ -147,8 +172,9 @@ def jacobi(op, r, sweeps=5, omega_l=0.8, omega_g=1.0):
 class Jacobi:
     """The preconditioner as a callable r -> M^-1 r (a fixed linear map)."""
 
-    def __init__(self, op, sweeps=5, omega_l=0.8, omega_g=1.0):
+    def __init__(self, op, sweeps=5, omega_l=0.8, omega_g=1.0, zblocks=1):
         self.op, self.sweeps, self.omega_l, self.omega_g = op, sweeps, omega_l, omega_g
+        self.zblocks = zblocks
 
     def __call__(self, r):
-        return jacobi(self.op, r, self.sweeps, self.omega_l, self.omega_g)
+        return jacobi(self.op, r, self.sweeps, self.omega_l, self.omega_g, self.zblocks)

@@ -24,7 +24,7 @@ class rk_grid(C.Structure):
 
 class rk_precond(C.Structure):
     _fields_ = [("kind", C.c_int), ("sweeps", C.c_int), ("omega_local", C.c_double),
-                ("omega_global", C.c_double)]
+                ("omega_global", C.c_double), ("zblocks", C.c_int)]
 
 
 class rk_config(C.Structure):

@@ -102,9 +102,9 @@ class GridOperator:
         L.check(L.lib().rk_op_apply(self.h, _p(x), _p(y)), "rk_op_apply")
         return y
 
-    def precond(self, r, z=None, kind=1, sweeps=5, omega_l=0.8, omega_g=1.0):
+    def precond(self, r, z=None, kind=1, sweeps=5, omega_l=0.8, omega_g=1.0, zblocks=1):
         z = torch.empty_like(r) if z is None else z
-        pc = L.rk_precond(kind, sweeps, omega_l, omega_g)
+        pc = L.rk_precond(kind, sweeps, omega_l, omega_g, zblocks)
         L.check(L.lib().rk_precond_apply(self.h, C.byref(pc), _p(r), _p(z)), "rk_precond_apply")
         return z
 
@@ -116,8 +116,8 @@ class GridOperator:
 
 def make_config(method="rgcrot", m=20, k_max=10, k_keep=5, select_count=1, precond="jacobi",
                 sweeps=5, omega_l=0.8, omega_g=1.0, tol=1e-8, max_matvecs=2000,
-                divergence=1e4, trunc="T1"):
-    pc = L.rk_precond(1 if precond == "jacobi" else 0, sweeps, omega_l, omega_g)
+                divergence=1e4, trunc="T1", zblocks=1):
+    pc = L.rk_precond(1 if precond == "jacobi" else 0, sweeps, omega_l, omega_g, zblocks)
     return L.rk_config(L.METHODS[method], m, k_max, k_keep, select_count, 0,
                        {"T1": 0, "T2": 1}[trunc], pc, tol, max_matvecs, divergence)
 
@@ -132,7 +132,7 @@ def config_from_params(prm, method=None):
                        select_count=0 if k == 0 else prm.p1,
                        sweeps=prm.sweeps, omega_l=prm.omega_l, omega_g=prm.omega_g,
                        tol=prm.tol, max_matvecs=prm.max_mv, divergence=prm.divergence,
-                       trunc=getattr(prm, "trunc", "T1"))
+                       trunc=getattr(prm, "trunc", "T1"), zblocks=getattr(prm, "zblocks", 1))
 
 
 def _report(r):

@@ -162,13 +162,20 @@ struct ChainStep {
     for (int d = 0; d < ST; ++d) bnd[PH][d] = bs[d * EY * SX];
     if (LOAD_R) rr[PH] = reinterpret_cast<const double*>(sb + G::R_OFF)[boff];
     inv[PH] = bs[ST * EY * SX];   // 1/D (0 outside the grid: TMA zero fill)
+    // block-Jacobi local sweep (R17): no coupling across z-block boundaries
+    bool cut_m = false, cut_p = false;
+    if (cp.zb > 0 && cp.local[0]) {
+      const int g = cp.zg0 + pl_tau;
+      cut_m = (g % cp.zb) == 0;
+      cut_p = ((g + 1) % cp.zb) == 0;
+    }
     double ya = 0.0, yb = 0.0, xc = 0.0;
 #pragma unroll
     for (int d = 0; d < ST; ++d) {
       int dx = 0, dy = 0, dz = 0;
       coffs<ST>(d, dx, dy, dz);
       const double* xt = dz < 0 ? xm : (dz > 0 ? xp : x0);
-      const double xv = xt[dy * XX + dx];
+      const double xv = (dz < 0 && cut_m) || (dz > 0 && cut_p) ? 0.0 : xt[dy * XX + dx];
       if (d == 0) xc = xv;
       if (d % 2 == 0) ya = fma(bnd[PH][d], xv, ya);
       else yb = fma(bnd[PH][d], xv, yb);
@@ -210,12 +217,18 @@ struct ChainStep {
     const double* rb = ring + (S - 1) * 3 * RPL + roff;
     const double* rm = rb + ((R + 2) % 3) * RPL;
     const double* r0 = rb + R * RPL;
+    bool cut_m = false, cut_p = false;       // block-Jacobi local sweep (R17)
+    if (cp.zb > 0 && cp.local[S]) {
+      const int g = cp.zg0 + pl_q;
+      cut_m = (g % cp.zb) == 0;
+      cut_p = ((g + 1) % cp.zb) == 0;
+    }
     double ya = 0.0, yb = 0.0, zc = 0.0;
 #pragma unroll
     for (int d = 0; d < ST; ++d) {
       int dx = 0, dy = 0, dz = 0;
       coffs<ST>(d, dx, dy, dz);
-      const double zv = dz > 0 ? up : (dz < 0 ? rm[0] : r0[dy * EX + dx]);
+      const double zv = dz > 0 ? (cut_p ? 0.0 : up) : (dz < 0 ? (cut_m ? 0.0 : rm[0]) : r0[dy * EX + dx]);
       if (d == 0) zc = zv;
       if (d % 2 == 0) ya = fma(bnd[R][d], zv, ya);
       else yb = fma(bnd[R][d], zv, yb);
@@ -505,7 +518,8 @@ int chain_max_stages(const rk_op* op) {
 }
 
 void chain_launch(rk_op* op, int nst, const int* kinds, const double* omegas, const double* xin,
-                  const double* r, double* out_t, double* out_mid, double* out) {
+                  const double* r, double* out_t, double* out_mid, double* out, const int* local,
+                  int zb) {
   rk_ctx* ctx = op->ctx;
   const int ci = cfg_index();
   const TileCfg tc = CFGS[ci];
@@ -526,6 +540,9 @@ void chain_launch(rk_op* op, int nst, const int* kinds, const double* omegas, co
   cp.out_mid = out_mid;
   cp.out = out;
   for (int s = 0; s < nst; ++s) cp.omega[s] = omegas[s];
+  cp.zb = zb;
+  cp.zg0 = (int)op->g.z0;
+  for (int s = 0; s < nst; ++s) cp.local[s] = local ? local[s] : 0;
   dim3 grid((unsigned)(op->g.nx / tc.tx), (unsigned)(op->g.ny / tc.ty), 1);   // z: launch_one
   // algorithmic bytes: bands once + stage-0 input + rhs (if any) + outputs (the
   // 1/D array is an implementation choice -- flops for bytes -- and not counted)
@@ -540,9 +557,11 @@ void chain_launch(rk_op* op, int nst, const int* kinds, const double* omegas, co
 
 void chain_run(rk_op* op, const std::vector<int>& kinds, const std::vector<double>& om,
                const double* xin, const double* r, double* out_t, double* out_mid, double* out,
-               double* za, double* zb) {
+               double* za, double* zb, const std::vector<int>& local, int zbs) {
   const int n = (int)kinds.size();
   const int nmax = chain_max_stages(op);
+  std::vector<int> loc(n, 0);
+  for (int q = 0; q < n && q < (int)local.size(); ++q) loc[q] = local[q];
   double* bufs[2] = {za, zb};
   if (xin == za) std::swap(bufs[0], bufs[1]);
   const double* rhs = kinds[0] == CK_SPMV1 ? out_t : r;
@@ -551,7 +570,8 @@ void chain_run(rk_op* op, const std::vector<int>& kinds, const std::vector<doubl
     for (int q = 0; q < n; ++q) {
       double* dst = (q == n - 1) ? out : ((q == n - 2 && out_mid) ? out_mid : bufs[q % 2]);
       if (kinds[q] == CK_SPMV1) stencil(op, SM_SPMV_SWEEP1, cur, nullptr, out_t, dst, om[q], nullptr);
-      else if (kinds[q] == CK_SWEEP) stencil(op, SM_SWEEP, cur, rhs, dst, nullptr, om[q], nullptr);
+      else if (kinds[q] == CK_SWEEP)
+        stencil(op, SM_SWEEP, cur, rhs, dst, nullptr, om[q], nullptr, loc[q] ? zbs : 0);
       else stencil(op, SM_SPMV, cur, nullptr, dst, nullptr, 0.0, nullptr);
       cur = dst;
     }
@@ -565,7 +585,8 @@ void chain_run(rk_op* op, const std::vector<int>& kinds, const std::vector<doubl
     const bool last = (i == g - 1);
     double* dst = last ? out : bufs[i % 2];
     chain_launch(op, len, kinds.data() + a, om.data() + a, cur, rhs,
-                 (kinds[a] == CK_SPMV1) ? out_t : nullptr, last ? out_mid : nullptr, dst);
+                 (kinds[a] == CK_SPMV1) ? out_t : nullptr, last ? out_mid : nullptr, dst,
+                 loc.data() + a, zbs);
     cur = dst;
     a += len;
   }

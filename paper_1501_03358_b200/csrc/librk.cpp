@@ -212,6 +212,16 @@ std::vector<double> t2_directions(int k, int m, const std::vector<double>& B,
   return W;
 }
 
+// Block-Jacobi z-blocks [R17]: equal blocks, and on several ranks every rank
+// owns whole blocks (its local sweeps then need no halo exchange).
+void check_zblocks(const rk_op* op, const rk_precond& pc) {
+  if (pc.zblocks <= 1) return;
+  RK_REQUIRE(op->g.nz_global % pc.zblocks == 0, RK_EINVAL, "zblocks must divide nz");
+  const int64_t zb = op->g.nz_global / pc.zblocks;
+  RK_REQUIRE(op->g.z0 % zb == 0 && op->g.nz_local % zb == 0, RK_EINVAL,
+             "every rank must own whole z-blocks (zblocks a multiple of the rank count)");
+}
+
 }  // namespace
 
 // --------------------------------------------------------------- solver
@@ -279,24 +289,32 @@ struct rk_solver {
   // temporally blocked kernel (up to chain_max_stages() stages per launch)
   // when available, else one stencil launch per stage (same arithmetic).
   void run_chain(const std::vector<int>& kinds, const std::vector<double>& om, const double* xin,
-                 const double* r, double* out_t, double* out_mid, double* out) {
-    chain_run(op, kinds, om, xin, r, out_t, out_mid, out, za, zb);
+                 const double* r, double* out_t, double* out_mid, double* out,
+                 const std::vector<int>& local = {}) {
+    chain_run(op, kinds, om, xin, r, out_t, out_mid, out, za, zb, local, zblock());
+  }
+  // block-Jacobi: planes per z-block of the local sweeps (0 = all sweeps global) [R17]
+  int zblock() const {
+    return cfg.pc.zblocks > 1 ? (int)(op->g.nz_global / cfg.pc.zblocks) : 0;
   }
 
   // Jacobi sweeps 2..sweeps+1 (the first sweep's output is in za):
-  // z <- z + w_l D^-1 (r - A z) (sweeps-1 times), then dst = z + w_g D^-1 (r - A z).
+  // z <- z + w_l D^-1 (r - A_loc z) (sweeps-1 times, local [R17]), then
+  // dst = z + w_g D^-1 (r - A z) (global).
   void sweeps(const double* r, double* dst, double* red) {
     const rk_precond& pc = cfg.pc;
     if (!red) {
       std::vector<int> k(pc.sweeps, CK_SWEEP);
       std::vector<double> w(pc.sweeps, pc.omega_local);
+      std::vector<int> loc(pc.sweeps, 1);
       w.back() = pc.omega_global;
-      run_chain(k, w, za, r, nullptr, nullptr, dst);
+      loc.back() = 0;
+      run_chain(k, w, za, r, nullptr, nullptr, dst, loc);
       return;
     }
     double *zin = za, *zout = zb;
     for (int q = 1; q < pc.sweeps; ++q) {
-      stencil(op, SM_SWEEP, zin, r, zout, nullptr, pc.omega_local, nullptr);
+      stencil(op, SM_SWEEP, zin, r, zout, nullptr, pc.omega_local, nullptr, zblock());
       std::swap(zin, zout);
     }
     stencil(op, SM_SWEEP_NORM, zin, r, dst, nullptr, pc.omega_global, red);
@@ -304,14 +322,17 @@ struct rk_solver {
   bool jac() const { return cfg.pc.kind == 1; }
 
   // dst = M^-1 A v  (left-preconditioned operator, Alg. 3 line 6):
-  // stages [t = A v, z1 = w_l t/D], sweeps 2..5 (w_l), sweep 6 (w_g)
+  // stages [t = A v, z1 = w_l t/D], sweeps 2..5 (w_l, local), sweep 6 (w_g)
   void apply_ahat(const double* v, double* dst) {
     if (jac()) {
       std::vector<int> k(cfg.pc.sweeps + 1, CK_SWEEP);
       std::vector<double> w(cfg.pc.sweeps + 1, cfg.pc.omega_local);
+      std::vector<int> loc(cfg.pc.sweeps + 1, 1);
       k[0] = CK_SPMV1;
+      loc[0] = 0;
       w.back() = cfg.pc.omega_global;
-      run_chain(k, w, v, nullptr, t, nullptr, dst);
+      loc.back() = 0;
+      run_chain(k, w, v, nullptr, t, nullptr, dst, loc);
     } else {
       stencil(op, SM_SPMV, v, nullptr, dst, nullptr, 0.0, nullptr);
     }
@@ -320,10 +341,13 @@ struct rk_solver {
   void apply_right(const double* rhs, double* phat, double* v) {
     std::vector<int> k(cfg.pc.sweeps + 1, CK_SWEEP);
     std::vector<double> w(cfg.pc.sweeps + 1, cfg.pc.omega_local);
+    std::vector<int> loc(cfg.pc.sweeps + 1, 1);
     w[cfg.pc.sweeps - 1] = cfg.pc.omega_global;
+    loc[cfg.pc.sweeps - 1] = 0;
     k.back() = CK_SPMV;
     w.back() = 0.0;
-    run_chain(k, w, za, rhs, nullptr, phat, v);
+    loc.back() = 0;
+    run_chain(k, w, za, rhs, nullptr, phat, v, loc);
   }
   // dst = M^-1 r (r need not be padded), optional ||dst||^2
   void apply_minv(const double* r, double* dst, double* red) {
@@ -992,13 +1016,17 @@ rk_status rk_precond_apply(rk_op* op, const rk_precond* pc, const double* r, dou
                               op->ctx->stream));
     } else {
       RK_REQUIRE(pc->kind == 1 && pc->sweeps >= 1, RK_EINVAL, "bad preconditioner");
+      check_zblocks(op, *pc);
       op_scratch(op);
       double *za = op->scratch[0], *zb = op->scratch[1];
       stencil(op, SM_SCALE, nullptr, r, za, nullptr, pc->omega_local, nullptr);
       std::vector<int> k(pc->sweeps, CK_SWEEP);
       std::vector<double> w(pc->sweeps, pc->omega_local);
+      std::vector<int> loc(pc->sweeps, 1);
       w.back() = pc->omega_global;
-      chain_run(op, k, w, za, r, nullptr, nullptr, z, za, zb);
+      loc.back() = 0;
+      const int zbl = pc->zblocks > 1 ? (int)(op->g.nz_global / pc->zblocks) : 0;
+      chain_run(op, k, w, za, r, nullptr, nullptr, z, za, zb, loc, zbl);
     }
     RK_CUDA(cudaStreamSynchronize(op->ctx->stream));
   });
@@ -1017,6 +1045,7 @@ rk_status rk_solver_create(rk_op* op, const rk_config* cfg, rk_solver** out) {
     RK_REQUIRE(cfg->trunc == 0 || cfg->trunc == 1, RK_EINVAL, "trunc: 0 (T1) or 1 (T2)");
     RK_REQUIRE(cfg->pc.kind == 0 || (cfg->pc.kind == 1 && cfg->pc.sweeps >= 1), RK_EINVAL,
                "bad preconditioner");
+    if (cfg->pc.kind == 1) check_zblocks(op, cfg->pc);
     RK_REQUIRE(cfg->max_matvecs >= 1, RK_EINVAL, "max_matvecs >= 1");
     RK_CUDA(cudaSetDevice(op->ctx->device));
     auto* s = new rk_solver();

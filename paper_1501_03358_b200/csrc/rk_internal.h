@@ -74,6 +74,7 @@ struct StencilParams {
   double* out1;
   double omega;
   RedArgs red;
+  int zb, zg0;          // local (block-Jacobi) sweep: z-block size in planes (0 = global), global z of plane 0
 };
 
 struct LcOut {
@@ -101,6 +102,8 @@ struct ChainParams {
   double* out;          // output of the last stage
   double omega[3];
   int zc;               // z planes per CTA
+  int zb, zg0;          // z-block size (0 = none) and global z of plane 0 (block-Jacobi)
+  int local[3];         // stage s is a local sweep (no coupling across z-blocks)
 };
 
 // Per-iteration device scalars of rBiCGStab (one 64-byte record per iteration).
@@ -208,19 +211,23 @@ struct Launch {
 // fused chain (chain.cu): max stages per launch for this operator (0 = unavailable)
 int chain_max_stages(const rk_op* op);
 void chain_launch(rk_op* op, int nst, const int* kinds, const double* omegas, const double* xin,
-                  const double* r, double* out_t, double* out_mid, double* out);
+                  const double* r, double* out_t, double* out_mid, double* out,
+                  const int* local = nullptr, int zb = 0);
 // Runs n chained stencil stages; fused (TMA) launches of up to chain_max_stages()
 // stages when available, else one stencil launch per stage.  za/zb: padded scratch.
+// local[q] != 0: stage q is a local sweep of the block-Jacobi preconditioner
+// (couplings across z-blocks of zbs planes dropped; reading R17).
 void chain_run(rk_op* op, const std::vector<int>& kinds, const std::vector<double>& om,
                const double* xin, const double* r, double* out_t, double* out_mid, double* out,
-               double* za, double* zb);
+               double* za, double* zb, const std::vector<int>& local = {}, int zbs = 0);
 
 // ------------------------------------------------------------ launch layer
 // All kernels are launched through these wrappers (stencil.cu, blockops.cu, bicg.cu).  Each
 // increments ctx->launches and, when profiling, is bracketed by events.
 void init_ctx_kernels(rk_ctx* ctx);
+// zb > 0: local sweep of the block-Jacobi preconditioner (z-blocks of zb planes)
 void stencil(rk_op* op, int mode, const double* x, const double* r, double* out0,
-             double* out1, double omega, double* red_out);
+             double* out1, double omega, double* red_out, int zb = 0);
 void bdot(rk_ctx* ctx, const std::vector<const double*>& cols, const double* w, int64_t N,
           double* out);
 void bupd(rk_ctx* ctx, const std::vector<const double*>& cols, const double* g, double gscale,

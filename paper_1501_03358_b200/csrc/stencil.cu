@@ -85,6 +85,21 @@ __global__ void __launch_bounds__(256) stencil_kernel(StencilParams sp) {
             if (uses<ST>(1, dy, dz)) xr[dy + 1][dz + 1] = __ldg(p + ip);
           }
         }
+      // block-Jacobi local sweep (R17): no coupling across z-block boundaries
+      if (sp.zb > 0) {
+        const int g = sp.zg0 + k;
+        const bool cut_m = (g % sp.zb) == 0, cut_p = ((g + 1) % sp.zb) == 0;
+#pragma unroll
+        for (int dy = 0; dy < 3; ++dy) {
+#pragma unroll
+          for (int t = 0; t < VEC; ++t) {
+            if (cut_m) xc[dy][0].v[t] = 0.0;
+            if (cut_p) xc[dy][2].v[t] = 0.0;
+          }
+          if (cut_m) xl[dy][0] = xr[dy][0] = 0.0;
+          if (cut_p) xl[dy][2] = xr[dy][2] = 0.0;
+        }
+      }
       // two interleaved FMA chains (even / odd bands), summed at the end --
       // the same order as the fused chain kernel (chain.cu)
       double y[VEC], ya[VEC], yb[VEC], a0[VEC];
@@ -241,9 +256,11 @@ void init_ctx_kernels(rk_ctx* ctx) {
 }
 
 void stencil(rk_op* op, int mode, const double* x, const double* r, double* out0, double* out1,
-             double omega, double* red_out) {
+             double omega, double* red_out, int zb) {
   rk_ctx* ctx = op->ctx;
-  if (mode != SM_SCALE) halo(op, x);
+  // a local sweep on ranks that own whole z-blocks needs no halo (R17)
+  const bool no_halo = zb > 0 && op->g.z0 % zb == 0 && op->g.nz_local % zb == 0;
+  if (mode != SM_SCALE && !no_halo) halo(op, x);
   StencilParams sp;
   sp.bands = op->bands;
   sp.invd = op->invd();
@@ -260,6 +277,8 @@ void stencil(rk_op* op, int mode, const double* x, const double* r, double* out0
   sp.out0 = out0;
   sp.out1 = out1;
   sp.omega = omega;
+  sp.zb = zb;
+  sp.zg0 = (int)op->g.z0;
   const bool red = (mode == SM_SWEEP_NORM || mode == SM_RESID || mode == SM_RESID_SWEEP1);
   sp.red = red ? red_args(ctx, red_out) : RedArgs{nullptr, nullptr, nullptr};
   // VEC = 2 needs even rows and 16-byte aligned rows of every array

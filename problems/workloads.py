@@ -30,6 +30,7 @@ class SolverParams:
     omega_l: float = 0.8
     omega_g: float = 1.0
     divergence: float = 1e4
+    zblocks: int = 1             # block-Jacobi z-blocks of the local sweeps (1 = global, R17)
 
 
 def k_trunc(k):

@@ -179,6 +179,49 @@ def test_chain_bitwise_equals_unfused(rk, ctx, shape, periodic, monkeypatch):
     plain.close()
 
 
+# Block-Jacobi preconditioner (reading R17): the local
+# sweeps drop every coupling between z-blocks.  Unfused and fused (chain) paths.
+@pytest.mark.parametrize("name,mk,zblocks,force", [
+    ("channel24", lambda: channel19(24), 4, False),                 # periodic z, 19-point
+    ("porous40", lambda: porous7(40, 4), 5, False),
+    ("c3_full_chain", lambda: porous7(128, 6), 4, False),           # fused chain (above L2)
+    ("random_96x48x40_chain", lambda: _random7(96, 48, 40, 0, 21), 8, True),
+    ("random_64x32x48_pz_chain", lambda: _random7(64, 32, 48, 4, 22), 3, True),
+])
+def test_block_jacobi_parity(rk, ctx, name, mk, zblocks, force, monkeypatch):
+    prob = mk()
+    if force:
+        monkeypatch.setenv("RK_FORCE_CHAIN", "1")
+    op = make_op(rk, ctx, prob)
+    monkeypatch.delenv("RK_FORCE_CHAIN", raising=False)
+    ref = Operator.from_problem(prob)
+    r = np.random.default_rng(9).uniform(-1, 1, prob.N)
+    z = op.precond(dev(r), zblocks=zblocks).cpu().numpy()
+    zr = Jacobi(ref, zblocks=zblocks)(r)
+    assert np.max(np.abs(z - zr)) <= 1e-12 * np.max(np.abs(zr))
+    zg = Jacobi(ref)(r)
+    assert np.max(np.abs(zr - zg)) > 1e-6 * np.max(np.abs(zg))   # the blocks matter
+    op.close()
+
+
+def test_block_jacobi_chain_bitwise_and_rejects_bad_blocks(rk, ctx, monkeypatch):
+    nx, ny, nz = 64, 32, 48
+    bands = dev(random_op_problem(nx, ny, nz, 4, OFFSETS7, 13))
+    mk = lambda: rk.GridOperator(ctx, nx, ny, nz, OFFSETS7, bands, 4)
+    monkeypatch.setenv("RK_FORCE_CHAIN", "1")
+    fused = mk()
+    monkeypatch.delenv("RK_FORCE_CHAIN")
+    monkeypatch.setenv("RK_NO_CHAIN", "1")
+    plain = mk()
+    monkeypatch.delenv("RK_NO_CHAIN")
+    r = dev(np.random.default_rng(2).uniform(-1, 1, nx * ny * nz))
+    assert torch.equal(fused.precond(r, zblocks=6), plain.precond(r, zblocks=6))
+    with pytest.raises(RuntimeError, match="zblocks"):
+        plain.precond(r, zblocks=5)                                  # 5 does not divide 48
+    fused.close()
+    plain.close()
+
+
 # ------------------------------------------------------------ solves
 def gpu_sequence(rk, ctx, w, solver_name=None, host=False, **policy):
     prob = w.problem()
@@ -249,6 +292,19 @@ def test_sequence_parity(rk, ctx, name, solver):
     ora = run_sequence(w, solver=method)
     gpu, _ = gpu_sequence(rk, ctx, w, method)
     compare_sequences(w, gpu, ora, method)
+
+
+@pytest.mark.parametrize("name,zblocks", [("c3s", 4), ("c2s", 2), ("c4hs", 4)])
+def test_sequence_parity_block_jacobi(rk, ctx, name, zblocks):
+    """Whole hybrid / rGCROT sequences with the block-Jacobi preconditioner."""
+    from dataclasses import replace
+    from problems.workloads import Workload
+    w0 = get_workload(name)
+    w = Workload(w0.name, w0.make_problem, replace(w0.params, zblocks=zblocks), w0.n_systems,
+                 w0.epoch_every, w0.description)
+    ora = run_sequence(w)
+    gpu, _ = gpu_sequence(rk, ctx, w)
+    compare_sequences(w, gpu, ora, w.params.method)
 
 
 @pytest.mark.parametrize("name", ["c2s", "c3s", "c4s"])

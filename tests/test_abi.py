@@ -58,11 +58,11 @@ def test_version_and_error_string(librk):
 
 
 def test_struct_layouts(librk):
-    # rk_config: method,m,k_max,k_keep,select_count,ortho,trunc (7 ints) + rk_precond (24 B,
-    # 8-aligned at 32) + tol + max_matvecs + divergence
-    assert ctypes.sizeof(librk.rk_precond) == 24
+    # rk_config: method,m,k_max,k_keep,select_count,ortho,trunc (7 ints) + rk_precond (32 B:
+    # 2 ints, 2 doubles, zblocks + padding; 8-aligned at 32) + tol + max_matvecs + divergence
+    assert ctypes.sizeof(librk.rk_precond) == 32
     assert librk.rk_config.pc.offset == 32
-    assert ctypes.sizeof(librk.rk_config) == 80
+    assert ctypes.sizeof(librk.rk_config) == 88
     assert ctypes.sizeof(librk.rk_report) == 72
     assert ctypes.sizeof(librk.rk_grid) == 48
 
@@ -75,7 +75,7 @@ def test_abi_struct_sizes_match_c(tmp_path):
     exe = tmp_path / "sz"
     subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
     out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()
-    assert out == ["80", "72", "48", "24", "32"]
+    assert out == ["88", "72", "48", "32", "32"]
 
 
 def test_product_does_not_import_oracle():
