@@ -73,9 +73,13 @@ typedef struct {
  * the paper's "sweeps ... on the local sub-domains" -- A_l drops every
  * coupling between the P equal z-blocks (R17); requires P | nz and,
  * on several ranks, that every rank owns whole blocks (those sweeps then
- * exchange no halo).  RK_EINVAL otherwise. */
+ * exchange no halo).  RK_EINVAL otherwise.
+ * kind 2 = SSOR (R18): from z = 0, `sweeps` x
+ * (forward then backward multicolour SOR pass, colour = (i&1) + 2(j&1) +
+ * 4(k&1), relaxation omega_local) and one global point-Jacobi sweep with
+ * omega_global; periodic axes need even extents (RK_EINVAL otherwise). */
 typedef struct {
-  int kind;            /* 0 none, 1 jacobi                          */
+  int kind;            /* 0 none, 1 jacobi, 2 ssor                  */
   int sweeps;          /* local relaxed sweeps (paper: 5)           */
   double omega_local;  /* 0.8 (reading D9)                          */
   double omega_global; /* 1.0 (reading D9)                          */

@@ -397,7 +397,7 @@ def run_sequence(workload, systems=None, solver=None, callback=None, switchback=
                           by rGCROT (SPEC refresh_every_n).
     Returns [(tag, x, report)]; a switched-back system has tag
     'rbicgstab+rgcrot' and a report with the summed counts."""
-    from .stencil import Operator, Jacobi
+    from .stencil import Operator
     prm = workload.params
     method = solver or prm.method
     prob = workload.problem()
@@ -413,7 +413,7 @@ def run_sequence(workload, systems=None, solver=None, callback=None, switchback=
         new_epoch = e != epoch
         if new_epoch:
             op = Operator.from_problem(prob, epoch=e)
-            pc = Jacobi(op, prm.sweeps, prm.omega_l, prm.omega_g, getattr(prm, "zblocks", 1))
+            pc = make_precond(op, prm)
             epoch = e
         if U is None:
             U = np.zeros((op.N, 0))
@@ -447,6 +447,18 @@ def run_sequence(workload, systems=None, solver=None, callback=None, switchback=
         if callback:
             callback(t, tag, x, U, C, rep)
     return out
+
+
+def make_precond(op, prm):
+    """The preconditioner named by prm.precond: Jacobi(5+1) (optionally block
+    Jacobi, R17), multicolour SSOR(5)+1 (R18) or none (identity)."""
+    from .stencil import Jacobi, SSOR
+    kind = getattr(prm, "precond", "jacobi")
+    if kind == "ssor":
+        return SSOR(op, prm.sweeps, getattr(prm, "omega_s", 1.0), prm.omega_g)
+    if kind == "none":
+        return lambda r: np.array(r, dtype=np.float64, copy=True)
+    return Jacobi(op, prm.sweeps, prm.omega_l, prm.omega_g, getattr(prm, "zblocks", 1))
 
 
 def hybrid_uses_rgcrot(t, n_sw, epoch_changed, refresh_on_epoch, refresh_every):

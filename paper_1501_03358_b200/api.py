@@ -103,6 +103,8 @@ class GridOperator:
         return y
 
     def precond(self, r, z=None, kind=1, sweeps=5, omega_l=0.8, omega_g=1.0, zblocks=1):
+        """M^-1 r: kind 1 = Jacobi(sweeps)+1 (zblocks > 1: block Jacobi, R17),
+        2 = multicolour SSOR(sweeps)+1 with omega_l as the SOR relaxation (R18)."""
         z = torch.empty_like(r) if z is None else z
         pc = L.rk_precond(kind, sweeps, omega_l, omega_g, zblocks)
         L.check(L.lib().rk_precond_apply(self.h, C.byref(pc), _p(r), _p(z)), "rk_precond_apply")
@@ -117,7 +119,7 @@ class GridOperator:
 def make_config(method="rgcrot", m=20, k_max=10, k_keep=5, select_count=1, precond="jacobi",
                 sweeps=5, omega_l=0.8, omega_g=1.0, tol=1e-8, max_matvecs=2000,
                 divergence=1e4, trunc="T1", zblocks=1):
-    pc = L.rk_precond(1 if precond == "jacobi" else 0, sweeps, omega_l, omega_g, zblocks)
+    pc = L.rk_precond({"none": 0, "jacobi": 1, "ssor": 2}[precond], sweeps, omega_l, omega_g, zblocks)
     return L.rk_config(L.METHODS[method], m, k_max, k_keep, select_count, 0,
                        {"T1": 0, "T2": 1}[trunc], pc, tol, max_matvecs, divergence)
 
@@ -128,9 +130,11 @@ def config_from_params(prm, method=None):
     if meth == "hybrid":
         meth = "rgcrot"
     k = 0 if meth in ("gmres", "bicgstab") else prm.k_max
+    pcn = getattr(prm, "precond", "jacobi")
     return make_config(method=meth, m=prm.m, k_max=k, k_keep=min(prm.k_t, k),
-                       select_count=0 if k == 0 else prm.p1,
-                       sweeps=prm.sweeps, omega_l=prm.omega_l, omega_g=prm.omega_g,
+                       select_count=0 if k == 0 else prm.p1, precond=pcn, sweeps=prm.sweeps,
+                       omega_l=getattr(prm, "omega_s", 1.0) if pcn == "ssor" else prm.omega_l,
+                       omega_g=prm.omega_g,
                        tol=prm.tol, max_matvecs=prm.max_mv, divergence=prm.divergence,
                        trunc=getattr(prm, "trunc", "T1"), zblocks=getattr(prm, "zblocks", 1))
 

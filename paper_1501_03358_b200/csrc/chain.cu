@@ -378,6 +378,12 @@ chain_kernel(const __grid_constant__ CUtensorMap map_b, const __grid_constant__ 
 #undef RK_CHAIN_STEP
 }
 
+}  // namespace rk
+
+#include "chain_x2.cuh"
+
+namespace rk {
+
 // ------------------------------------------------------------------- host
 namespace {
 
@@ -403,15 +409,19 @@ void encode(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims,
   RK_REQUIRE(r == CUDA_SUCCESS, RK_ECUDA, "cuTensorMapEncodeTiled failed");
 }
 
-template <int ST, int NST, int TX, int TY, int PD, int K0, int K1, int K2>
+template <int ST, int NST, int TX, int TY, int PD, int K0, int K1, int K2, int X2>
 void launch_one(rk_op* op, ChainParams cp, dim3 grid) {
   using G = ChainGeom<ST, NST, TX, TY, PD>;
   static_assert(G::SMEM <= 232448, "chain tile exceeds 227 KB of shared memory");
-  auto kern = chain_kernel<ST, NST, TX, TY, PD, K0, K1, K2>;
+  using KernFn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, ChainParams);
+  KernFn kern;
+  if constexpr (X2 != 0) kern = chain_kernel_x2<ST, NST, TX, TY, PD, K0, K1, K2>;
+  else kern = chain_kernel<ST, NST, TX, TY, PD, K0, K1, K2>;
+  const int nthr = X2 ? G::NTHR / 2 : G::NTHR;
   static int occ = 0;   // resident CTAs per SM of this instantiation
   if (!occ) {
     RK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
-    RK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, G::NTHR, G::SMEM));
+    RK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nthr, G::SMEM));
     occ = std::max(1, occ);
   }
   // z chunks: a single wave of SMs x occ CTAs -- chunks = resident slots /
@@ -443,30 +453,30 @@ void launch_one(rk_op* op, ChainParams cp, dim3 grid) {
     cuuint32_t box[3] = {(cuuint32_t)G::XX, (cuuint32_t)G::XY, 1};
     encode(&mx, cp.xin - op->P, 3, dims, str, box);
   }
-  dim3 blk(G::EX, G::EY);
+  dim3 blk(X2 ? G::EX / 2 : G::EX, G::EY);
   kern<<<grid, blk, G::SMEM, op->ctx->stream>>>(mb, mr, mx, cp);
 }
 
-template <int NST, int TX, int TY, int PD>
+template <int NST, int TX, int TY, int PD, int X2 = 0>
 void chain_dispatch(rk_op* op, const int* k, const ChainParams& cp, dim3 grid) {
   if constexpr (NST == 3) {
     if (k[0] == CK_SPMV1 && k[1] == CK_SWEEP && k[2] == CK_SWEEP)
-      return launch_one<7, 3, TX, TY, PD, CK_SPMV1, CK_SWEEP, CK_SWEEP>(op, cp, grid);
+      return launch_one<7, 3, TX, TY, PD, CK_SPMV1, CK_SWEEP, CK_SWEEP, X2>(op, cp, grid);
     if (k[0] == CK_SWEEP && k[1] == CK_SWEEP && k[2] == CK_SWEEP)
-      return launch_one<7, 3, TX, TY, PD, CK_SWEEP, CK_SWEEP, CK_SWEEP>(op, cp, grid);
+      return launch_one<7, 3, TX, TY, PD, CK_SWEEP, CK_SWEEP, CK_SWEEP, X2>(op, cp, grid);
     if (k[0] == CK_SWEEP && k[1] == CK_SWEEP && k[2] == CK_SPMV)
-      return launch_one<7, 3, TX, TY, PD, CK_SWEEP, CK_SWEEP, CK_SPMV>(op, cp, grid);
+      return launch_one<7, 3, TX, TY, PD, CK_SWEEP, CK_SWEEP, CK_SPMV, X2>(op, cp, grid);
   } else if constexpr (NST == 2) {
     if (k[0] == CK_SPMV1 && k[1] == CK_SWEEP)
-      return launch_one<7, 2, TX, TY, PD, CK_SPMV1, CK_SWEEP, 0>(op, cp, grid);
+      return launch_one<7, 2, TX, TY, PD, CK_SPMV1, CK_SWEEP, 0, X2>(op, cp, grid);
     if (k[0] == CK_SWEEP && k[1] == CK_SWEEP)
-      return launch_one<7, 2, TX, TY, PD, CK_SWEEP, CK_SWEEP, 0>(op, cp, grid);
+      return launch_one<7, 2, TX, TY, PD, CK_SWEEP, CK_SWEEP, 0, X2>(op, cp, grid);
     if (k[0] == CK_SWEEP && k[1] == CK_SPMV)
-      return launch_one<7, 2, TX, TY, PD, CK_SWEEP, CK_SPMV, 0>(op, cp, grid);
+      return launch_one<7, 2, TX, TY, PD, CK_SWEEP, CK_SPMV, 0, X2>(op, cp, grid);
   } else {
-    if (k[0] == CK_SPMV1) return launch_one<7, 1, TX, TY, PD, CK_SPMV1, 0, 0>(op, cp, grid);
-    if (k[0] == CK_SWEEP) return launch_one<7, 1, TX, TY, PD, CK_SWEEP, 0, 0>(op, cp, grid);
-    return launch_one<7, 1, TX, TY, PD, CK_SPMV, 0, 0>(op, cp, grid);
+    if (k[0] == CK_SPMV1) return launch_one<7, 1, TX, TY, PD, CK_SPMV1, 0, 0, X2>(op, cp, grid);
+    if (k[0] == CK_SWEEP) return launch_one<7, 1, TX, TY, PD, CK_SWEEP, 0, 0, X2>(op, cp, grid);
+    return launch_one<7, 1, TX, TY, PD, CK_SPMV, 0, 0, X2>(op, cp, grid);
   }
   throw Error(RK_EINVAL, "unsupported chain stage combination");
 }
@@ -479,7 +489,7 @@ void chain_dispatch(rk_op* op, const int* k, const ChainParams& cp, dim3 grid) {
 struct TileCfg {
   int tx, ty, pd;
 };
-constexpr TileCfg CFGS[] = {{32, 16, 2}, {32, 8, 2}, {16, 8, 2}, {16, 8, 3}, {16, 16, 2}};
+constexpr TileCfg CFGS[] = {{32, 16, 2}, {32, 8, 2}, {16, 8, 2}, {16, 8, 3}, {16, 16, 2}, {32, 16, 2}};
 constexpr int NCFG = sizeof(CFGS) / sizeof(CFGS[0]);
 constexpr int DEFAULT_CFG = 0;
 
@@ -496,7 +506,10 @@ void chain_dispatch_cfg(int ci, rk_op* op, const int* k, const ChainParams& cp, 
     case 1: return chain_dispatch<NST, 32, 8, 2>(op, k, cp, grid);
     case 2: return chain_dispatch<NST, 16, 8, 2>(op, k, cp, grid);
     case 3: return chain_dispatch<NST, 16, 8, 3>(op, k, cp, grid);
-    default: return chain_dispatch<NST, 16, 16, 2>(op, k, cp, grid);
+    case 4: return chain_dispatch<NST, 16, 16, 2>(op, k, cp, grid);
+    default:   // x-pairs (chain_x2.cuh); needs an even halo
+      if constexpr (NST == 3) return chain_dispatch<NST, 32, 16, 2, 1>(op, k, cp, grid);
+      else return chain_dispatch<NST, 32, 16, 2>(op, k, cp, grid);
   }
 }
 

@@ -212,6 +212,30 @@ std::vector<double> t2_directions(int k, int m, const std::vector<double>& B,
   return W;
 }
 
+// SSOR(sweeps) + 1 preconditioner (reading R18): from z = 0, `sweeps` x
+// (forward colour passes 0..7, backward 7..0) of in-place multicolour SOR
+// with omega_local, then the global point-Jacobi sweep (omega_global) into
+// dst (+ ||dst||^2 into red).  zbuf: padded scratch.
+void ssor_apply(rk_op* op, const rk_precond& pc, const double* r, double* dst, double* zbuf,
+                double* red) {
+  RK_CUDA(cudaMemsetAsync(zbuf, 0, sizeof(double) * op->N, op->ctx->stream));
+  for (int s = 0; s < pc.sweeps; ++s) {
+    for (int c = 0; c < 8; ++c) colour_sweep(op, zbuf, r, pc.omega_local, c);
+    for (int c = 7; c >= 0; --c) colour_sweep(op, zbuf, r, pc.omega_local, c);
+  }
+  stencil(op, red ? SM_SWEEP_NORM : SM_SWEEP, zbuf, r, dst, nullptr, pc.omega_global, red);
+}
+
+// SSOR's colouring needs even extents on periodic axes (a wrap would couple
+// two cells of one colour)
+void check_ssor(const rk_op* op, const rk_precond& pc) {
+  if (pc.kind != 2) return;
+  const uint32_t pm = op->g.periodic_mask;
+  RK_REQUIRE(!(pm & 1) || op->g.nx % 2 == 0, RK_EINVAL, "SSOR: periodic x needs an even nx");
+  RK_REQUIRE(!(pm & 2) || op->g.ny % 2 == 0, RK_EINVAL, "SSOR: periodic y needs an even ny");
+  RK_REQUIRE(!(pm & 4) || op->g.nz_global % 2 == 0, RK_EINVAL, "SSOR: periodic z needs an even nz");
+}
+
 // Block-Jacobi z-blocks [R17]: equal blocks, and on several ranks every rank
 // owns whole blocks (its local sweeps then need no halo exchange).
 void check_zblocks(const rk_op* op, const rk_precond& pc) {
@@ -320,6 +344,10 @@ struct rk_solver {
     stencil(op, SM_SWEEP_NORM, zin, r, dst, nullptr, pc.omega_global, red);
   }
   bool jac() const { return cfg.pc.kind == 1; }
+  bool ssor() const { return cfg.pc.kind == 2; }
+  void ssor_to(const double* r, double* dst, double* red) {
+    ssor_apply(op, cfg.pc, r, dst, za, red);
+  }
 
   // dst = M^-1 A v  (left-preconditioned operator, Alg. 3 line 6):
   // stages [t = A v, z1 = w_l t/D], sweeps 2..5 (w_l, local), sweep 6 (w_g)
@@ -333,6 +361,9 @@ struct rk_solver {
       w.back() = cfg.pc.omega_global;
       loc.back() = 0;
       run_chain(k, w, v, nullptr, t, nullptr, dst, loc);
+    } else if (ssor()) {
+      stencil(op, SM_SPMV, v, nullptr, t, nullptr, 0.0, nullptr);
+      ssor_to(t, dst, nullptr);
     } else {
       stencil(op, SM_SPMV, v, nullptr, dst, nullptr, 0.0, nullptr);
     }
@@ -354,6 +385,8 @@ struct rk_solver {
     if (jac()) {
       stencil(op, SM_SCALE, nullptr, r, za, nullptr, cfg.pc.omega_local, nullptr);
       sweeps(r, dst, red);
+    } else if (ssor()) {
+      ssor_to(r, dst, red);
     } else {
       RK_CUDA(cudaMemcpyAsync(dst, r, sizeof(double) * N, cudaMemcpyDeviceToDevice, ctx->stream));
       if (red) bdot(ctx, {dst}, dst, N, red);
@@ -469,6 +502,9 @@ struct rk_solver {
       if (jac()) {
         stencil(op, SM_RESID_SWEEP1, x, b, rt, za, cfg.pc.omega_local, misc(TRUE2));
         sweeps(rt, V[0], misc(RHAT2));
+      } else if (ssor()) {
+        stencil(op, SM_RESID, x, b, rt, nullptr, 0.0, misc(TRUE2));
+        ssor_to(rt, V[0], misc(RHAT2));
       } else {
         stencil(op, SM_RESID, x, b, V[0], nullptr, 0.0, misc(RHAT2));
       }
@@ -679,6 +715,7 @@ struct rk_solver {
       }
       if (rep.krylov_matvecs >= cfg.max_matvecs) break;
       if (jac()) sweeps(rt, V[0], nullptr);                   // r = M^-1 r_true
+      else if (ssor()) ssor_to(rt, V[0], nullptr);
       else RK_CUDA(cudaMemcpyAsync(V[0], rt, sizeof(double) * N, cudaMemcpyDeviceToDevice, ctx->stream));
     }
   }
@@ -744,6 +781,7 @@ struct rk_solver {
           apply_right(p, ph, v);               // p_hat = M^-1 p ; v = A p_hat
         } else {
           bicg_p(op, r, p, v, ph, 1.0, false, cur, i ? bi(i - 1) : cur, i == 0);
+          if (ssor()) ssor_to(p, ph, nullptr);   // p_hat = M^-1 p (SSOR, R18)
           stencil(op, SM_SPMV, ph, nullptr, v, nullptr, 0.0, nullptr);
         }
         rep.krylov_matvecs += 1;
@@ -756,8 +794,12 @@ struct rk_solver {
         }
         // line 8: alpha = rho / sigma ; s = r - alpha v (+ first sweep of s_hat)
         bicg_s(op, r, v, s, jac() ? za : sh, wl, jac(), cur);
-        if (jac()) apply_right(s, sh, tt);      // s_hat = M^-1 s ; t = A s_hat (line 12)
-        else stencil(op, SM_SPMV, sh, nullptr, tt, nullptr, 0.0, nullptr);
+        if (jac()) {
+          apply_right(s, sh, tt);               // s_hat = M^-1 s ; t = A s_hat (line 12)
+        } else {
+          if (ssor()) ssor_to(s, sh, nullptr);
+          stencil(op, SM_SPMV, sh, nullptr, tt, nullptr, 0.0, nullptr);
+        }
         rep.krylov_matvecs += 1;
         if (k > 0) {                                              // line 12a
           bdot(ctx, C, tt, N, eta(1));
@@ -1014,6 +1056,11 @@ rk_status rk_precond_apply(rk_op* op, const rk_precond* pc, const double* r, dou
     if (pc->kind == 0) {
       RK_CUDA(cudaMemcpyAsync(z, r, sizeof(double) * op->N, cudaMemcpyDeviceToDevice,
                               op->ctx->stream));
+    } else if (pc->kind == 2) {
+      RK_REQUIRE(pc->sweeps >= 1, RK_EINVAL, "bad preconditioner");
+      check_ssor(op, *pc);
+      op_scratch(op);
+      ssor_apply(op, *pc, r, z, op->scratch[0], nullptr);
     } else {
       RK_REQUIRE(pc->kind == 1 && pc->sweeps >= 1, RK_EINVAL, "bad preconditioner");
       check_zblocks(op, *pc);
@@ -1043,8 +1090,9 @@ rk_status rk_solver_create(rk_op* op, const rk_config* cfg, rk_solver** out) {
     RK_REQUIRE(cfg->k_keep >= 0 && cfg->k_keep <= cfg->k_max, RK_EINVAL, "0 <= k_keep <= k_max");
     RK_REQUIRE(cfg->ortho == 0, RK_EUNSUPPORTED, "only CGS2");
     RK_REQUIRE(cfg->trunc == 0 || cfg->trunc == 1, RK_EINVAL, "trunc: 0 (T1) or 1 (T2)");
-    RK_REQUIRE(cfg->pc.kind == 0 || (cfg->pc.kind == 1 && cfg->pc.sweeps >= 1), RK_EINVAL,
-               "bad preconditioner");
+    RK_REQUIRE(cfg->pc.kind == 0 || ((cfg->pc.kind == 1 || cfg->pc.kind == 2) && cfg->pc.sweeps >= 1),
+               RK_EINVAL, "bad preconditioner");
+    check_ssor(op, cfg->pc);
     if (cfg->pc.kind == 1) check_zblocks(op, cfg->pc);
     RK_REQUIRE(cfg->max_matvecs >= 1, RK_EINVAL, "max_matvecs >= 1");
     RK_CUDA(cudaSetDevice(op->ctx->device));

@@ -253,6 +253,9 @@ int validate_bands(rk_op* op);
 // band S := 1 / D (the Jacobi sweeps' reciprocal, computed once per matrix
 // epoch; 1.0 / D is correctly rounded, so every kernel sees the same bits)
 void compute_invdiag(rk_op* op);
+// one multicolour SOR pass over the cells of `colour` (0..7), in place on the
+// padded vector z (SSOR preconditioner, reading R18)
+void colour_sweep(rk_op* op, double* z, const double* r, double omega, int colour);
 
 // communication (comm.cpp): no-ops for one rank
 void halo(rk_op* op, const double* v);

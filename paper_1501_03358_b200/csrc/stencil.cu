@@ -299,6 +299,77 @@ void stencil(rk_op* op, int mode, const double* x, const double* r, double* out0
   if (red) allreduce(ctx, red_out, 1);
 }
 
+// Multicolour SOR pass of the SSOR preconditioner (reading R18): the cells
+// of colour c = (i&1) + 2 (j&1) + 4 (k_global&1) are relaxed in place,
+// z_n += w (r_n - (A z)_n) / D_n; they only couple to other colours (every
+// stencil offset is in {-1,0,1}^3), so the pass is race free.  One thread
+// per cell of the colour; x/y neighbours clamped (zero coefficient) or
+// wrapped, z neighbours from the ghost planes or wrapped (single rank).
+template <int ST>
+__global__ void __launch_bounds__(256) colour_sweep_kernel(StencilParams sp, int colour) {
+  const int ci = colour & 1, cj = (colour >> 1) & 1, ck = (colour >> 2) & 1;
+  const int hx = (sp.nx - ci + 1) / 2;                 // cells of parity ci in a row
+  const int hy = (sp.ny - cj + 1) / 2;
+  const int kstart = ((ck - sp.zg0) % 2 + 2) % 2;      // first local plane of parity ck (global)
+  const int hz = (sp.nzl - kstart + 1) / 2;
+  const int64_t total = (int64_t)hx * hy * hz;
+  double* z = const_cast<double*>(sp.x);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = ci + 2 * (int)(e % hx);
+    const int64_t rest = e / hx;
+    const int j = cj + 2 * (int)(rest % hy);
+    const int k = kstart + 2 * (int)(rest / hy);
+    const int64_t n = (int64_t)k * sp.P + (int64_t)j * sp.nx + i;
+    double ya = 0.0, yb = 0.0;
+#pragma unroll
+    for (int d = 0; d < ST; ++d) {
+      int dx = 0, dy = 0, dz = 0;
+      offs<ST>(d, dx, dy, dz);
+      int ii = i + dx, jj = j + dy, kk = k + dz;
+      if (sp.px) ii = ii < 0 ? sp.nx - 1 : (ii >= sp.nx ? 0 : ii);
+      else ii = ii < 0 ? 0 : (ii >= sp.nx ? sp.nx - 1 : ii);
+      if (sp.py) jj = jj < 0 ? sp.ny - 1 : (jj >= sp.ny ? 0 : jj);
+      else jj = jj < 0 ? 0 : (jj >= sp.ny ? sp.ny - 1 : jj);
+      if (sp.wrapz) kk = kk < 0 ? sp.nzl - 1 : (kk >= sp.nzl ? 0 : kk);
+      const double a = sp.bands[(int64_t)d * sp.N + n];
+      const double xv = z[(int64_t)kk * sp.P + (int64_t)jj * sp.nx + ii];
+      if (d % 2 == 0) ya = fma(a, xv, ya);
+      else yb = fma(a, xv, yb);
+    }
+    z[n] = fma(sp.omega * (sp.r[n] - (ya + yb)), sp.invd[n], z[n]);
+  }
+}
+
+void colour_sweep(rk_op* op, double* z, const double* r, double omega, int colour) {
+  rk_ctx* ctx = op->ctx;
+  halo(op, z);
+  StencilParams sp;
+  std::memset(&sp, 0, sizeof(sp));
+  sp.bands = op->bands;
+  sp.invd = op->invd();
+  sp.N = op->N;
+  sp.P = op->P;
+  sp.nx = (int)op->g.nx;
+  sp.ny = (int)op->g.ny;
+  sp.nzl = (int)op->g.nz_local;
+  sp.px = (op->g.periodic_mask & 1) ? 1 : 0;
+  sp.py = (op->g.periodic_mask & 2) ? 1 : 0;
+  sp.wrapz = op->wrapz;
+  sp.x = z;
+  sp.r = r;
+  sp.omega = omega;
+  sp.zg0 = (int)op->g.z0;
+  const int64_t cells = (op->N + 7) / 8;
+  Launch L(ctx, "ssor_colour", 8.0 * op->N * (op->S + 4) / 8.0);
+  switch (op->S) {
+    case 7: launch_k(ctx, colour_sweep_kernel<7>, cells, dim3(256), sp, colour); break;
+    case 19: launch_k(ctx, colour_sweep_kernel<19>, cells, dim3(256), sp, colour); break;
+    default: launch_k(ctx, colour_sweep_kernel<27>, cells, dim3(256), sp, colour); break;
+  }
+  L.done();
+}
+
 __global__ void invdiag_kernel(const double* __restrict__ D, double* __restrict__ inv, int64_t N) {
   for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < N; n += (int64_t)gridDim.x * blockDim.x)
     inv[n] = 1.0 / D[n];

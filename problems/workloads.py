@@ -31,6 +31,8 @@ class SolverParams:
     omega_g: float = 1.0
     divergence: float = 1e4
     zblocks: int = 1             # block-Jacobi z-blocks of the local sweeps (1 = global, R17)
+    precond: str = "jacobi"      # jacobi | ssor (multicolour, R18) | none
+    omega_s: float = 1.0         # SSOR relaxation (SPEC S:106 default)
 
 
 def k_trunc(k):

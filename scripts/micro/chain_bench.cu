@@ -47,8 +47,8 @@ int main(int argc, char** argv) {
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  const char* names[] = {"32x16 pd2", "32x8 pd2", "16x8 pd2", "16x8 pd3", "16x16 pd2"};
-  for (int ci = 0; ci < 5; ++ci) {
+  const char* names[] = {"32x16 pd2", "32x8 pd2", "16x8 pd2", "16x8 pd3", "16x16 pd2", "32x16 pd2 x-pairs"};
+  for (int ci = 0; ci < 6; ++ci) {
   char buf[8];
   snprintf(buf, 8, "%d", ci);
   setenv("RK_CHAIN_CFG", buf, 1);
@@ -99,5 +99,5 @@ int main(int argc, char** argv) {
 }
 // chain_run's unfused fallback is not exercised here
 namespace rk {
-void stencil(rk_op*, int, const double*, const double*, double*, double*, double, double*) { abort(); }
+void stencil(rk_op*, int, const double*, const double*, double*, double*, double, double*, int) { abort(); }
 }

@@ -158,8 +158,9 @@ def test_precond_parity_chain(rk, ctx, name, mk, monkeypatch):
     op.close()
 
 
+@pytest.mark.parametrize("cfg", ["0", "5"])   # one cell per thread / x-pairs (chain_x2.cuh)
 @pytest.mark.parametrize("shape,periodic", [((64, 32, 48), 4), ((32, 16, 17), 4), ((96, 48, 40), 0)])
-def test_chain_bitwise_equals_unfused(rk, ctx, shape, periodic, monkeypatch):
+def test_chain_bitwise_equals_unfused(rk, ctx, shape, periodic, cfg, monkeypatch):
     """The fused chain and the one-stage-per-launch stencil path share the
     per-cell arithmetic (two FMA chains, 1/D), so M^-1 r and M^-1 A v agree
     bit for bit; RK_NO_CHAIN (read at rk_op_create) selects the unfused path."""
@@ -173,8 +174,12 @@ def test_chain_bitwise_equals_unfused(rk, ctx, shape, periodic, monkeypatch):
     plain = mk()
     monkeypatch.delenv("RK_NO_CHAIN")
     r = dev(np.random.default_rng(2).uniform(-1, 1, nx * ny * nz))
+    monkeypatch.setenv("RK_CHAIN_CFG", cfg)              # read per launch
     a, b = fused.precond(r), plain.precond(r)
+    za, zb_ = fused.precond(r, zblocks=nz if nz % 8 else 8), plain.precond(r, zblocks=nz if nz % 8 else 8)
+    monkeypatch.delenv("RK_CHAIN_CFG")
     assert torch.equal(a, b)
+    assert torch.equal(za, zb_)
     fused.close()
     plain.close()
 
@@ -220,6 +225,34 @@ def test_block_jacobi_chain_bitwise_and_rejects_bad_blocks(rk, ctx, monkeypatch)
         plain.precond(r, zblocks=5)                                  # 5 does not divide 48
     fused.close()
     plain.close()
+
+
+# Multicolour SSOR(5)+1 preconditioner (reading R18).
+@pytest.mark.parametrize("name,mk", [
+    ("c1", lambda: convection_diffusion_c1(16)),
+    ("channel24", lambda: channel19(24)),                             # periodic x/z, 19-point
+    ("porous40", lambda: porous7(40, 4)),
+    ("random_33x18x21", lambda: _random7(33, 18, 21, 0, 23)),          # odd extents
+])
+def test_ssor_parity(rk, ctx, name, mk):
+    from oracle.stencil import SSOR
+    prob = mk()
+    op = make_op(rk, ctx, prob)
+    ref = Operator.from_problem(prob)
+    r = np.random.default_rng(4).uniform(-1, 1, prob.N)
+    z = op.precond(dev(r), kind=2, omega_l=1.0).cpu().numpy()
+    zr = SSOR(ref, 5, 1.0, 1.0)(r)
+    assert np.max(np.abs(z - zr)) <= 1e-12 * np.max(np.abs(zr))
+    op.close()
+
+
+def test_ssor_rejects_odd_periodic_extent(rk, ctx):
+    nx, ny, nz = 16, 8, 9
+    bands = dev(random_op_problem(nx, ny, nz, 4, OFFSETS7, 3))
+    op = rk.GridOperator(ctx, nx, ny, nz, OFFSETS7, bands, 4)
+    with pytest.raises(RuntimeError, match="even nz"):
+        op.precond(dev(np.ones(nx * ny * nz)), kind=2)
+    op.close()
 
 
 # ------------------------------------------------------------ solves
@@ -292,6 +325,20 @@ def test_sequence_parity(rk, ctx, name, solver):
     ora = run_sequence(w, solver=method)
     gpu, _ = gpu_sequence(rk, ctx, w, method)
     compare_sequences(w, gpu, ora, method)
+
+
+@pytest.mark.parametrize("name", ["c3s", "c2s", "c1"])
+def test_sequence_parity_ssor(rk, ctx, name):
+    """Whole sequences with the SSOR preconditioner (left for rGCROT, right
+    for rBiCGStab, D2)."""
+    from dataclasses import replace
+    from problems.workloads import Workload
+    w0 = get_workload(name)
+    w = Workload(w0.name, w0.make_problem, replace(w0.params, precond="ssor"), w0.n_systems,
+                 w0.epoch_every, w0.description)
+    ora = run_sequence(w)
+    gpu, _ = gpu_sequence(rk, ctx, w)
+    compare_sequences(w, gpu, ora, w.params.method)
 
 
 @pytest.mark.parametrize("name,zblocks", [("c3s", 4), ("c2s", 2), ("c4hs", 4)])
@@ -573,3 +620,44 @@ def test_full_size_sequence_vs_stored_oracle(rk, ctx, name):
         xsamp = x[gold["sample_idx"]]
         assert np.max(np.abs(xsamp - np.array(go["xsample"]))) <= 1e-6 * xn, t
     assert abs(tot_g - tot_o) <= 0.1 * tot_o, (tot_g, tot_o)
+
+
+def test_maximum_columns_rgcrot(rk, ctx):
+    """The largest block products librk accepts: k_max + m + 1 = 80 columns
+    (R9) -- bdot splits into two launches, bupd/lincomb use the 80-column
+    instantiations -- on the shrunken channel sequence, vs the oracle."""
+    from dataclasses import replace
+    from problems.workloads import Workload
+    w0 = get_workload("c2s")
+    prm = replace(w0.params, m=40, k_max=39, k_t=29, p1=1)
+    w = Workload(w0.name, w0.make_problem, prm, 4, w0.epoch_every, w0.description)
+    ora = run_sequence(w)
+    gpu, _ = gpu_sequence(rk, ctx, w)
+    compare_sequences(w, gpu, ora, prm.method)
+    assert max(r["k_after"] for r, _ in gpu) >= 2
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 1), (3, 1, 2), (5, 3, 1), (7, 5, 3)])
+def test_tiny_and_odd_grids(rk, ctx, shape):
+    """Degenerate grids (a single cell, single rows / planes, odd N: the
+    VEC = 1 paths) through SpMV, Jacobi, SSOR and a hybrid solve vs the
+    oracle and the dense direct solution."""
+    from oracle.stencil import SSOR, to_dense
+    nx, ny, nz = shape
+    prob = _random7(nx, ny, nz, 0, 31)
+    op = make_op(rk, ctx, prob)
+    ref = Operator.from_problem(prob)
+    x = np.random.default_rng(5).uniform(-1, 1, prob.N)
+    assert np.allclose(op.apply(dev(x)).cpu().numpy(), ref.apply(x), rtol=1e-13, atol=1e-13)
+    assert np.allclose(op.precond(dev(x)).cpu().numpy(), Jacobi(ref)(x), rtol=1e-12, atol=1e-13)
+    assert np.allclose(op.precond(dev(x), kind=2, omega_l=1.0).cpu().numpy(), SSOR(ref)(x),
+                       rtol=1e-12, atol=1e-13)
+    for method in ("rgcrot", "rbicgstab"):
+        cfg = rk.make_config(method=method, m=4, k_max=2, k_keep=1, select_count=1, tol=1e-10)
+        s = rk.Solver(op, cfg)
+        xs, rep = s.solve(dev(x))
+        assert rep["outcome"] == "CONVERGED"
+        xd = np.linalg.solve(to_dense(ref), x)
+        assert np.linalg.norm(xs.cpu().numpy() - xd) <= 1e-8 * np.linalg.norm(xd) * 10
+        s.close()
+    op.close()

@@ -301,3 +301,53 @@ def test_block_jacobi_matches_dense_sweeps():
     z = z + 1.0 * Dinv * (r - A @ z)
     assert np.allclose(jacobi(op, r, zblocks=2), z, rtol=0, atol=1e-13 * np.abs(z).max())
     assert np.array_equal(jacobi(op, r, zblocks=1), jacobi(op, r))
+
+
+# ------------------------------------------------------ SSOR (R18)
+def test_ssor_diagonal_closed_form():
+    """On a diagonal A one forward SOR pass with omega = 1 solves exactly:
+    z = D^-1 r, and neither the backward pass nor the global sweep moves it
+    (SPEC S:120-style closed form)."""
+    from oracle.stencil import ssor
+    rng = np.random.default_rng(1)
+    nx = ny = nz = 4
+    bands = np.zeros((7, nz, ny, nx))
+    bands[0] = rng.uniform(1, 3, (nz, ny, nx))
+    op = Operator(nx, ny, nz, 0, OFFSETS7, bands)
+    r = rng.uniform(-1, 1, op.N)
+    assert np.allclose(ssor(op, r, sweeps=1, omega=1.0), r / op.diag(), rtol=0, atol=1e-15)
+
+
+@pytest.mark.parametrize("mk", [lambda: channel19(8), lambda: porous7(8, 2),
+                                lambda: convection_diffusion_c1(8)])
+def test_ssor_matches_block_triangular_formula(mk):
+    """Multicolour SSOR written as matrices: with the colour order of
+    colour_of, L / U = the couplings to earlier / later colours of the dense
+    expansion, one symmetric sweep is z <- z + (D/w + L)^-1 (r - A z), then
+    z <- z + (D/w + U)^-1 (r - A z) (triangular solves, an independent code
+    path from the colour loop), and the global sweep z += w_g D^-1 (r - A z)."""
+    import scipy.linalg as sla
+    from oracle.stencil import colour_of, ssor
+    prob = mk()
+    op = Operator.from_problem(prob)
+    A = to_dense(op)
+    col = colour_of(op)
+    perm = np.argsort(col, kind="stable")
+    Ap = A[np.ix_(perm, perm)]
+    cp = col[perm]
+    D = np.diag(np.diag(Ap))
+    L = np.where(cp[:, None] > cp[None, :], Ap, 0.0)
+    U = np.where(cp[:, None] < cp[None, :], Ap, 0.0)
+    assert np.count_nonzero(np.where(cp[:, None] == cp[None, :], Ap, 0.0) - D) == 0   # colours decouple
+    w = 1.1
+    r = np.random.default_rng(3).uniform(-1, 1, op.N)
+    rp = r[perm]
+    z = np.zeros(op.N)
+    for _ in range(3):
+        z = z + sla.solve_triangular(D / w + L, rp - Ap @ z, lower=True)
+        z = z + sla.solve_triangular(D / w + U, rp - Ap @ z, lower=False)
+    z = z + (rp - Ap @ z) / np.diag(Ap)
+    out = np.empty(op.N)
+    out[perm] = z
+    ref = ssor(op, r, sweeps=3, omega=w)
+    assert np.allclose(ref, out, rtol=0, atol=1e-12 * np.abs(out).max())

@@ -11,6 +11,8 @@ run that NCCL code here; these tests run the SAME protocol with gloo over
 world_size 2 and 3 and check, against the single-domain oracle:
   * halo exchange + local stencil == global SpMV (periodic and Dirichlet z),
   * the Jacobi(5+1) preconditioner with a halo per sweep == global M^-1,
+  * block Jacobi with one z-block per rank and NO halo in the local sweeps
+    == the oracle's global block-Jacobi M^-1 (reading R17),
   * one GMRES cycle with all-reduced (batched, CGS2) dots == the global one,
   * the reduced scalars are bit-identical on every rank.
 """
@@ -100,6 +102,25 @@ class Slab:
             z = z + wl * (r - self.spmv(z)) / D
         return z + wg * (r - self.spmv(z)) / D
 
+    def spmv_local(self, v):
+        """Local stencil with zero ghost planes and NO exchange: the operator
+        of the block-Jacobi local sweeps when every rank owns one z-block
+        (reading R17; librk skips the halo for such sweeps)."""
+        xp = self.pad(v)
+        y = np.zeros((self.nzl, self.prob.ny, self.prob.nx))
+        mask_xy = self.prob.periodic & 3
+        for d, (dx, dy, dz) in enumerate(self.offsets):
+            xs = shifted(xp, int(dx), int(dy), 0, mask_xy)[1 + dz:1 + dz + self.nzl]
+            y += self.bands[d] * xs
+        return y.reshape(-1)
+
+    def block_jacobi(self, r, sweeps=5, wl=0.8, wg=1.0):
+        D = self.bands[0].reshape(-1)
+        z = wl * r / D
+        for _ in range(sweeps - 1):
+            z = z + wl * (r - self.spmv_local(z)) / D
+        return z + wg * (r - self.spmv(z)) / D
+
     def allreduce(self, vals):
         t = torch.tensor(np.asarray(vals, dtype=np.float64))
         dist.all_reduce(t)
@@ -140,6 +161,7 @@ def _worker(rank, world, port, case, q):
         xl = xg[sl.z0 * P:sl.z1 * P]
         y = sl.spmv(xl)
         z = sl.jacobi(xl)
+        zbj = sl.block_jacobi(xl)
         b = prob.rhs(1, sl.z0, sl.z1).reshape(-1)
         xc, H = dist_gmres_cycle(sl, b, 6)
         # replicated state must be bit-identical across ranks
@@ -147,7 +169,7 @@ def _worker(rank, world, port, case, q):
         Hs = [torch.zeros_like(Ht) for _ in range(world)]
         dist.all_gather(Hs, Ht)
         same = all(torch.equal(Hs[0], h) for h in Hs)
-        q.put((rank, sl.z0, sl.z1, y, z, xc, same))
+        q.put((rank, sl.z0, sl.z1, y, z, zbj, xc, same))
     finally:
         dist.destroy_process_group()
 
@@ -173,10 +195,13 @@ def test_slab_decomposition_matches_global(case, world):
     zg = pc(xg)
     b = prob.rhs(1).reshape(-1)
     xc_g, _ = gmres(op, pc, b, SolverParams(m=6, k_max=0, p1=0, tol=1e-30, max_mv=6))
+    zbj_g = Jacobi(op, zblocks=world)(xg) if prob.nz % world == 0 else None
     P = prob.nx * prob.ny
-    for rank, z0, z1, y, z, xc, same in res:
+    for rank, z0, z1, y, z, zbj, xc, same in res:
         sl = slice(z0 * P, z1 * P)
         assert np.allclose(y, yg[sl], rtol=0, atol=1e-12 * np.abs(yg).max())
         assert np.allclose(z, zg[sl], rtol=0, atol=1e-12 * np.abs(zg).max())
+        if zbj_g is not None:     # halo-free local sweeps == global block Jacobi (R17)
+            assert np.allclose(zbj, zbj_g[sl], rtol=0, atol=1e-12 * np.abs(zbj_g).max())
         assert np.allclose(xc, xc_g[sl], rtol=0, atol=1e-10 * np.abs(xc_g).max())
         assert same, "replicated Hessenberg differs across ranks"
