@@ -94,12 +94,16 @@ __global__ void __launch_bounds__(256) bupd_kernel(ColPtrs Q, int ncol, const do
 // ahead of the FMAs (a remainder branch let the compiler sink them).
 constexpr int TRV = 2, TG = 4, TILE_ROWS = 512 * TRV;
 
-constexpr int DRV = 4, DG = 2, DTILE_ROWS = 512 * DRV;
+#ifndef RK_BDOT_RV
+#define RK_BDOT_RV 4
+#define RK_BDOT_G 2
+#endif
+constexpr int DRV = RK_BDOT_RV, DG = RK_BDOT_G;
 
-template <int NC>
-__global__ void __launch_bounds__(256) bdot_tile_kernel(ColPtrs Q, int ncol, const double* __restrict__ w,
+template <int NC, int BT>
+__global__ void __launch_bounds__(BT) bdot_tile_kernel(ColPtrs Q, int ncol, const double* __restrict__ w,
                                                         int64_t N, RedArgs ra) {
-  constexpr int RV = DRV, G = DG, TILE_ROWS = DTILE_ROWS;
+  constexpr int RV = DRV, G = DG, TILE_ROWS = 2 * BT * DRV;
   double acc[NC];
 #pragma unroll
   for (int c = 0; c < NC; ++c) acc[c] = 0.0;
@@ -109,7 +113,7 @@ __global__ void __launch_bounds__(256) bdot_tile_kernel(ColPtrs Q, int ncol, con
     const int64_t r0 = t * TILE_ROWS + 2 * threadIdx.x;
     double2 wv[RV];
 #pragma unroll
-    for (int v = 0; v < RV; ++v) wv[v] = __ldg(reinterpret_cast<const double2*>(w + r0 + 512 * v));
+    for (int v = 0; v < RV; ++v) wv[v] = __ldg(reinterpret_cast<const double2*>(w + r0 + 2 * BT * v));
 #pragma unroll
     for (int c = 0; c < NC; c += G) {
       if (c < ncol) {
@@ -118,7 +122,7 @@ __global__ void __launch_bounds__(256) bdot_tile_kernel(ColPtrs Q, int ncol, con
         for (int u = 0; u < G; ++u)
 #pragma unroll
           for (int v = 0; v < RV; ++v) {
-            const Vec<2> a = ldv_stream<2>(Q.p[c + u] + r0 + 512 * v);
+            const Vec<2> a = ldv_stream<2>(Q.p[c + u] + r0 + 2 * BT * v);
             q[u][v] = make_double2(a.v[0], a.v[1]);
           }
 #pragma unroll
@@ -401,7 +405,8 @@ void bdot(rk_ctx* ctx, const std::vector<const double*>& cols_all, const double*
     const int64_t work = N / vec;
     Launch L(ctx, "bdot", 8.0 * N * (ncol + 1));
 #define RK_BDOT(NCV)                                                                          \
-  if (vec == 2) launch_k(ctx, bdot_tile_kernel<NCV>, work / DRV, dim3(256), Q, ncol, w, N, ra); \
+  if (vec == 2)                                                                                     \
+    launch_k(ctx, bdot_tile_kernel<NCV, 256>, work / DRV, dim3(256), Q, ncol, w, N, ra);            \
   else launch_k(ctx, bdot_kernel<NCV, 1>, work, dim3(256), Q, ncol, w, N, ra);
     switch (nc) {
       case 8: RK_BDOT(8); break;

@@ -133,6 +133,9 @@ __device__ __forceinline__ void block_reduce_store(const double (&v)[NV], int nv
     for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
     if (lane == 0) ra.partials[(int64_t)q * G + blockIdx.x] = s;
   }
+#ifdef RK_EXP_NO_FINAL   // experiment only: per-CTA partials, no cross-CTA finalisation
+  return;
+#endif
   __threadfence();
   __syncthreads();
   if (tid == 0) last = (atomicAdd(ra.counter, 1u) == (unsigned)(G - 1));
