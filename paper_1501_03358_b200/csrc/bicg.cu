@@ -13,6 +13,7 @@ __global__ void __launch_bounds__(256) bicg_p_kernel(const double* __restrict__ 
                                                      const double* __restrict__ v, const double* __restrict__ D,
                                                      double* __restrict__ z, double wl, int64_t N,
                                                      const BiIter* cur, const BiIter* prev, int first) {
+  RK_PDL_ENTRY();
   double beta = 0.0, omega = 0.0;
   if (!first) {
     const double alpha = prev->rho / prev->sigma;
@@ -51,6 +52,7 @@ __global__ void __launch_bounds__(256) bicg_s_kernel(const double* __restrict__ 
                                                      double* __restrict__ s, const double* __restrict__ D,
                                                      double* __restrict__ z, double wl, int64_t N,
                                                      const BiIter* cur, RedArgs ra) {
+  RK_PDL_ENTRY();
   const double alpha = cur->rho / cur->sigma;
   double acc[1] = {0.0};
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -88,6 +90,7 @@ __global__ void __launch_bounds__(256) bicg_xr_kernel(double* __restrict__ x, do
                                                       const double* __restrict__ rt, int64_t N, BiIter* cur,
                                                       double* xi, const double* eta1, const double* eta2,
                                                       int k, RedArgs ra) {
+  RK_PDL_ENTRY();
   const double alpha = cur->rho / cur->sigma;
   const double omega = cur->ts / cur->tt;
   int mode;  // 0 full update, 1 exact exit, 2 breakdown (no update)
@@ -142,6 +145,7 @@ __global__ void __launch_bounds__(256) bicg_xr_kernel(double* __restrict__ x, do
 
 // Alg. 4 line 1c bookkeeping: xi = -eta0 ; rho_0 = ||r_0||^2 (r~ = r_0).
 __global__ void bicg_setup_kernel(double* xi, const double* eta0, int k, BiIter* it0) {
+  RK_PDL_ENTRY();
   for (int c = threadIdx.x; c < k; c += blockDim.x) xi[c] = -eta0[c];
   if (threadIdx.x == 0) it0->rr = it0->rho;
 }
@@ -196,7 +200,7 @@ void bicg_xr(rk_ctx* ctx, double* x, double* r, const double* s, const double* t
 
 void bicg_setup(rk_ctx* ctx, double* xi, const double* eta0, int k, BiIter* it0) {
   Launch L(ctx, "bicg_setup", 0);
-  bicg_setup_kernel<<<1, 128, 0, ctx->stream>>>(xi, eta0, k, it0);
+  launch_pdl(ctx, bicg_setup_kernel, dim3(1), dim3(128), 0, xi, eta0, k, it0);
   L.done();
 }
 

@@ -11,6 +11,7 @@ namespace rk {
 template <int NC, int VEC>
 __global__ void __launch_bounds__(256) bdot_kernel(ColPtrs Q, int ncol, const double* __restrict__ w,
                                                    int64_t N, RedArgs ra) {
+  RK_PDL_ENTRY();
   double acc[NC];
 #pragma unroll
   for (int c = 0; c < NC; ++c) acc[c] = 0.0;
@@ -43,6 +44,7 @@ __global__ void __launch_bounds__(256) bupd_kernel(ColPtrs Q, int ncol, const do
                                                    double gs, double* __restrict__ w, int64_t N,
                                                    const double* d0, const double* d1,
                                                    const double* d2, RedArgs ra) {
+  RK_PDL_ENTRY();
   __shared__ double gsh[NC];
   for (int c = threadIdx.x; c < NC; c += blockDim.x) gsh[c] = c < ncol ? gs * g[c] : 0.0;
   __syncthreads();
@@ -103,6 +105,7 @@ constexpr int DRV = RK_BDOT_RV, DG = RK_BDOT_G;
 template <int NC, int BT>
 __global__ void __launch_bounds__(BT) bdot_tile_kernel(ColPtrs Q, int ncol, const double* __restrict__ w,
                                                         int64_t N, RedArgs ra) {
+  RK_PDL_ENTRY();
   constexpr int RV = DRV, G = DG, TILE_ROWS = 2 * BT * DRV;
   double acc[NC];
 #pragma unroll
@@ -155,6 +158,7 @@ __global__ void __launch_bounds__(256) bupd_tile_kernel(ColPtrs Q, int ncol, con
                                                         double gs, double* __restrict__ w, int64_t N,
                                                         const double* d0, const double* d1,
                                                         const double* d2, RedArgs ra) {
+  RK_PDL_ENTRY();
   constexpr int RV = TRV, G = TG;
   __shared__ double gsh[NC];
   for (int c = threadIdx.x; c < NC; c += blockDim.x) gsh[c] = c < ncol ? gs * g[c] : 0.0;
@@ -237,6 +241,7 @@ template <int VEC>
 __global__ void __launch_bounds__(256) normalize_kernel(double* __restrict__ w, int64_t N,
                                                         const double* nrm2, const double* nin2,
                                                         double* flag) {
+  RK_PDL_ENTRY();
   const double h = sqrt(*nrm2);
   bool brk = false;
   if (nin2) brk = !(h > 1e-14 * sqrt(*nin2));
@@ -256,6 +261,7 @@ __global__ void __launch_bounds__(256) normalize_kernel(double* __restrict__ w, 
 template <int NC, int VEC>
 __global__ void __launch_bounds__(256) lincomb_kernel(ColPtrs Q, int ncol, const double* __restrict__ coef,
                                                       int nout, LcOut lo, int64_t N) {
+  RK_PDL_ENTRY();
   __shared__ double cs[MAXOUT][NC];
   for (int t = threadIdx.x; t < MAXOUT * NC; t += blockDim.x) {
     const int o = t / NC, c = t % NC;
@@ -311,6 +317,7 @@ template <int NC, int VEC>
 __global__ void __launch_bounds__(256) proj_kernel(ColPtrs C, ColPtrs U, int k, const double* __restrict__ xi,
                                                    double* __restrict__ r, double* __restrict__ x,
                                                    int64_t N, RedArgs ra) {
+  RK_PDL_ENTRY();
   __shared__ double xs[NC];
   for (int c = threadIdx.x; c < NC; c += blockDim.x) xs[c] = c < k ? xi[c] : 0.0;
   __syncthreads();
@@ -365,6 +372,7 @@ __global__ void __launch_bounds__(256) proj_kernel(ColPtrs C, ColPtrs U, int k, 
 template <int NC>
 __global__ void __launch_bounds__(256) rotate_kernel(ColPtrs Qc, int k, int kout, const double* __restrict__ T,
                                                      int64_t N) {
+  RK_PDL_ENTRY();
   __shared__ double ts[NC * NC];
   for (int t = threadIdx.x; t < k * kout; t += blockDim.x) ts[t] = T[t];
   __syncthreads();

@@ -249,6 +249,7 @@ template <int ST, int NST, int TX, int TY, int PD, int K0, int K1, int K2>
 __global__ void __launch_bounds__((TX + 2 * (NST - 1)) * (TY + 2 * (NST - 1)), 1)
 chain_kernel(const __grid_constant__ CUtensorMap map_b, const __grid_constant__ CUtensorMap map_r,
              const __grid_constant__ CUtensorMap map_x, ChainParams cp) {
+  RK_PDL_ENTRY();
   using G = ChainGeom<ST, NST, TX, TY, PD>;
   constexpr int HALO = G::HALO, EX = G::EX, XX = G::XX, NXB = G::NXB, NB = G::NB;
   constexpr int SX = G::SX, PADB = G::PADB, PADX = G::PADX;
@@ -454,7 +455,7 @@ void launch_one(rk_op* op, ChainParams cp, dim3 grid) {
     encode(&mx, cp.xin - op->P, 3, dims, str, box);
   }
   dim3 blk(X2 ? G::EX / 2 : G::EX, G::EY);
-  kern<<<grid, blk, G::SMEM, op->ctx->stream>>>(mb, mr, mx, cp);
+  launch_pdl(op->ctx, kern, grid, blk, G::SMEM, mb, mr, mx, cp);
 }
 
 template <int NST, int TX, int TY, int PD, int X2 = 0>

@@ -190,7 +190,7 @@ void launch_k(rk_ctx* ctx, void (*kern)(KArgs...), int64_t work_threads, dim3 bl
   }
   const int64_t want = std::max<int64_t>(1, (work_threads + threads - 1) / threads);
   const int grid = (int)std::min<int64_t>(want, (int64_t)ctx->sms * occ);
-  kern<<<grid, blk, 0, ctx->stream>>>(std::forward<Args>(args)...);
+  launch_pdl(ctx, kern, dim3(grid), blk, 0, std::forward<Args>(args)...);
 }
 
 inline RedArgs red_args(rk_ctx* ctx, double* out) {

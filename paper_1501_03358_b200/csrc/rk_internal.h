@@ -130,6 +130,7 @@ struct ProfAgg {
 struct rk_ctx {
   int device = 0, rank = 0, nranks = 1, sms = 148;
   int64_t l2_bytes = 0;         // L2 capacity (chain policy)
+  bool pdl = true;              // programmatic dependent launch (env RK_NO_PDL: off)
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   double* partials = nullptr;
@@ -207,6 +208,34 @@ struct Launch {
     if (on) RK_CUDA(cudaEventRecord(ctx->pending[idx].b, ctx->stream));
   }
 };
+
+// Every librk kernel is launched with programmatic stream serialization
+// (PDL): the next kernel's CTAs may become resident while this kernel's last
+// CTAs still run; each kernel begins with RK_PDL_ENTRY (griddepcontrol.wait:
+// the predecessor grid has completed and its memory is visible; then
+// launch_dependents), so the overlap hides launch latency and tails without
+// changing any result.
+#define RK_PDL_ENTRY()                                         \
+  do {                                                         \
+    asm volatile("griddepcontrol.wait;" ::: "memory");          \
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); \
+  } while (0)
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(rk_ctx* ctx, void (*kern)(KArgs...), dim3 grid, dim3 blk, size_t smem,
+                Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = blk;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = ctx->pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  RK_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
 
 // fused chain (chain.cu): max stages per launch for this operator (0 = unavailable)
 int chain_max_stages(const rk_op* op);

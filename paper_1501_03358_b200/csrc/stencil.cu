@@ -1,6 +1,8 @@
 // sm_100a stencil kernels of librk (SURVEY.md §2.4 K1 SpMV, K2 Jacobi
 // sweeps), one stage per launch; the temporally blocked chain is chain.cu.
 // HBM-bound fp64 work on the CUDA cores (0.1-0.3 flop/B).
+#include <cstdlib>
+
 #include "kcommon.cuh"
 
 namespace rk {
@@ -14,6 +16,7 @@ namespace rk {
 // neighbouring rank), or wrap for a single-rank periodic z.
 template <int ST, int MODE, int VEC>
 __global__ void __launch_bounds__(256) stencil_kernel(StencilParams sp) {
+  RK_PDL_ENTRY();
   constexpr bool RED = (MODE == SM_SWEEP_NORM || MODE == SM_RESID || MODE == SM_RESID_SWEEP1);
   const int BX = blockDim.x, BY = blockDim.y;
   const int tx = threadIdx.x, ty = threadIdx.y;
@@ -170,6 +173,7 @@ __global__ void __launch_bounds__(256) stencil_kernel(StencilParams sp) {
 template <int ST>
 __global__ void validate_kernel(const double* bands, int64_t N, int nx, int ny, int z0,
                                 int nz_global, int pmask, unsigned* bad) {
+  RK_PDL_ENTRY();
   for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < N;
        n += (int64_t)gridDim.x * blockDim.x) {
     const int i = (int)(n % nx);
@@ -248,6 +252,7 @@ void init_ctx_kernels(rk_ctx* ctx) {
   int l2 = 0;
   RK_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, ctx->device));
   ctx->l2_bytes = l2;
+  ctx->pdl = std::getenv("RK_NO_PDL") == nullptr;
   // per-CTA partials for up to MAXCOL + 4 values, up to 8 resident 256-thread CTAs per SM
   ctx->partials_cap = (size_t)(MAXCOL + 4) * sms * 8;
   RK_CUDA(cudaMalloc(&ctx->partials, ctx->partials_cap * sizeof(double)));
@@ -307,6 +312,7 @@ void stencil(rk_op* op, int mode, const double* x, const double* r, double* out0
 // wrapped, z neighbours from the ghost planes or wrapped (single rank).
 template <int ST>
 __global__ void __launch_bounds__(256) colour_sweep_kernel(StencilParams sp, int colour) {
+  RK_PDL_ENTRY();
   const int ci = colour & 1, cj = (colour >> 1) & 1, ck = (colour >> 2) & 1;
   const int hx = (sp.nx - ci + 1) / 2;                 // cells of parity ci in a row
   const int hy = (sp.ny - cj + 1) / 2;
@@ -371,6 +377,7 @@ void colour_sweep(rk_op* op, double* z, const double* r, double omega, int colou
 }
 
 __global__ void invdiag_kernel(const double* __restrict__ D, double* __restrict__ inv, int64_t N) {
+  RK_PDL_ENTRY();
   for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < N; n += (int64_t)gridDim.x * blockDim.x)
     inv[n] = 1.0 / D[n];
 }
