@@ -32,6 +32,9 @@
 
 #include "rk_internal.h"
 
+#ifndef RK_CHAIN_COMPUTEONLY
+#define RK_CHAIN_COMPUTEONLY 0  // experiments: 1 = no TMA after the prologue (stale data)
+#endif
 #ifndef RK_CHAIN_LOADONLY
 #define RK_CHAIN_LOADONLY 0   // experiments: 1 = TMA traffic only, no stage arithmetic
 #endif
@@ -328,8 +331,8 @@ chain_kernel(const __grid_constant__ CUtensorMap map_b, const __grid_constant__ 
 #define RK_CHAIN_STEP(PHV)                                                                         \
   {                                                                                                \
     if (tau >= tau_end) break;                                                                     \
-    if (tid == 0 && tau + PD <= qlast) issue(tau + PD, xsi, bsi);                                  \
-    if (tau + 1 <= qlast) mbar_wait(&bars[xsp], parp);                                             \
+    if (!RK_CHAIN_COMPUTEONLY && tid == 0 && tau + PD <= qlast) issue(tau + PD, xsi, bsi);         \
+    if (!RK_CHAIN_COMPUTEONLY && tau + 1 <= qlast) mbar_wait(&bars[xsp], parp);                    \
     using SP = ChainStep<ST, NST, TX, TY, PD, K0, K1, K2, PHV>;                                    \
     if (RK_CHAIN_LOADONLY) {                                                                       \
       __syncthreads();                                                                             \
