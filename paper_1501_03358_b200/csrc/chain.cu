@@ -32,6 +32,12 @@
 
 #include "rk_internal.h"
 
+// 1/D: recomputed from the diagonal band (1.0 / D is correctly rounded, so
+// the bits equal librk's precomputed 1/D band used by the unfused kernels);
+// RK_CHAIN_TMA_INVD = 1 streams that band instead (one more array per plane).
+#ifndef RK_CHAIN_TMA_INVD
+#define RK_CHAIN_TMA_INVD 1
+#endif
 #ifndef RK_CHAIN_COMPUTEONLY
 #define RK_CHAIN_COMPUTEONLY 0  // experiments: 1 = no TMA after the prologue (stale data)
 #endif
@@ -71,7 +77,8 @@ struct ChainGeom {
   static constexpr int PADX = (HALO + 1) % 2;                         // input box starts at gx0 - 1 - PADX
   static constexpr int XX = (EX + 2 + PADX + 1) / 2 * 2, XY = EY + 2; // input tile (+1 halo)
   static constexpr int NB = PD + 1, NXB = PD + 2;
-  static constexpr int B_BYTES = (ST + 1) * EY * SX * 8;           // bands + 1/D
+  static constexpr int NBAND = ST + (RK_CHAIN_TMA_INVD ? 1 : 0);     // bands (+ 1/D)
+  static constexpr int B_BYTES = NBAND * EY * SX * 8;
   static constexpr int R_BYTES = EY * SX * 8;
   static constexpr int X_BYTES = XY * XX * 8;
   __host__ __device__ static constexpr int al(int b) { return (b + 127) / 128 * 128; }
@@ -164,7 +171,8 @@ struct ChainStep {
 #pragma unroll
     for (int d = 0; d < ST; ++d) bnd[PH][d] = bs[d * EY * SX];
     if (LOAD_R) rr[PH] = reinterpret_cast<const double*>(sb + G::R_OFF)[boff];
-    inv[PH] = bs[ST * EY * SX];   // 1/D (0 outside the grid: TMA zero fill)
+    if (RK_CHAIN_TMA_INVD) inv[PH] = bs[ST * EY * SX];   // 1/D (0 outside the grid: zero fill)
+    else inv[PH] = bnd[PH][0] != 0.0 ? 1.0 / bnd[PH][0] : 0.0;
     // block-Jacobi local sweep (R17): no coupling across z-block boundaries
     bool cut_m = false, cut_p = false;
     if (cp.zb > 0 && cp.local[0]) {
@@ -440,9 +448,9 @@ void launch_one(rk_op* op, ChainParams cp, dim3 grid) {
   const cuuint64_t nx = op->g.nx, ny = op->g.ny, nz = op->g.nz_local;
   CUtensorMap mb, mr, mx;
   {
-    cuuint64_t dims[4] = {nx, ny, nz, (cuuint64_t)ST + 1};          // bands, then 1/D
+    cuuint64_t dims[4] = {nx, ny, nz, (cuuint64_t)G::NBAND};       // bands (then 1/D)
     cuuint64_t str[3] = {nx * 8, nx * ny * 8, (cuuint64_t)op->N * 8};
-    cuuint32_t box[4] = {(cuuint32_t)G::SX, (cuuint32_t)G::EY, 1, (cuuint32_t)ST + 1};
+    cuuint32_t box[4] = {(cuuint32_t)G::SX, (cuuint32_t)G::EY, 1, (cuuint32_t)G::NBAND};
     encode(&mb, cp.bands, 4, dims, str, box);
   }
   {
@@ -495,7 +503,7 @@ struct TileCfg {
 };
 constexpr TileCfg CFGS[] = {{32, 16, 2}, {32, 8, 2}, {16, 8, 2}, {16, 8, 3}, {16, 16, 2}, {32, 16, 2}};
 constexpr int NCFG = sizeof(CFGS) / sizeof(CFGS[0]);
-constexpr int DEFAULT_CFG = 0;
+constexpr int DEFAULT_CFG = 5;   // x-pairs with register z-columns (chain_x2.cuh)
 
 int cfg_index() {
   const char* e = std::getenv("RK_CHAIN_CFG");

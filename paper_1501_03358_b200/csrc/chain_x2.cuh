@@ -2,10 +2,12 @@
 //
 // Same schedule, shared-memory rings, TMA feed and per-cell arithmetic as
 // chain_kernel (so the results are bit-identical), but every thread owns an
-// x-pair of cells (2c, 2c+1) of its row: bands, 1/D, rhs, centre and the
-// y / z neighbours of the pair come in 16-byte shared loads, the pair's x
-// neighbours are each other's centres plus two 8-byte loads, and the ring /
-// global stores are 16 bytes.  Per cell this halves the load and integer
+// x-pair of cells (2c, 2c+1) of its row: bands, 1/D, rhs and the y
+// neighbours of the pair come in 16-byte shared loads, the pair's x
+// neighbours are each other's centres plus two 8-byte loads, the ring /
+// global stores are 16 bytes, and the pair's own z-column (input at planes
+// tau-1, tau; each stage's output at the two previous planes) stays in
+// registers, so shared memory only serves the in-plane neighbours.  Per cell this halves the load and integer
 // instructions of the one-cell kernel (whose step was issue-latency bound,
 // DESIGN.md §7) at half the thread count.  Requires an even halo (NST = 3)
 // so that every pair is either interior or halo; x tile offsets are even,
@@ -49,9 +51,11 @@ struct ChainStepX2 {
     return make_double2(a0 + b0, a1 + b1);
   }
 
+  // xc / xm: this thread's input pair at planes tau and tau-1 (registers,
+  // z-column reuse); the pair at tau+1 is read from the tile and becomes xc
   static __device__ __forceinline__ double2 stage0(bool st_ok, int pl_tau, const unsigned char* sb,
-                                                   const double* xm, const double* x0,
-                                                   const double* xp, double* ring,
+                                                   const double* x0, const double* xp,
+                                                   double2& xc, double2& xm, double* ring,
                                                    double2 (&bnd)[3][ST], double2 (&rr)[3],
                                                    double2 (&inv)[3], int64_t cxy, int boff,
                                                    int roff, const ChainParams& cp) {
@@ -59,7 +63,12 @@ struct ChainStepX2 {
     const double* bs = reinterpret_cast<const double*>(sb) + boff;
 #pragma unroll
     for (int d = 0; d < ST; ++d) bnd[PH][d] = ld2(bs + d * EY * SX);
-    inv[PH] = ld2(bs + ST * EY * SX);   // 1/D (0 outside the grid: TMA zero fill)
+    if (RK_CHAIN_TMA_INVD) {
+      inv[PH] = ld2(bs + ST * EY * SX);   // 1/D (0 outside the grid: TMA zero fill)
+    } else {
+      inv[PH].x = bnd[PH][0].x != 0.0 ? 1.0 / bnd[PH][0].x : 0.0;
+      inv[PH].y = bnd[PH][0].y != 0.0 ? 1.0 / bnd[PH][0].y : 0.0;
+    }
     if (LOAD_R) rr[PH] = ld2(reinterpret_cast<const double*>(sb + G::R_OFF) + boff);
     bool cut_m = false, cut_p = false;   // block-Jacobi local sweep (R17)
     if (cp.zb > 0 && cp.local[0]) {
@@ -67,11 +76,14 @@ struct ChainStepX2 {
       cut_m = (g % cp.zb) == 0;
       cut_p = ((g + 1) % cp.zb) == 0;
     }
-    const double2 c = ld2(x0);
+    const double2 c = xc;
     const double l = x0[-1], r = x0[2];
     const double2 ym = ld2(x0 - XX), yp = ld2(x0 + XX);
-    const double2 zm = cut_m ? make_double2(0.0, 0.0) : ld2(xm);
-    const double2 zp = cut_p ? make_double2(0.0, 0.0) : ld2(xp);
+    const double2 xnext = ld2(xp);
+    const double2 zm = cut_m ? make_double2(0.0, 0.0) : xm;
+    const double2 zp = cut_p ? make_double2(0.0, 0.0) : xnext;
+    xm = xc;
+    xc = xnext;
     const double2 y = apply7(bnd[PH], c, l, r, ym, yp, zm, zp);
     double2 val;
     if (K0 == CK_SPMV1) {
@@ -93,16 +105,18 @@ struct ChainStepX2 {
     return val;
   }
 
+  // hc / hm: stage S-1's outputs for this thread at planes q and q-1
+  // (registers, written in the two previous steps); up: at plane q+1 (this step)
   template <int S>
   static __device__ __forceinline__ double2 stage(bool st_ok, int pl_q, double* ring,
                                                   double2 (&bnd)[3][ST], double2 (&rr)[3],
                                                   double2 (&inv)[3], int64_t cxy, int roff,
-                                                  double2 up, const ChainParams& cp) {
+                                                  double2 hc, double2 hm, double2 up,
+                                                  const ChainParams& cp) {
     static_assert(ST == 7, "single-barrier chain steps need a 7-point stencil");
     constexpr int KIND[3] = {K0, K1, K2};
     constexpr int R = (PH - S + 3) % 3;
     const double* rb = ring + (S - 1) * 3 * RPL + roff;
-    const double* rm = rb + ((R + 2) % 3) * RPL;
     const double* r0 = rb + R * RPL;
     bool cut_m = false, cut_p = false;   // block-Jacobi local sweep (R17)
     if (cp.zb > 0 && cp.local[S]) {
@@ -110,10 +124,10 @@ struct ChainStepX2 {
       cut_m = (g % cp.zb) == 0;
       cut_p = ((g + 1) % cp.zb) == 0;
     }
-    const double2 c = ld2(r0);
+    const double2 c = hc;
     const double l = r0[-1], r = r0[2];
     const double2 ym = ld2(r0 - EX), yp = ld2(r0 + EX);
-    const double2 zm = cut_m ? make_double2(0.0, 0.0) : ld2(rm);
+    const double2 zm = cut_m ? make_double2(0.0, 0.0) : hm;
     const double2 zp = cut_p ? make_double2(0.0, 0.0) : up;
     const double2 y = apply7(bnd[R], c, l, r, ym, yp, zm, zp);
     const double2 val = (KIND[S] == CK_SWEEP)
@@ -201,30 +215,51 @@ chain_kernel_x2(const __grid_constant__ CUtensorMap map_b, const __grid_constant
 #pragma unroll
     for (int d = 0; d < ST; ++d) bnd[s][d] = make_double2(0.0, 0.0);
   }
+  // z-column registers: input pair at planes tau, tau-1 (tiles of slots 1, 0
+  // at tau0) and the stage outputs of the two previous steps
+  double2 xc = *reinterpret_cast<const double2*>(xtile(1)), xm = *reinterpret_cast<const double2*>(xtile(0));
+  const double2 zero2 = make_double2(0.0, 0.0);
+  double2 h1c = zero2, h1m = zero2, h2c = zero2, h2m = zero2;
   const int tau_end = z1 + HALO;
 #define RK_CHAIN2_STEP(PHV)                                                                        \
   {                                                                                                \
     if (tau >= tau_end) break;                                                                     \
-    if (tid == 0 && tau + PD <= qlast) issue(tau + PD, xsi, bsi);                                  \
-    if (tau + 1 <= qlast) mbar_wait(&bars[xsp], parp);                                             \
+    if (!RK_CHAIN_COMPUTEONLY && tid == 0 && tau + PD <= qlast) issue(tau + PD, xsi, bsi);         \
+    if (!RK_CHAIN_COMPUTEONLY && tau + 1 <= qlast) mbar_wait(&bars[xsp], parp);                    \
     using SP = ChainStepX2<ST, NST, TX, TY, PD, K0, K1, K2, PHV>;                                  \
+    if (RK_CHAIN_LOADONLY) {                                                                       \
+      __syncthreads();                                                                             \
+      xsm = xs0;                                                                                   \
+      xs0 = xsp;                                                                                   \
+      adv(xsp, NXB);                                                                               \
+      if (xsp == 0) parp ^= 1u;                                                                    \
+      adv(bs0, NB);                                                                                \
+      adv(xsi, NXB);                                                                               \
+      adv(bsi, NB);                                                                                \
+      ++tau;                                                                                       \
+      continue;                                                                                    \
+    }                                                                                              \
     const double2 v0 = SP::stage0(interior && tau >= z0 && tau < z1 && (pz || tau < nz),          \
-                                  pl_of(tau), smem + bs0 * G::BSLOT, xtile(xsm), xtile(xs0),       \
-                                  xtile(xsp), ring, bnd, rr, inv, cxy, boff, roff, cp);            \
+                                  pl_of(tau), smem + bs0 * G::BSLOT, xtile(xs0), xtile(xsp), xc,   \
+                                  xm, ring, bnd, rr, inv, cxy, boff, roff, cp);                    \
     if constexpr (NST >= 2) {                                                                      \
-      double2 v1 = make_double2(0.0, 0.0);                                                         \
+      double2 v1 = zero2;                                                                          \
       if (tau >= tau0 + 2) {                                                                       \
         const int q = tau - 1;                                                                     \
         v1 = SP::template stage<1>(interior && q >= z0 && q < z1, pl_of(q), ring, bnd, rr, inv,    \
-                                   cxy, roff, v0, cp);                                             \
+                                   cxy, roff, h1c, h1m, v0, cp);                                   \
       }                                                                                            \
       if constexpr (NST >= 3) {                                                                    \
         if (tau >= tau0 + 4) {                                                                     \
           const int q = tau - 2;                                                                   \
           SP::template stage<2>(interior && q >= z0 && q < z1, pl_of(q), ring, bnd, rr, inv, cxy, \
-                                roff, v1, cp);                                                     \
+                                roff, h2c, h2m, v1, cp);                                           \
         }                                                                                          \
+        h2m = h2c;                                                                                 \
+        h2c = v1;                                                                                  \
       }                                                                                            \
+      h1m = h1c;                                                                                   \
+      h1c = v0;                                                                                    \
     }                                                                                              \
     __syncthreads();                                                                               \
     xsm = xs0;                                                                                     \

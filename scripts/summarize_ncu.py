@@ -21,11 +21,13 @@ def cls_of(name, grid=None):
         mode = int(m.group(2))
         return {0: "stencil_spmv", 1: "stencil_spmv_sweep1", 2: "stencil_sweep", 3: "stencil_sweep",
                 4: "stencil_resid", 5: "stencil_resid_sweep1", 6: "stencil_scale"}[mode]
-    m = re.search(r"chain_kernel<(\d+), (\d+)", name)
+    m = re.search(r"chain_kernel(_x2)?<(\d+), (\d+)", name)
     if m:
         return "chain"
     for k in ("bdot", "bupd", "normalize", "lincomb", "proj", "rotate", "bicg_p", "bicg_s",
-              "bicg_xr", "bicg_setup", "validate", "chain"):
+              "bicg_xr", "bicg_setup", "validate", "chain", "invdiag", "colour_sweep"):
+        if re.search(rf"\b{k}_tile_kernel\b", name):
+            return k
         if re.search(rf"\b{k}(_kernel)?\b", name) or f"{k}_kernel" in name:
             return k
     return name.split("(")[0][:40]
