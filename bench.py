@@ -313,7 +313,7 @@ def run_rk(args):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             wall = float(t.item())
         e2e = {"value": round(wall / args.steps / T, 3), "unit": "ms/system",
-               "h2d_bytes_per_step": int(T * Nl * 8 * 2 * world),
+               "h2d_bytes_per_step": int(T * Nl * 8 * world),      # b_t (x0 = 0 is not uploaded)
                "d2h_bytes_per_step": int(T * Nl * 8 * world)}
     if rank != 0:
         return

@@ -179,6 +179,11 @@ rk_status rk_solve(rk_solver* s, const double* b, double* x, double tol, rk_repo
 /* Same with HOST b and x: the host<->device copies are part of the call. */
 rk_status rk_solve_host(rk_solver* s, const double* b_host, double* x_host, double tol,
                         rk_report* rep);
+/* HOST b, HOST initial guess x0_host (NULL: x0 = 0, the paper's x_hat = 0,
+ * nothing is uploaded or cleared for it), HOST solution x_host
+ * (written on exit; may alias x0_host).  Copies are part of the call. */
+rk_status rk_solve_host_ex(rk_solver* s, const double* b_host, const double* x0_host,
+                           double* x_host, double tol, rk_report* rep);
 /* Residual history of the last solve: rows (krylov_matvecs, ||b-Ax|| or NaN,
  * preconditioned / updated ||r||).  out is HOST [cap][3]. */
 rk_status rk_history(rk_solver* s, double* out, int64_t cap, int64_t* len);

@@ -6,7 +6,7 @@ C-ABI.  The objects mirror the ABI one to one:
 
   Context       rk_ctx_create / rk_launch_count / rk_profile_*
   GridOperator  rk_op_create / rk_op_apply / rk_precond_apply / rk_op_update_bands
-  Solver        rk_solver_create / rk_solve / rk_solve_host / rk_solver_set_method /
+  Solver        rk_solver_create / rk_solve / rk_solve_host(_ex) / rk_solver_set_method /
                 rk_recycle_set / rk_recycle_dim / rk_recycle_export / rk_history
   solve_sequence  the hybrid/sequence controller of PAPER P:662-669 (host
                   control only: switch, epoch refresh, one rk_solve per system)
@@ -166,11 +166,12 @@ class Solver:
         L.check(L.lib().rk_solve(self.h, _p(b), _p(x), tol, C.byref(rep)), "rk_solve")
         return x, _report(rep)
 
-    def solve_host(self, b_host, x_host, tol=0.0):
-        """b_host, x_host: CPU float64 tensors (pinned for async copies)."""
+    def solve_host(self, b_host, x_host, tol=0.0, x0_zero=False):
+        """b_host, x_host: CPU float64 tensors (pinned for async copies).
+        x_host holds x0 on entry unless x0_zero (x0 = 0 without touching it)."""
         rep = L.rk_report()
-        L.check(L.lib().rk_solve_host(self.h, _p(b_host), _p(x_host), tol, C.byref(rep)),
-                "rk_solve_host")
+        L.check(L.lib().rk_solve_host_ex(self.h, _p(b_host), None if x0_zero else _p(x_host),
+                                         _p(x_host), tol, C.byref(rep)), "rk_solve_host_ex")
         return x_host, _report(rep)
 
     def recycle_dim(self):
@@ -248,13 +249,17 @@ def solve_sequence(solver, rhs, n, method, n_sw=0, epoch_of=None, bands_for_epoc
             solver.set_method(tag)
         b = rhs(t)
         x = x_out[t] if x_out is not None else torch.zeros_like(b)
-        x.zero_()
-        solve = solver.solve_host if host else solver.solve
-        _, r = solve(b, x, tol)
+        if host:   # x_hat = 0 without clearing the host buffer
+            solve = lambda b_, x_: solver.solve_host(b_, x_, tol, x0_zero=True)
+        else:
+            x.zero_()
+            solve = lambda b_, x_: solver.solve(b_, x_, tol)
+        _, r = solve(b, x)
         if method == "hybrid" and tag == "rbicgstab" and switchback and r["outcome"] != "CONVERGED":
             solver.set_method("rgcrot")
-            x.zero_()
-            _, r2 = solve(b, x, tol)
+            if not host:
+                x.zero_()
+            _, r2 = solve(b, x)
             for key in ("krylov_matvecs", "operator_applications", "seconds"):
                 r2[key] += r[key]
             r = r2

@@ -1269,7 +1269,8 @@ rk_status rk_solve(rk_solver* s, const double* b, double* xu, double tol, rk_rep
   });
 }
 
-rk_status rk_solve_host(rk_solver* s, const double* bh, double* xh, double tol, rk_report* rep) {
+rk_status rk_solve_host_ex(rk_solver* s, const double* bh, const double* x0h, double* xh, double tol,
+                           rk_report* rep) {
   return guarded([&] {
     RK_REQUIRE(s && bh && xh, RK_EINVAL, "NULL argument");
     RK_CUDA(cudaSetDevice(s->ctx->device));
@@ -1277,8 +1278,11 @@ rk_status rk_solve_host(rk_solver* s, const double* bh, double* xh, double tol, 
     const auto t0 = std::chrono::steady_clock::now();
     RK_CUDA(cudaMemcpyAsync(s->bdev, bh, sizeof(double) * s->N, cudaMemcpyHostToDevice,
                             s->ctx->stream));
-    RK_CUDA(cudaMemcpyAsync(s->x, xh, sizeof(double) * s->N, cudaMemcpyHostToDevice,
-                            s->ctx->stream));
+    if (x0h)
+      RK_CUDA(cudaMemcpyAsync(s->x, x0h, sizeof(double) * s->N, cudaMemcpyHostToDevice,
+                              s->ctx->stream));
+    else
+      RK_CUDA(cudaMemsetAsync(s->x, 0, sizeof(double) * s->N, s->ctx->stream));
     if (!(tol > 0)) tol = s->cfg.tol;
     rk_report r;
     std::memset(&r, 0, sizeof(r));
@@ -1294,6 +1298,10 @@ rk_status rk_solve_host(rk_solver* s, const double* bh, double* xh, double tol, 
     s->last = r;
     if (rep) *rep = r;
   });
+}
+
+rk_status rk_solve_host(rk_solver* s, const double* bh, double* xh, double tol, rk_report* rep) {
+  return rk_solve_host_ex(s, bh, xh, xh, tol, rep);
 }
 
 rk_status rk_history(rk_solver* s, double* out, int64_t cap, int64_t* len) {

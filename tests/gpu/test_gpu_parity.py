@@ -422,6 +422,32 @@ def test_sequence_parity_host_buffers(rk, ctx):
     compare_sequences(w, gpu, ora, w.params.method)
 
 
+def test_solve_host_ex_nonzero_x0(rk, ctx):
+    """rk_solve_host_ex with a HOST initial guess (reading R6) equals the
+    device rk_solve from the same x0; x0 = NULL equals x0 = 0."""
+    w = get_workload("c3s")
+    prob = w.problem()
+    op = make_op(rk, ctx, prob)
+    b = prob.rhs(2).reshape(-1)
+    x0 = np.random.default_rng(8).uniform(-0.1, 0.1, prob.N)
+    outs = []
+    for mode in ("dev", "host", "dev0", "host0"):
+        s = rk.Solver(op, rk.config_from_params(w.params, "rgcrot"))
+        if mode == "dev":
+            x, r = s.solve(dev(b), dev(x0))
+        elif mode == "dev0":
+            x, r = s.solve(dev(b), dev(np.zeros(prob.N)))
+        else:
+            xh = torch.from_numpy(x0.copy() if mode == "host" else np.full(prob.N, np.nan)).pin_memory()
+            x, r = s.solve_host(torch.from_numpy(b).pin_memory(), xh, x0_zero=(mode == "host0"))
+        assert r["outcome"] == "CONVERGED"
+        outs.append(x.cpu().numpy())
+        s.close()
+    assert np.array_equal(outs[0], outs[1])
+    assert np.array_equal(outs[2], outs[3])
+    op.close()
+
+
 def test_recycle_space_invariants_after_hybrid(rk, ctx):
     """After the hybrid the exported space satisfies A U = C, C^T C = I
     (BASELINE north_star: 1e-12), i.e. the rBiCGStab-side QR refresh."""
