@@ -197,6 +197,9 @@ rk_status rk_solver_workspace(rk_solver* s, int64_t* nvec);
  * algorithmic bytes. */
 rk_status rk_launch_count(rk_ctx* ctx, int64_t* count);
 rk_status rk_profile_enable(rk_ctx* ctx, int on, const char* filter);
+/* Bracket only every `every`-th matching launch (>= 1; default 1): a live
+ * sample of a kernel class with less event traffic in a timed region. */
+rk_status rk_profile_every(rk_ctx* ctx, int every);
 /* names: HOST buffer of cap x 32 chars; launches, ms, bytes: HOST [cap]. */
 rk_status rk_profile_read(rk_ctx* ctx, int cap, char* names, int64_t* launches,
                           double* ms, double* bytes, int* n);

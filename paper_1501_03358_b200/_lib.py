@@ -84,6 +84,7 @@ def lib():
         "rk_solver_workspace": ([vp, P(i64)], i32),
         "rk_launch_count": ([vp, P(i64)], i32),
         "rk_profile_enable": ([vp, i32, C.c_char_p], i32),
+        "rk_profile_every": ([vp, i32], i32),
         "rk_profile_read": ([vp, i32, vp, vp, vp, vp, P(i32)], i32),
     }
     for name, (args, res) in sig.items():
@@ -106,4 +107,4 @@ EXPORTED = ["rk_last_error", "rk_version", "rk_nccl_unique_id", "rk_ctx_create",
             "rk_op_apply", "rk_precond_apply", "rk_solver_create", "rk_solver_destroy",
             "rk_solver_set_method", "rk_recycle_set", "rk_recycle_dim", "rk_recycle_export",
             "rk_solve", "rk_solve_host", "rk_solve_host_ex", "rk_history", "rk_solver_workspace", "rk_launch_count",
-            "rk_profile_enable", "rk_profile_read"]
+            "rk_profile_enable", "rk_profile_every", "rk_profile_read"]

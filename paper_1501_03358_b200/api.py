@@ -44,9 +44,10 @@ class Context:
         L.check(L.lib().rk_launch_count(self.h, C.byref(n)), "rk_launch_count")
         return n.value
 
-    def profile(self, on=True, filter=None):
+    def profile(self, on=True, filter=None, every=1):
         L.check(L.lib().rk_profile_enable(self.h, 1 if on else 0,
                                           filter.encode() if filter else None), "rk_profile_enable")
+        L.check(L.lib().rk_profile_every(self.h, every), "rk_profile_every")
 
     def profile_read(self, reset=False):
         cap = 64

@@ -466,7 +466,13 @@ void launch_one(rk_op* op, ChainParams cp, dim3 grid) {
     encode(&mx, cp.xin - op->P, 3, dims, str, box);
   }
   dim3 blk(X2 ? G::EX / 2 : G::EX, G::EY);
-  launch_pdl(op->ctx, kern, grid, blk, G::SMEM, mb, mr, mx, cp);
+  // PDL lets the next grid's CTAs become resident early; next to the chain
+  // (one 200 KB-smem CTA per SM) that measured 9 % slower at c3, so by
+  // default neither the chain nor its successor overlaps (RK_PDL_MODE)
+  rk_ctx* ctx = op->ctx;
+  const bool allow = ctx->pdl && ctx->pdl_mode == 0 && !ctx->pdl_skip_next;
+  ctx->pdl_skip_next = ctx->pdl_mode >= 2;
+  launch_pdl_if(ctx, allow, kern, grid, blk, G::SMEM, mb, mr, mx, cp);
 }
 
 template <int NST, int TX, int TY, int PD, int X2 = 0>

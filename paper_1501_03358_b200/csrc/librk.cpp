@@ -1336,6 +1336,14 @@ rk_status rk_profile_enable(rk_ctx* ctx, int on, const char* filter) {
   });
 }
 
+rk_status rk_profile_every(rk_ctx* ctx, int every) {
+  return guarded([&] {
+    RK_REQUIRE(ctx && every >= 1, RK_EINVAL, "every >= 1");
+    ctx->prof_every = every;
+    ctx->prof_seen = 0;
+  });
+}
+
 rk_status rk_profile_read(rk_ctx* ctx, int cap, char* names, int64_t* launches, double* ms,
                           double* bytes, int* n) {
   return guarded([&] {

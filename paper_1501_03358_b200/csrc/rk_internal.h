@@ -131,6 +131,8 @@ struct rk_ctx {
   int device = 0, rank = 0, nranks = 1, sms = 148;
   int64_t l2_bytes = 0;         // L2 capacity (chain policy)
   bool pdl = true;              // programmatic dependent launch (env RK_NO_PDL: off)
+  int pdl_mode = 2;             // RK_PDL_MODE: 0 all kernels; 1 not the chain; 2 neither the chain nor its successor
+  bool pdl_skip_next = false;   // set by a chain launch (mode 2)
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   double* partials = nullptr;
@@ -140,6 +142,8 @@ struct rk_ctx {
   // profiling
   bool prof_on = false;
   std::string prof_filter;
+  int prof_every = 1;           // bracket every n-th matching launch
+  int64_t prof_seen = 0;
   struct Pending {
     std::string cls;
     cudaEvent_t a, b;
@@ -182,7 +186,8 @@ struct Launch {
   size_t idx = 0;
   Launch(rk_ctx* c, const char* cls, double bytes) : ctx(c) {
     ++ctx->launches;
-    if (ctx->prof_on && (ctx->prof_filter.empty() || strstr(cls, ctx->prof_filter.c_str()))) {
+    if (ctx->prof_on && (ctx->prof_filter.empty() || strstr(cls, ctx->prof_filter.c_str())) &&
+        (ctx->prof_seen++ % ctx->prof_every) == 0) {
       on = true;
       rk_ctx::Pending p;
       p.cls = cls;
@@ -215,6 +220,10 @@ struct Launch {
 // the predecessor grid has completed and its memory is visible; then
 // launch_dependents), so the overlap hides launch latency and tails without
 // changing any result.
+template <typename... KArgs, typename... Args>
+void launch_pdl_if(rk_ctx* ctx, bool allow, void (*kern)(KArgs...), dim3 grid, dim3 blk,
+                   size_t smem, Args&&... args);
+
 #define RK_PDL_ENTRY()                                         \
   do {                                                         \
     asm volatile("griddepcontrol.wait;" ::: "memory");          \
@@ -222,8 +231,8 @@ struct Launch {
   } while (0)
 
 template <typename... KArgs, typename... Args>
-void launch_pdl(rk_ctx* ctx, void (*kern)(KArgs...), dim3 grid, dim3 blk, size_t smem,
-                Args&&... args) {
+void launch_pdl_if(rk_ctx* ctx, bool allow, void (*kern)(KArgs...), dim3 grid, dim3 blk,
+                   size_t smem, Args&&... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = blk;
@@ -231,10 +240,18 @@ void launch_pdl(rk_ctx* ctx, void (*kern)(KArgs...), dim3 grid, dim3 blk, size_t
   cfg.stream = ctx->stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = ctx->pdl ? 1 : 0;
+  attr[0].val.programmaticStreamSerializationAllowed = allow ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   RK_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(rk_ctx* ctx, void (*kern)(KArgs...), dim3 grid, dim3 blk, size_t smem,
+                Args&&... args) {
+  const bool allow = ctx->pdl && !ctx->pdl_skip_next;
+  ctx->pdl_skip_next = false;
+  launch_pdl_if(ctx, allow, kern, grid, blk, smem, std::forward<Args>(args)...);
 }
 
 // fused chain (chain.cu): max stages per launch for this operator (0 = unavailable)
