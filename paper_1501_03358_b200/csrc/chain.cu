@@ -470,7 +470,9 @@ void launch_one(rk_op* op, ChainParams cp, dim3 grid) {
   // (one 200 KB-smem CTA per SM) that measured 9 % slower at c3, so by
   // default neither the chain nor its successor overlaps (RK_PDL_MODE)
   rk_ctx* ctx = op->ctx;
-  const bool allow = ctx->pdl && ctx->pdl_mode == 0 && !ctx->pdl_skip_next;
+  // mode 0: chain and successor overlap; 1: chain does not; 2: neither;
+  // 3: the chain overlaps its predecessor, its successor does not
+  const bool allow = ctx->pdl && (ctx->pdl_mode == 0 || ctx->pdl_mode == 3) && !ctx->pdl_skip_next;
   ctx->pdl_skip_next = ctx->pdl_mode >= 2;
   launch_pdl_if(ctx, allow, kern, grid, blk, G::SMEM, mb, mr, mx, cp);
 }

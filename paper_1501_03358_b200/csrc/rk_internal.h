@@ -131,7 +131,7 @@ struct rk_ctx {
   int device = 0, rank = 0, nranks = 1, sms = 148;
   int64_t l2_bytes = 0;         // L2 capacity (chain policy)
   bool pdl = true;              // programmatic dependent launch (env RK_NO_PDL: off)
-  int pdl_mode = 2;             // RK_PDL_MODE: 0 all kernels; 1 not the chain; 2 neither the chain nor its successor
+  int pdl_mode = 3;             // RK_PDL_MODE (chain.cu): default 3 = the chain overlaps its predecessor, its successor does not
   bool pdl_skip_next = false;   // set by a chain launch (mode 2)
   cudaStream_t stream = nullptr;
   bool own_stream = false;

@@ -742,3 +742,27 @@ def test_full_size_kernels_sampled(rk, ctx, name):
         assert abs(y[g].item() - yo) <= 1e-12 * yabs, (k, j, i)
         assert abs(z[g].item() - zo) <= 1e-12 * max(abs(zo), 1e-3 * float(np.abs(r_h).max())), (k, j, i)
     op.close()
+
+
+@pytest.mark.parametrize("name,force,kw", [("c3m", True, {}), ("c2s", False, {}),
+                                          ("c3s", False, {"precond": "ssor"})])
+def test_run_to_run_bitwise(rk, ctx, name, force, kw, monkeypatch):
+    """Race detection without compute-sanitizer (closed on this pool): every
+    reduction is a fixed-order two-stage tree and the chain's shared-memory
+    pipeline is barrier/mbarrier ordered, so two runs of the same sequence
+    must agree bit for bit -- a race (e.g. a ring slot reused too early)
+    shows up as a run-to-run difference."""
+    from dataclasses import replace
+    from problems.workloads import Workload
+    w0 = get_workload(name)
+    w = Workload(w0.name, w0.make_problem, replace(w0.params, **kw), w0.n_systems, w0.epoch_every,
+                 w0.description)
+    if force:
+        monkeypatch.setenv("RK_FORCE_CHAIN", "1")
+    a, _ = gpu_sequence(rk, ctx, w)
+    b, _ = gpu_sequence(rk, ctx, w)
+    monkeypatch.delenv("RK_FORCE_CHAIN", raising=False)
+    for (ra, xa), (rb, xb) in zip(a, b):
+        assert np.array_equal(xa, xb)
+        assert ra["krylov_matvecs"] == rb["krylov_matvecs"]
+        assert ra["final_true_res"] == rb["final_true_res"]
