@@ -92,7 +92,10 @@ typedef struct {
   int k_max;           /* max recycle dimension                             */
   int k_keep;          /* k_t: dimension after truncation       */
   int select_count;    /* p1: candidates added per cycle, 0..2  */
-  int ortho;           /* 0 = CGS2 (block classical Gram-Schmidt, twice)    */
+  int ortho;           /* 0 = CGS2 (block classical Gram-Schmidt, twice);   
+                        * 1 = Gram-corrected CGS2: coefficients (2I - G) Q^T w
+                        * with G = Q^T Q from lagged dots, one update pass  
+                        * (R19; falls back to 0 for odd N)        */
   int trunc;           /* 0 = T1 (drop the oldest columns);     
                         * 1 = T2 (keep the directions of range(C) with the 
                         * smallest principal angles to the cycle's image  

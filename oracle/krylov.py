@@ -198,6 +198,7 @@ def rgcrot(op, pc, b, U, C, prm, valid=True, hook=None):
         H = np.zeros((m + 1, m))
         Bm = np.zeros((k, m))
         V[:, 0] = r / rho                                  # line 4
+        Grow = np.zeros((k + m + 1, k + m + 1))            # cgs2g: lagged Gram rows
         m_eff = m
         for j in range(m):                                 # line 5
             w = ahat(V[:, j])                              # line 6
@@ -210,6 +211,25 @@ def rgcrot(op, pc, b, U, C, prm, valid=True, hook=None):
                 for l in range(j + 1):                     # lines 7-9
                     H[l, j] = V[:, l] @ w
                     w = w - V[:, l] * H[l, j]
+            elif prm.ortho == "cgs2g":
+                # [R19] CGS2 with the second pass taken from the Gram matrix:
+                # g = Q^T w, G = Q^T Q (C-block = I; the other rows are the
+                # lagged dots Q_j^T v_j of each step), h = g + (g - G g) =
+                # (2I - G) g -- CGS2's coefficients g1 + g2 in exact
+                # arithmetic -- and ONE update w -= Q h.
+                Q = np.column_stack([C, V[:, :j + 1]])
+                Grow[k + j, :k + j + 1] = Q.T @ V[:, j]      # lagged row of v_j
+                L = Grow[k:k + j + 1, :k + j + 1]                 # rows of v_0..v_j (lower part)
+                G = np.eye(k + j + 1)
+                G[k:, :] = L
+                G[:, k:] = L.T
+                Lv = L[:, k:]
+                G[k:, k:] = Lv + Lv.T - np.diag(np.diag(Lv))
+                g = Q.T @ w
+                h = 2.0 * g - G @ g
+                w = w - Q @ h
+                Bm[:, j] = h[:k]
+                H[:j + 1, j] = h[k:]
             else:
                 # [D8] block classical Gram-Schmidt over [C V_j], applied twice
                 Q = np.column_stack([C, V[:, :j + 1]])

@@ -119,10 +119,11 @@ class GridOperator:
 
 def make_config(method="rgcrot", m=20, k_max=10, k_keep=5, select_count=1, precond="jacobi",
                 sweeps=5, omega_l=0.8, omega_g=1.0, tol=1e-8, max_matvecs=2000,
-                divergence=1e4, trunc="T1", zblocks=1):
+                divergence=1e4, trunc="T1", zblocks=1, ortho="cgs2g"):
     pc = L.rk_precond({"none": 0, "jacobi": 1, "ssor": 2}[precond], sweeps, omega_l, omega_g, zblocks)
-    return L.rk_config(L.METHODS[method], m, k_max, k_keep, select_count, 0,
-                       {"T1": 0, "T2": 1}[trunc], pc, tol, max_matvecs, divergence)
+    return L.rk_config(L.METHODS[method], m, k_max, k_keep, select_count,
+                       {"cgs2": 0, "cgs2g": 1}[ortho], {"T1": 0, "T2": 1}[trunc], pc, tol,
+                       max_matvecs, divergence)
 
 
 def config_from_params(prm, method=None):
@@ -137,7 +138,8 @@ def config_from_params(prm, method=None):
                        omega_l=getattr(prm, "omega_s", 1.0) if pcn == "ssor" else prm.omega_l,
                        omega_g=prm.omega_g,
                        tol=prm.tol, max_matvecs=prm.max_mv, divergence=prm.divergence,
-                       trunc=getattr(prm, "trunc", "T1"), zblocks=getattr(prm, "zblocks", 1))
+                       trunc=getattr(prm, "trunc", "T1"), zblocks=getattr(prm, "zblocks", 1),
+                       ortho=getattr(prm, "ortho", "cgs2g"))
 
 
 def _report(r):

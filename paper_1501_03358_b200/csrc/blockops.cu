@@ -153,6 +153,154 @@ __global__ void __launch_bounds__(BT) bdot_tile_kernel(ColPtrs Q, int ncol, cons
   block_reduce_store<NC>(acc, ncol, ra);
 }
 
+// Two right-hand sides: [Q^T w, Q^T v] in one read of Q (the Gram-corrected
+// CGS2 of reading R19 needs Q_j^T v_j, the lagged Gram row of the newest basis
+// vector, next to the projection coefficients Q_j^T w).  Values 0..NC-1 go to
+// out (w), NC.. to out2 (v); only the first ncol of each are stored.
+template <int NC>
+__global__ void __launch_bounds__(256) bdot2_tile_kernel(ColPtrs Q, int ncol, const double* __restrict__ w,
+                                                         const double* __restrict__ v, int64_t N, RedArgs ra) {
+  RK_PDL_ENTRY();
+  constexpr int RV = 2, G = 2, BT = 256, TILE_ROWS = 2 * BT * RV;
+  double acc[2 * NC];
+#pragma unroll
+  for (int c = 0; c < 2 * NC; ++c) acc[c] = 0.0;
+  const int64_t ntile = N / TILE_ROWS;
+#pragma unroll 1
+  for (int64_t t = blockIdx.x; t < ntile; t += gridDim.x) {
+    const int64_t r0 = t * TILE_ROWS + 2 * threadIdx.x;
+    double2 wv[RV], vv[RV];
+#pragma unroll
+    for (int u = 0; u < RV; ++u) {
+      wv[u] = __ldg(reinterpret_cast<const double2*>(w + r0 + 2 * BT * u));
+      vv[u] = __ldg(reinterpret_cast<const double2*>(v + r0 + 2 * BT * u));
+    }
+#pragma unroll
+    for (int c = 0; c < NC; c += G) {
+      if (c < ncol) {
+        double2 q[G][RV];
+#pragma unroll
+        for (int g = 0; g < G; ++g)
+#pragma unroll
+          for (int u = 0; u < RV; ++u) {
+            const Vec<2> a = ldv_stream<2>(Q.p[c + g] + r0 + 2 * BT * u);
+            q[g][u] = make_double2(a.v[0], a.v[1]);
+          }
+#pragma unroll
+        for (int g = 0; g < G; ++g)
+#pragma unroll
+          for (int u = 0; u < RV; ++u) {
+            acc[c + g] = fma(q[g][u].x, wv[u].x, acc[c + g]);
+            acc[c + g] = fma(q[g][u].y, wv[u].y, acc[c + g]);
+            acc[NC + c + g] = fma(q[g][u].x, vv[u].x, acc[NC + c + g]);
+            acc[NC + c + g] = fma(q[g][u].y, vv[u].y, acc[NC + c + g]);
+          }
+      }
+    }
+  }
+  for (int64_t r = ntile * TILE_ROWS + 2 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x); r < N;
+       r += 2 * (int64_t)gridDim.x * blockDim.x) {
+    const Vec<2> wv = ldv_ro<2>(w + r), vv = ldv_ro<2>(v + r);
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+      if (c < ncol) {
+        const Vec<2> a = ldv_stream<2>(Q.p[c] + r);
+        acc[c] = fma(a.v[0], wv.v[0], acc[c]);
+        acc[c] = fma(a.v[1], wv.v[1], acc[c]);
+        acc[NC + c] = fma(a.v[0], vv.v[0], acc[NC + c]);
+        acc[NC + c] = fma(a.v[1], vv.v[1], acc[NC + c]);
+      }
+  }
+  block_reduce_store<2 * NC>(acc, 2 * NC, ra);
+}
+
+// The Gram-corrected CGS2 update (reading R19): every CTA forms, in shared
+// memory, h = 2 g - G g from the projection coefficients g = Q^T w and the
+// Gram matrix G = Q^T Q of the basis Q = [C, v_0 .. v_j] (C-block = I; the
+// rows of v_0 .. v_j are the lagged dots grow[k + i][0 .. k + i], row stride
+// MAXCOL), then streams w <- w - Q h (+ ||w||^2) like bupd_tile_kernel.
+// CTA 0 stores h (the Hessenberg / B column) to hout.
+template <int NC>
+__global__ void __launch_bounds__(256) bupd_gram_kernel(ColPtrs Q, int ncol, int k, const double* __restrict__ g,
+                                                        const double* __restrict__ grow, double* __restrict__ hout,
+                                                        double* __restrict__ w, int64_t N, RedArgs ra) {
+  RK_PDL_ENTRY();
+  constexpr int RV = TRV, G = TG;
+  __shared__ double gs[NC], hs[NC];
+  for (int c = threadIdx.x; c < NC; c += blockDim.x) gs[c] = c < ncol ? g[c] : 0.0;
+  __syncthreads();
+  for (int c = threadIdx.x; c < NC; c += blockDim.x) {
+    double h = 0.0;
+    if (c < ncol) {
+      double gg = 0.0;
+      for (int l = 0; l < ncol; ++l) {
+        double Gcl;
+        if (c < k && l < k) Gcl = (c == l) ? 1.0 : 0.0;
+        else if (c >= l) Gcl = grow[(int64_t)c * MAXCOL + l];
+        else Gcl = grow[(int64_t)l * MAXCOL + c];
+        gg = fma(Gcl, gs[l], gg);
+      }
+      h = 2.0 * gs[c] - gg;
+    }
+    hs[c] = h;
+    if (blockIdx.x == 0 && c < ncol) hout[c] = h;
+  }
+  __syncthreads();
+  const volatile double* hv = hs;
+  double acc[1] = {0.0};
+  const int64_t ntile = N / TILE_ROWS;
+#pragma unroll 1
+  for (int64_t t = blockIdx.x; t < ntile; t += gridDim.x) {
+    const int64_t r0 = t * TILE_ROWS + 2 * threadIdx.x;
+    double2 wv[RV];
+#pragma unroll
+    for (int u = 0; u < RV; ++u) wv[u] = *reinterpret_cast<const double2*>(w + r0 + 512 * u);
+#pragma unroll
+    for (int c = 0; c < NC; c += G) {
+      if (c < ncol) {
+        double hc[G];
+#pragma unroll
+        for (int u = 0; u < G; ++u) hc[u] = hv[c + u];
+        double2 q[G][RV];
+#pragma unroll
+        for (int u = 0; u < G; ++u)
+#pragma unroll
+          for (int vv = 0; vv < RV; ++vv) {
+            const Vec<2> a = ldv_stream<2>(Q.p[c + u] + r0 + 512 * vv);
+            q[u][vv] = make_double2(a.v[0], a.v[1]);
+          }
+#pragma unroll
+        for (int u = 0; u < G; ++u)
+#pragma unroll
+          for (int vv = 0; vv < RV; ++vv) {
+            wv[vv].x = fma(-hc[u], q[u][vv].x, wv[vv].x);
+            wv[vv].y = fma(-hc[u], q[u][vv].y, wv[vv].y);
+          }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < RV; ++u) {
+      *reinterpret_cast<double2*>(w + r0 + 512 * u) = wv[u];
+      acc[0] = fma(wv[u].x, wv[u].x, acc[0]);
+      acc[0] = fma(wv[u].y, wv[u].y, acc[0]);
+    }
+  }
+  for (int64_t r = ntile * TILE_ROWS + 2 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x); r < N;
+       r += 2 * (int64_t)gridDim.x * blockDim.x) {
+    double2 wn = *reinterpret_cast<const double2*>(w + r);
+#pragma unroll 1
+    for (int c = 0; c < ncol; ++c) {
+      const Vec<2> a = ldv_stream<2>(Q.p[c] + r);
+      wn.x = fma(-hs[c], a.v[0], wn.x);
+      wn.y = fma(-hs[c], a.v[1], wn.y);
+    }
+    *reinterpret_cast<double2*>(w + r) = wn;
+    acc[0] = fma(wn.x, wn.x, acc[0]);
+    acc[0] = fma(wn.y, wn.y, acc[0]);
+  }
+  block_reduce_store<1>(acc, 1, ra);
+}
+
 template <int NC, int ND>
 __global__ void __launch_bounds__(256) bupd_tile_kernel(ColPtrs Q, int ncol, const double* __restrict__ g,
                                                         double gs, double* __restrict__ w, int64_t N,
@@ -476,6 +624,64 @@ void bupd(rk_ctx* ctx, const std::vector<const double*>& cols, const double* g, 
 #undef RK_BUPD
   L.done();
   if (nd) allreduce(ctx, red_out, nd);
+}
+
+void bdot2(rk_ctx* ctx, const std::vector<const double*>& cols_all, const double* w, const double* v,
+           int64_t N, double* out_w, double* out_v) {
+  const int total = (int)cols_all.size();
+  RK_REQUIRE(total <= MAXCOL + 1, RK_EINVAL, "too many columns in a block product");
+  const bool tiled = pick_vec(N, {w, v}, cols_all) == 2;
+  if (!tiled) {   // odd sizes / misaligned: two single-RHS block dots
+    bdot(ctx, cols_all, w, N, out_w);
+    bdot(ctx, cols_all, v, N, out_v);
+    return;
+  }
+  for (int off = 0; off < total; off += 24) {
+    std::vector<const double*> cols(cols_all.begin() + off, cols_all.begin() + std::min(total, off + 24));
+    const int ncol = (int)cols.size();
+    const int nc = nc_round(ncol);
+    RedArgs ra = red_args(ctx, out_w + off);
+    ra.out2 = out_v + off;
+    ra.split = nc;
+    ra.valid = ncol;
+    ColPtrs Q = make_cols_padded(cols, nc);
+    Launch L(ctx, "bdot", 8.0 * N * (ncol + 2));
+    switch (nc) {
+      case 8: launch_k(ctx, bdot2_tile_kernel<8>, N / 4, dim3(256), Q, ncol, w, v, N, ra); break;
+      case 16: launch_k(ctx, bdot2_tile_kernel<16>, N / 4, dim3(256), Q, ncol, w, v, N, ra); break;
+      default: launch_k(ctx, bdot2_tile_kernel<24>, N / 4, dim3(256), Q, ncol, w, v, N, ra); break;
+    }
+    L.done();
+    allreduce(ctx, out_w + off, ncol);
+    allreduce(ctx, out_v + off, ncol);
+  }
+}
+
+void bupd_gram(rk_ctx* ctx, const std::vector<const double*>& cols, int k, const double* g,
+               const double* grow, double* hout, double* w, int64_t N, double* red_out) {
+  const int ncol = (int)cols.size();
+  RK_REQUIRE(ncol <= MAXCOL, RK_EINVAL, "too many columns in a block product");
+  RK_REQUIRE(pick_vec(N, {w}, cols) == 2, RK_EUNSUPPORTED, "bupd_gram needs even N, aligned columns");
+  const int nc = nc_round(ncol);
+  ColPtrs Q = make_cols_padded(cols, nc);
+  RedArgs ra = red_args(ctx, red_out);
+  Launch L(ctx, "bupd", 8.0 * N * (ncol + 2));
+#define RK_BG(NCV) launch_k(ctx, bupd_gram_kernel<NCV>, N / (2 * TRV), dim3(256), Q, ncol, k, g, grow, hout, w, N, ra)
+  switch (nc) {
+    case 8: RK_BG(8); break;
+    case 16: RK_BG(16); break;
+    case 24: RK_BG(24); break;
+    case 32: RK_BG(32); break;
+    case 40: RK_BG(40); break;
+    case 48: RK_BG(48); break;
+    case 56: RK_BG(56); break;
+    case 64: RK_BG(64); break;
+    case 72: RK_BG(72); break;
+    default: RK_BG(80); break;
+  }
+#undef RK_BG
+  L.done();
+  allreduce(ctx, red_out, 1);
 }
 
 void normalize(rk_ctx* ctx, double* w, int64_t N, const double* nrm2, const double* nin2,

@@ -158,7 +158,13 @@ __device__ __forceinline__ void block_reduce_store(const double (&v)[NV], int nv
       double s = (s0 + s1) + (s2 + s3);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
-      if (lane == 0) ra.out[q] = s;
+      if (lane == 0) {
+        if (q < ra.split) {
+          if (q < ra.valid) ra.out[q] = s;
+        } else if (q - ra.split < ra.valid) {
+          ra.out2[q - ra.split] = s;
+        }
+      }
     }
     if (tid == 0) atomicExch(ra.counter, 0u);
   }
@@ -194,7 +200,11 @@ void launch_k(rk_ctx* ctx, void (*kern)(KArgs...), int64_t work_threads, dim3 bl
 }
 
 inline RedArgs red_args(rk_ctx* ctx, double* out) {
-  return RedArgs{ctx->partials, ctx->counter, out};
+  RedArgs ra;
+  ra.partials = ctx->partials;
+  ra.counter = ctx->counter;
+  ra.out = out;
+  return ra;
 }
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }

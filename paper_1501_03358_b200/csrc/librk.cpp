@@ -270,7 +270,7 @@ struct rk_solver {
   double* dsc = nullptr;
   double* hsc = nullptr;
   size_t nsc = 0;
-  size_t o_arn = 0, o_misc = 0, o_coef = 0, o_gram = 0, o_T = 0, o_bi = 0, o_eta = 0;
+  size_t o_arn = 0, o_misc = 0, o_coef = 0, o_gram = 0, o_T = 0, o_bi = 0, o_eta = 0, o_grow = 0;
   int max_it = 0;
   std::vector<std::array<double, 3>> history;
   rk_report last{};
@@ -344,6 +344,8 @@ struct rk_solver {
     stencil(op, SM_SWEEP_NORM, zin, r, dst, nullptr, pc.omega_global, red);
   }
   bool jac() const { return cfg.pc.kind == 1; }
+  // Gram-corrected CGS2 [R19] (needs the 16-byte tiled kernels: even N, aligned)
+  bool gram_ortho() const { return cfg.ortho == 1 && (N % 2 == 0) && (op->P % 2 == 0); }
   bool ssor() const { return cfg.pc.kind == 2; }
   void ssor_to(const double* r, double* dst, double* red) {
     ssor_apply(op, cfg.pc, r, dst, za, red);
@@ -553,10 +555,17 @@ struct rk_solver {
         double* g2 = g1 + (MAXCOL + 1);
         auto Qw = Q;
         Qw.push_back(w);
-        bdot(ctx, Qw, w, N, g1);                              // lines 6a-9, CGS pass 1 (+ ||w||^2)
-        bupd(ctx, Q, g1, 1.0, w, N, {}, nullptr);
-        bdot(ctx, Q, w, N, g2);                               // CGS pass 2 [D8]
-        bupd(ctx, Q, g2, 1.0, w, N, {nullptr}, g1 + 2 * (MAXCOL + 1));
+        if (gram_ortho()) {
+          // [R19] one read of [C V_j] for g = Q^T w (+ ||w||^2) and the lagged
+          // Gram row Q^T v_j, one for w -= Q (2 g - G g); h lands in g2
+          bdot2(ctx, Qw, w, V[j], N, g1, dsc + o_grow + (size_t)(k + j) * MAXCOL);
+          bupd_gram(ctx, Q, k, g1, dsc + o_grow, g2, w, N, g1 + 2 * (MAXCOL + 1));
+        } else {
+          bdot(ctx, Qw, w, N, g1);                            // lines 6a-9, CGS pass 1 (+ ||w||^2)
+          bupd(ctx, Q, g1, 1.0, w, N, {}, nullptr);
+          bdot(ctx, Q, w, N, g2);                             // CGS pass 2 [D8]
+          bupd(ctx, Q, g2, 1.0, w, N, {nullptr}, g1 + 2 * (MAXCOL + 1));
+        }
         normalize(ctx, w, N, g1 + 2 * (MAXCOL + 1), g1 + ncol, g1 + 2 * (MAXCOL + 1) + 1);  // line 10
       }
       fetch(o_arn, STEP * m);
@@ -576,8 +585,10 @@ struct rk_solver {
       for (int j = 0; j < m_eff; ++j) {
         const double* h1 = hsc + o_arn + STEP * j;
         const double* h2 = h1 + (MAXCOL + 1);
-        for (int c = 0; c < k; ++c) B[c + (size_t)j * k] = h1[c] + h2[c];
-        for (int l = 0; l <= j; ++l) H[l + (size_t)j * (m_eff + 1)] = h1[k + l] + h2[k + l];
+        // CGS2: h = g1 + g2; Gram-corrected [R19]: h is stored in the g2 slot
+        const double g1w = gram_ortho() ? 0.0 : 1.0;
+        for (int c = 0; c < k; ++c) B[c + (size_t)j * k] = g1w * h1[c] + h2[c];
+        for (int l = 0; l <= j; ++l) H[l + (size_t)j * (m_eff + 1)] = g1w * h1[k + l] + h2[k + l];
         H[j + 1 + (size_t)j * (m_eff + 1)] = std::sqrt(h1[2 * (MAXCOL + 1)]);
       }
       const double prec_res = ls_givens(H, m_eff, rho, y);   // line 12
@@ -1088,7 +1099,7 @@ rk_status rk_solver_create(rk_op* op, const rk_config* cfg, rk_solver** out) {
     RK_REQUIRE(cfg->k_max <= 46, RK_EINVAL, "k_max <= 46");
     RK_REQUIRE(cfg->select_count >= 0 && cfg->select_count <= 2, RK_EINVAL, "select_count 0..2");
     RK_REQUIRE(cfg->k_keep >= 0 && cfg->k_keep <= cfg->k_max, RK_EINVAL, "0 <= k_keep <= k_max");
-    RK_REQUIRE(cfg->ortho == 0, RK_EUNSUPPORTED, "only CGS2");
+    RK_REQUIRE(cfg->ortho == 0 || cfg->ortho == 1, RK_EINVAL, "ortho: 0 (CGS2) or 1 (Gram-corrected CGS2)");
     RK_REQUIRE(cfg->trunc == 0 || cfg->trunc == 1, RK_EINVAL, "trunc: 0 (T1) or 1 (T2)");
     RK_REQUIRE(cfg->pc.kind == 0 || ((cfg->pc.kind == 1 || cfg->pc.kind == 2) && cfg->pc.sweeps >= 1),
                RK_EINVAL, "bad preconditioner");
@@ -1135,6 +1146,8 @@ rk_status rk_solver_create(rk_op* op, const rk_config* cfg, rk_solver** out) {
       s->o_gram = o;
       o += (size_t)MAXCOL * MAXCOL;
       s->o_T = o;
+      o += (size_t)MAXCOL * MAXCOL;
+      s->o_grow = o;                       // lagged Gram rows [R19]
       o += (size_t)MAXCOL * MAXCOL;
       o = (o + 7) & ~size_t(7);
       s->o_bi = o;

@@ -48,7 +48,10 @@ struct ColPtrs {
 struct RedArgs {
   double* partials;     // [nval][gridDim.x]
   unsigned* counter;    // last-block ticket (reset by the last block)
-  double* out;          // nval results
+  double* out;          // nval results (value q -> out[q] ...
+  double* out2 = nullptr;   // ... or, for q >= split, out2[q - split])
+  int split = 1 << 30;
+  int valid = 1 << 30;  // only values with (q mod split) < valid are stored
 };
 
 // Stencil kernel modes (K1/K2 of SURVEY §2.4)
@@ -278,6 +281,12 @@ void bdot(rk_ctx* ctx, const std::vector<const double*>& cols, const double* w, 
           double* out);
 void bupd(rk_ctx* ctx, const std::vector<const double*>& cols, const double* g, double gscale,
           double* w, int64_t N, const std::vector<const double*>& dots, double* red_out);
+// [Q^T w, Q^T v] in one read of Q (Gram-corrected CGS2, R19)
+void bdot2(rk_ctx* ctx, const std::vector<const double*>& cols, const double* w, const double* v,
+           int64_t N, double* out_w, double* out_v);
+// w <- w - Q h with h = 2 g - G g (G from the lagged Gram rows), ||w||^2 -> red_out
+void bupd_gram(rk_ctx* ctx, const std::vector<const double*>& cols, int k, const double* g,
+               const double* grow, double* hout, double* w, int64_t N, double* red_out);
 void normalize(rk_ctx* ctx, double* w, int64_t N, const double* nrm2, const double* nin2,
                double* flag);
 void lincomb(rk_ctx* ctx, const std::vector<const double*>& cols, const double* coef, int nout,

@@ -351,8 +351,7 @@ __global__ void __launch_bounds__(256) colour_sweep_kernel(StencilParams sp, int
 void colour_sweep(rk_op* op, double* z, const double* r, double omega, int colour) {
   rk_ctx* ctx = op->ctx;
   halo(op, z);
-  StencilParams sp;
-  std::memset(&sp, 0, sizeof(sp));
+  StencilParams sp{};
   sp.bands = op->bands;
   sp.invd = op->invd();
   sp.N = op->N;

@@ -354,6 +354,22 @@ def test_sequence_parity_block_jacobi(rk, ctx, name, zblocks):
     compare_sequences(w, gpu, ora, w.params.method)
 
 
+@pytest.mark.parametrize("name,ortho", [("c2s", "cgs2"), ("c2s", "cgs2g"), ("c3s", "cgs2"),
+                                        ("c3s", "cgs2g"), ("c4hs", "cgs2g"), ("c3m", "cgs2g")])
+def test_sequence_parity_ortho(rk, ctx, name, ortho):
+    """Both Arnoldi orthogonalisations of librk -- CGS2 (D8) and the
+    Gram-corrected CGS2 with one read of [C V_j] per pass (R19) -- against
+    the oracle running the same scheme."""
+    from dataclasses import replace
+    from problems.workloads import Workload
+    w0 = get_workload(name)
+    w = Workload(w0.name, w0.make_problem, replace(w0.params, ortho=ortho), w0.n_systems,
+                 w0.epoch_every, w0.description)
+    ora = run_sequence(w)
+    gpu, _ = gpu_sequence(rk, ctx, w)
+    compare_sequences(w, gpu, ora, w.params.method)
+
+
 @pytest.mark.parametrize("name", ["c2s", "c3s", "c4s"])
 def test_sequence_parity_T2(rk, ctx, name):
     """Truncation T2 (principal angles, reading R13): host Householder QR +

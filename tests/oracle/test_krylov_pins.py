@@ -101,14 +101,17 @@ def test_rgcrot_cycle_is_optimal_over_U_plus_Krylov():
     assert np.linalg.norm(x - xb) <= 1e-8 * np.linalg.norm(xb)
 
 
-def test_rgcrot_invariants_every_cycle():
+@pytest.mark.parametrize("ortho", ["cgs2", "cgs2g"])
+def test_rgcrot_invariants_every_cycle(ortho):
     """Eq. (4) V _|_ C, eq. (5) A_hat V_m = C B + V_{m+1} H_, Arnoldi
     orthonormality, A_hat U = C and C^T C = I after line 14a,
-    residual _|_ C after each cycle (D20), monotone true residual."""
+    residual _|_ C after each cycle (D20), monotone true residual -- for CGS2
+    (D8) and the Gram-corrected CGS2 (R19).  (The paper's MGS keeps V _|_ C
+    only to ~1e-9 here; it is compared in test_rgcrot_mgs_and_cgs2_agree.)"""
     w = get_workload("c2s")
     prob = w.problem()
     op, pc, _ = _setup(prob)
-    prm = w.params
+    prm = replace(w.params, ortho=ortho)
     U = np.zeros((op.N, 0))
     C = np.zeros((op.N, 0))
     Anorm = np.abs(to_dense(op)).sum(axis=1).max()
@@ -404,3 +407,21 @@ def test_hybrid_refresh_on_epoch_policy():
     assert all(r.outcome == CONVERGED for _, _, r in out)
     every = run_sequence(w, refresh_every=2)
     assert [t for t, _, _ in every] == ["rgcrot"] * 3 + ["rbicgstab", "rgcrot"] * 3
+
+
+def test_cgs2g_equals_cgs2_coefficients():
+    """R19: the Gram-corrected coefficients (2I - G) Q^T w equal CGS2's
+    g1 + g2 = Q^T w + Q^T (w - Q Q^T w) in exact arithmetic; on a basis whose
+    orthogonality is perturbed at 1e-9 they agree to O(1e-17) relative
+    (second order in the perturbation), and both leave w orthogonal to Q."""
+    rng = np.random.default_rng(6)
+    N, n = 400, 12
+    Q = _orth(rng.standard_normal((N, n)))
+    Q = Q + 1e-9 * rng.standard_normal((N, n))
+    w = rng.standard_normal(N)
+    g1 = Q.T @ w
+    g2 = Q.T @ (w - Q @ g1)
+    h = 2.0 * g1 - (Q.T @ Q) @ g1
+    assert np.linalg.norm(h - (g1 + g2)) <= 1e-15 * np.linalg.norm(g1)
+    wg = w - Q @ h
+    assert np.linalg.norm(Q.T @ wg) <= 1e-14 * np.linalg.norm(w)
