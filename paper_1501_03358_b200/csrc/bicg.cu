@@ -12,8 +12,19 @@ template <int VEC>
 __global__ void __launch_bounds__(256) bicg_p_kernel(const double* __restrict__ r, double* __restrict__ p,
                                                      const double* __restrict__ v, const double* __restrict__ D,
                                                      double* __restrict__ z, double wl, int64_t N,
-                                                     const BiIter* cur, const BiIter* prev, int first) {
+                                                     BiIter* cur, const BiIter* prev, int first,
+                                                     double thr_conv, double thr_div) {
   RK_PDL_ENTRY();
+  // lookahead gate: every CTA takes the same decision from the records
+  // written by the previous iteration (flag, sigma) and its bicg_xr (rho, rr)
+  bool stop = false;
+  if (!first) {
+    const double rn2 = sqrt(cur->rr);
+    stop = prev->flag != 0.0 || prev->sigma == 0.0 || !(rn2 > thr_conv) || cur->rho == 0.0 ||
+           !(rn2 <= thr_div);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) cur->stop = stop ? 1.0 : 0.0;
+  if (stop) return;
   double beta = 0.0, omega = 0.0;
   if (!first) {
     const double alpha = prev->rho / prev->sigma;
@@ -53,6 +64,7 @@ __global__ void __launch_bounds__(256) bicg_s_kernel(const double* __restrict__ 
                                                      double* __restrict__ z, double wl, int64_t N,
                                                      const BiIter* cur, RedArgs ra) {
   RK_PDL_ENTRY();
+  RK_GATE(ra.gate);
   const double alpha = cur->rho / cur->sigma;
   double acc[1] = {0.0};
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -91,6 +103,7 @@ __global__ void __launch_bounds__(256) bicg_xr_kernel(double* __restrict__ x, do
                                                       double* xi, const double* eta1, const double* eta2,
                                                       int k, RedArgs ra) {
   RK_PDL_ENTRY();
+  RK_GATE(ra.gate);
   const double alpha = cur->rho / cur->sigma;
   const double omega = cur->ts / cur->tt;
   int mode;  // 0 full update, 1 exact exit, 2 breakdown (no update)
@@ -153,15 +166,17 @@ __global__ void bicg_setup_kernel(double* xi, const double* eta0, int k, BiIter*
 
 // =================================================================== host
 void bicg_p(rk_op* op, const double* r, double* p, const double* v, double* z, double wl,
-            bool jacobi, const BiIter* cur, const BiIter* prev, int first) {
+            bool jacobi, BiIter* cur, const BiIter* prev, int first, double thr_conv, double thr_div) {
   rk_ctx* ctx = op->ctx;
   const double* D = jacobi ? op->invd() : nullptr;   // 1 / D
   const int vec = pick_vec(op->N, {r, p, v, z, D});
   Launch L(ctx, "bicg_p", 8.0 * op->N * ((first ? 3 : 5) + (jacobi ? 1 : 0)));
   if (vec == 2)
-    launch_k(ctx, bicg_p_kernel<2>, op->N / 2, dim3(256), r, p, v, D, z, wl, op->N, cur, prev, first);
+    launch_k(ctx, bicg_p_kernel<2>, op->N / 2, dim3(256), r, p, v, D, z, wl, op->N, cur, prev, first,
+             thr_conv, thr_div);
   else
-    launch_k(ctx, bicg_p_kernel<1>, op->N, dim3(256), r, p, v, D, z, wl, op->N, cur, prev, first);
+    launch_k(ctx, bicg_p_kernel<1>, op->N, dim3(256), r, p, v, D, z, wl, op->N, cur, prev, first,
+             thr_conv, thr_div);
   L.done();
 }
 

@@ -12,6 +12,7 @@ template <int NC, int VEC>
 __global__ void __launch_bounds__(256) bdot_kernel(ColPtrs Q, int ncol, const double* __restrict__ w,
                                                    int64_t N, RedArgs ra) {
   RK_PDL_ENTRY();
+  RK_GATE(ra.gate);
   double acc[NC];
 #pragma unroll
   for (int c = 0; c < NC; ++c) acc[c] = 0.0;
@@ -45,6 +46,7 @@ __global__ void __launch_bounds__(256) bupd_kernel(ColPtrs Q, int ncol, const do
                                                    const double* d0, const double* d1,
                                                    const double* d2, RedArgs ra) {
   RK_PDL_ENTRY();
+  RK_GATE(ra.gate);
   __shared__ double gsh[NC];
   for (int c = threadIdx.x; c < NC; c += blockDim.x) gsh[c] = c < ncol ? gs * g[c] : 0.0;
   __syncthreads();
@@ -106,6 +108,7 @@ template <int NC, int BT>
 __global__ void __launch_bounds__(BT) bdot_tile_kernel(ColPtrs Q, int ncol, const double* __restrict__ w,
                                                         int64_t N, RedArgs ra) {
   RK_PDL_ENTRY();
+  RK_GATE(ra.gate);
   constexpr int RV = DRV, G = DG, TILE_ROWS = 2 * BT * DRV;
   double acc[NC];
 #pragma unroll
@@ -307,6 +310,7 @@ __global__ void __launch_bounds__(256) bupd_tile_kernel(ColPtrs Q, int ncol, con
                                                         const double* d0, const double* d1,
                                                         const double* d2, RedArgs ra) {
   RK_PDL_ENTRY();
+  RK_GATE(ra.gate);
   constexpr int RV = TRV, G = TG;
   __shared__ double gsh[NC];
   for (int c = threadIdx.x; c < NC; c += blockDim.x) gsh[c] = c < ncol ? gs * g[c] : 0.0;
@@ -587,6 +591,7 @@ void bupd(rk_ctx* ctx, const std::vector<const double*>& cols, const double* g, 
   const int vec = pick_vec(N, {w, nd > 0 ? dots[0] : nullptr, nd > 1 ? dots[1] : nullptr,
                                nd > 2 ? dots[2] : nullptr}, cols);
   RedArgs ra = nd ? red_args(ctx, red_out) : RedArgs{nullptr, nullptr, nullptr};
+  ra.gate = ctx->gate;
   ColPtrs Q = make_cols_padded(cols, nc);
   const double* d[3] = {nullptr, nullptr, nullptr};
   for (int q = 0; q < nd; ++q) d[q] = dots[q];

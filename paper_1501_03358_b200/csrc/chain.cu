@@ -261,6 +261,7 @@ __global__ void __launch_bounds__((TX + 2 * (NST - 1)) * (TY + 2 * (NST - 1)), 1
 chain_kernel(const __grid_constant__ CUtensorMap map_b, const __grid_constant__ CUtensorMap map_r,
              const __grid_constant__ CUtensorMap map_x, ChainParams cp) {
   RK_PDL_ENTRY();
+  RK_GATE(cp.gate);
   using G = ChainGeom<ST, NST, TX, TY, PD>;
   constexpr int HALO = G::HALO, EX = G::EX, XX = G::XX, NXB = G::NXB, NB = G::NB;
   constexpr int SX = G::SX, PADB = G::PADB, PADX = G::PADX;
@@ -575,6 +576,7 @@ void chain_launch(rk_op* op, int nst, const int* kinds, const double* omegas, co
   for (int s = 0; s < nst; ++s) cp.omega[s] = omegas[s];
   cp.zb = zb;
   cp.zg0 = (int)op->g.z0;
+  cp.gate = ctx->gate;
   for (int s = 0; s < nst; ++s) cp.local[s] = local ? local[s] : 0;
   dim3 grid((unsigned)(op->g.nx / tc.tx), (unsigned)(op->g.ny / tc.ty), 1);   // z: launch_one
   // algorithmic bytes: bands once + stage-0 input + rhs (if any) + outputs (the

@@ -149,6 +149,7 @@ __global__ void __launch_bounds__((TX + 2 * (NST - 1)) * (TY + 2 * (NST - 1)) / 
 chain_kernel_x2(const __grid_constant__ CUtensorMap map_b, const __grid_constant__ CUtensorMap map_r,
                 const __grid_constant__ CUtensorMap map_x, ChainParams cp) {
   RK_PDL_ENTRY();
+  RK_GATE(cp.gate);
   using G = ChainGeom<ST, NST, TX, TY, PD>;
   constexpr int HALO = G::HALO, EX = G::EX, XX = G::XX, NXB = G::NXB, NB = G::NB;
   constexpr int SX = G::SX, PADB = G::PADB, PADX = G::PADX;

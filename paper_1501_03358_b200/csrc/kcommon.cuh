@@ -204,6 +204,7 @@ inline RedArgs red_args(rk_ctx* ctx, double* out) {
   ra.partials = ctx->partials;
   ra.counter = ctx->counter;
   ra.out = out;
+  ra.gate = ctx->gate;
   return ra;
 }
 

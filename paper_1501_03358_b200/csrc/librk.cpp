@@ -274,6 +274,8 @@ struct rk_solver {
   int max_it = 0;
   std::vector<std::array<double, 3>> history;
   rk_report last{};
+  cudaEvent_t bev[2] = {nullptr, nullptr};    // rBiCGStab lookahead: iteration records landed
+  bool lookahead = true;                      // RK_BICG_LOOKAHEAD=0 disables
 
   static constexpr size_t STEP = 2 * (MAXCOL + 1) + 2;  // g1[81] g2[81] nrm2 brk
   // misc slots
@@ -777,25 +779,31 @@ struct rk_solver {
       sync();
       double rr = hbi(0)->rr;
       const double r0n = std::sqrt(rr);
-      int i = 0;
-      int status = -1;
-      while (std::sqrt(rr) > tol * beta && rep.krylov_matvecs < cfg.max_matvecs) {  // line 3
-        RK_REQUIRE(i + 1 < max_it, RK_ESTATE, "rBiCGStab iteration record overflow");
-        BiIter* cur = bi(i);
-        if (hbi(i)->rho == 0.0) {                                  // line 5
-          status = RK_BREAKDOWN;
-          break;
-        }
+      const double thr_conv = tol * beta, thr_div = cfg.divergence_factor * r0n;
+      // One rBiCGStab iteration (lines 5-15) on the stream, ending with the
+      // copy of its scalar records to the host and an event.  Iteration j+1
+      // is enqueued before the host has read iteration j (lookahead): its
+      // bicg_p re-takes the host's stop decision on the device (line 3's
+      // test, line 5, the breakdown / exact-exit flags of j, [D17]) and, if
+      // it stops, every later kernel of j+1 returns at once (ctx->gate).
+      auto enqueue = [&](int j) {
+        struct GateReset {
+          rk_ctx* c;
+          ~GateReset() { c->gate = nullptr; }
+        } gate_reset{ctx};
+        BiIter* cur = bi(j);
+        const BiIter* prev = j ? bi(j - 1) : cur;
         // line 6 + p_hat = M^-1 p (right preconditioning) ; line 7: v = A p_hat
         if (jac()) {
-          bicg_p(op, r, p, v, za, wl, true, cur, i ? bi(i - 1) : cur, i == 0);
+          bicg_p(op, r, p, v, za, wl, true, cur, prev, j == 0, thr_conv, thr_div);
+          ctx->gate = j ? &cur->stop : nullptr;
           apply_right(p, ph, v);               // p_hat = M^-1 p ; v = A p_hat
         } else {
-          bicg_p(op, r, p, v, ph, 1.0, false, cur, i ? bi(i - 1) : cur, i == 0);
+          bicg_p(op, r, p, v, ph, 1.0, false, cur, prev, j == 0, thr_conv, thr_div);
+          ctx->gate = j ? &cur->stop : nullptr;
           if (ssor()) ssor_to(p, ph, nullptr);   // p_hat = M^-1 p (SSOR, R18)
           stencil(op, SM_SPMV, ph, nullptr, v, nullptr, 0.0, nullptr);
         }
-        rep.krylov_matvecs += 1;
         // line 7a: eta1 = C^T v ; v -= C eta1 ; sigma = r~^T v
         if (k > 0) {
           bdot(ctx, C, v, N, eta(0));
@@ -811,7 +819,6 @@ struct rk_solver {
           if (ssor()) ssor_to(s, sh, nullptr);
           stencil(op, SM_SPMV, sh, nullptr, tt, nullptr, 0.0, nullptr);
         }
-        rep.krylov_matvecs += 1;
         if (k > 0) {                                              // line 12a
           bdot(ctx, C, tt, N, eta(1));
           bupd(ctx, C, eta(1), 1.0, tt, N, {s, nullptr}, &cur->ts);
@@ -819,9 +826,28 @@ struct rk_solver {
           bdot(ctx, {s, tt}, tt, N, &cur->ts);
         }
         // lines 13-15 (+13a): omega ; x ; r ; xi ; next rho, ||r||^2
-        bicg_xr(ctx, x, r, s, tt, ph, sh, rtl, N, cur, bi(i + 1), xi, eta(0), eta(1), k);
-        fetch(o_bi + 8 * (size_t)i, 16);
-        sync();
+        bicg_xr(ctx, x, r, s, tt, ph, sh, rtl, N, cur, bi(j + 1), xi, eta(0), eta(1), k);
+        ctx->gate = nullptr;
+        fetch(o_bi + 8 * (size_t)j, 16);
+        RK_CUDA(cudaEventRecord(bev[j & 1], ctx->stream));
+      };
+      const int m0 = rep.krylov_matvecs;
+      int i = 0;
+      int queued = 0;   // iterations 0 .. queued-1 are on the stream
+      int status = -1;
+      while (std::sqrt(rr) > tol * beta && rep.krylov_matvecs < cfg.max_matvecs) {  // line 3
+        RK_REQUIRE(i + 1 < max_it, RK_ESTATE, "rBiCGStab iteration record overflow");
+        if (hbi(i)->rho == 0.0) {                                  // line 5
+          status = RK_BREAKDOWN;
+          break;
+        }
+        if (queued == i) enqueue(queued++);
+        // lookahead: iteration i+1 runs iff i ends normally, which spends
+        // exactly two matvecs per iteration
+        if (lookahead && queued == i + 1 && i + 2 < max_it && m0 + 2 * (i + 1) < cfg.max_matvecs)
+          enqueue(queued++);
+        RK_CUDA(cudaEventSynchronize(bev[i & 1]));
+        rep.krylov_matvecs += 2;
         const BiIter hc = *hbi(i);
         if (hc.sigma == 0.0) {
           rep.krylov_matvecs -= 1;   // the oracle stops before t = A s_hat
@@ -841,11 +867,13 @@ struct rk_solver {
         ++i;
         rr = hbi(i)->rr;
         record((double)rep.krylov_matvecs, std::numeric_limits<double>::quiet_NaN(), std::sqrt(rr));
-        if (!(std::sqrt(rr) <= cfg.divergence_factor * r0n)) {   // [D17] instability
+        if (!(std::sqrt(rr) <= thr_div)) {   // [D17] instability
           status = RK_UNSTABLE;
           break;
         }
       }
+      // a speculative iteration still on the stream gates itself off; the
+      // records of a stopped iteration are never read
       rep.cycles_or_iters += i;
       // line 17a: x = x - U xi
       if (k > 0) {
@@ -1158,12 +1186,16 @@ rk_status rk_solver_create(rk_op* op, const rk_config* cfg, rk_solver** out) {
       RK_CUDA(cudaMalloc(&s->dsc, o * sizeof(double)));
       RK_CUDA(cudaMemsetAsync(s->dsc, 0, o * sizeof(double), s->ctx->stream));
       RK_CUDA(cudaMallocHost(&s->hsc, o * sizeof(double)));
+      for (auto& e : s->bev) RK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      if (const char* la = std::getenv("RK_BICG_LOOKAHEAD")) s->lookahead = std::atoi(la) != 0;
       std::memset(s->hsc, 0, o * sizeof(double));
       RK_CUDA(cudaStreamSynchronize(s->ctx->stream));
     } catch (...) {
       for (auto b : s->bases) cudaFree(b);
       cudaFree(s->dsc);
       cudaFreeHost(s->hsc);
+      for (auto e : s->bev)
+        if (e) cudaEventDestroy(e);
       delete s;
       throw;
     }
@@ -1179,6 +1211,8 @@ void rk_solver_destroy(rk_solver* s) {
   cudaFree(s->bdev);
   cudaFree(s->dsc);
   cudaFreeHost(s->hsc);
+  for (auto e : s->bev)
+    if (e) cudaEventDestroy(e);
   delete s;
 }
 

@@ -52,6 +52,7 @@ struct RedArgs {
   double* out2 = nullptr;   // ... or, for q >= split, out2[q - split])
   int split = 1 << 30;
   int valid = 1 << 30;  // only values with (q mod split) < valid are stored
+  const double* gate = nullptr;   // kernel is a no-op when *gate != 0 (rBiCGStab lookahead)
 };
 
 // Stencil kernel modes (K1/K2 of SURVEY §2.4)
@@ -78,6 +79,7 @@ struct StencilParams {
   double omega;
   RedArgs red;
   int zb, zg0;          // local (block-Jacobi) sweep: z-block size in planes (0 = global), global z of plane 0
+  const double* gate;   // no-op when *gate != 0 (rBiCGStab lookahead)
 };
 
 struct LcOut {
@@ -107,6 +109,7 @@ struct ChainParams {
   int zc;               // z planes per CTA
   int zb, zg0;          // z-block size (0 = none) and global z of plane 0 (block-Jacobi)
   int local[3];         // stage s is a local sweep (no coupling across z-blocks)
+  const double* gate;   // no-op when *gate != 0 (rBiCGStab lookahead)
 };
 
 // Per-iteration device scalars of rBiCGStab (one 64-byte record per iteration).
@@ -118,7 +121,7 @@ struct BiIter {
   double ts;     // t_i^T s_i           (t projected)
   double tt;     // ||t_i||^2
   double flag;   // 0 normal, 1 exact exit (s = 0), 2 breakdown
-  double pad;
+  double stop;   // 1: this iteration is not run (set by its bicg_p; gates the rest)
 };
 
 }  // namespace rk
@@ -136,6 +139,7 @@ struct rk_ctx {
   bool pdl = true;              // programmatic dependent launch (env RK_NO_PDL: off)
   int pdl_mode = 3;             // RK_PDL_MODE (chain.cu): default 3 = the chain overlaps its predecessor, its successor does not
   bool pdl_skip_next = false;   // set by a chain launch (mode 2)
+  const double* gate = nullptr; // copied into the kernels launched while set (rBiCGStab lookahead)
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   double* partials = nullptr;
@@ -232,6 +236,11 @@ void launch_pdl_if(rk_ctx* ctx, bool allow, void (*kern)(KArgs...), dim3 grid, d
     asm volatile("griddepcontrol.wait;" ::: "memory");          \
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); \
   } while (0)
+// a gated kernel (the speculative next rBiCGStab iteration) returns at once
+#define RK_GATE(g)                        \
+  do {                                    \
+    if ((g) != nullptr && *(g) != 0.0) return; \
+  } while (0)
 
 template <typename... KArgs, typename... Args>
 void launch_pdl_if(rk_ctx* ctx, bool allow, void (*kern)(KArgs...), dim3 grid, dim3 blk,
@@ -296,8 +305,12 @@ void proj(rk_ctx* ctx, const std::vector<const double*>& C, const std::vector<co
 // [q_0 .. q_{k-1}] <- [q_0 .. q_{k-1}] T in place, T k x kout (column-major),
 // outputs into the first kout columns (kout = -1: square).
 void rotate(rk_ctx* ctx, const std::vector<double*>& cols, const double* T, int64_t N, int kout = -1);
+// also decides whether iteration `cur` runs at all (lookahead): it stops when
+// the previous iteration ended the loop (flag / sigma), converged
+// (||r|| <= thr_conv), diverged (||r|| > thr_div) or rho == 0; cur->stop gates
+// the rest of the iteration's kernels
 void bicg_p(rk_op* op, const double* r, double* p, const double* v, double* z, double wl,
-            bool jacobi, const BiIter* cur, const BiIter* prev, int first);
+            bool jacobi, BiIter* cur, const BiIter* prev, int first, double thr_conv, double thr_div);
 void bicg_s(rk_op* op, const double* r, const double* v, double* s, double* z, double wl,
             bool jacobi, BiIter* cur);
 void bicg_xr(rk_ctx* ctx, double* x, double* r, const double* s, const double* t, const double* ph,

@@ -17,6 +17,7 @@ namespace rk {
 template <int ST, int MODE, int VEC>
 __global__ void __launch_bounds__(256) stencil_kernel(StencilParams sp) {
   RK_PDL_ENTRY();
+  RK_GATE(sp.gate);
   constexpr bool RED = (MODE == SM_SWEEP_NORM || MODE == SM_RESID || MODE == SM_RESID_SWEEP1);
   const int BX = blockDim.x, BY = blockDim.y;
   const int tx = threadIdx.x, ty = threadIdx.y;
@@ -285,6 +286,7 @@ void stencil(rk_op* op, int mode, const double* x, const double* r, double* out0
   sp.omega = omega;
   sp.zb = zb;
   sp.zg0 = (int)op->g.z0;
+  sp.gate = ctx->gate;
   const bool red = (mode == SM_SWEEP_NORM || mode == SM_RESID || mode == SM_RESID_SWEEP1);
   sp.red = red ? red_args(ctx, red_out) : RedArgs{nullptr, nullptr, nullptr};
   // VEC = 2 needs even rows and 16-byte aligned rows of every array
@@ -314,6 +316,7 @@ void stencil(rk_op* op, int mode, const double* x, const double* r, double* out0
 template <int ST>
 __global__ void __launch_bounds__(256) colour_sweep_kernel(StencilParams sp, int colour) {
   RK_PDL_ENTRY();
+  RK_GATE(sp.gate);
   const int ci = colour & 1, cj = (colour >> 1) & 1, ck = (colour >> 2) & 1;
   const int hx = (sp.nx - ci + 1) / 2;                 // cells of parity ci in a row
   const int hy = (sp.ny - cj + 1) / 2;
@@ -366,6 +369,7 @@ void colour_sweep(rk_op* op, double* z, const double* r, double omega, int colou
   sp.r = r;
   sp.omega = omega;
   sp.zg0 = (int)op->g.z0;
+  sp.gate = ctx->gate;
   const int64_t cells = (op->N + 7) / 8;
   Launch L(ctx, "ssor_colour", 8.0 * op->N * (op->S + 4) / 8.0);
   switch (op->S) {
