@@ -156,6 +156,123 @@ __global__ void __launch_bounds__(BT) bdot_tile_kernel(ColPtrs Q, int ncol, cons
   block_reduce_store<NC>(acc, ncol, ra);
 }
 
+// Bulk-copy-fed variant of bdot_tile_kernel (same column-chunk order and
+// summation order per thread, one CTA per SM): the w rows and column chunks
+// of a CTA's 2048-row tiles stream through a ring of BS shared-memory slots
+// of 16 KB filled by 1-D cp.async.bulk, so the bytes in flight per SM are set
+// by the ring (128 KB), not by the register budget that caps the tile
+// kernel at 2 CTAs/SM (read-only streaming needs ~128 KB in flight per SM to
+// reach the HBM ceiling; scripts/micro/read_bw.cu).
+namespace {
+__device__ __forceinline__ uint32_t bk_smem(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ bool bk_try(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(bk_smem(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+}  // namespace
+
+constexpr int BK_ROWS = 2048, BK_SLOTS = 8, BK_BYTES = BK_ROWS * 8;
+constexpr size_t BK_SMEM = (size_t)BK_SLOTS * BK_BYTES + BK_SLOTS * sizeof(uint64_t);
+
+template <int NC>
+__global__ void __launch_bounds__(256, 1) bdot_bulk_kernel(ColPtrs Q, int ncol, const double* __restrict__ w,
+                                                           int64_t N, RedArgs ra) {
+  RK_PDL_ENTRY();
+  RK_GATE(ra.gate);
+  extern __shared__ __align__(128) unsigned char bk_sm[];
+  double2* ring = reinterpret_cast<double2*>(bk_sm);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(bk_sm + (size_t)BK_SLOTS * BK_BYTES);
+  double acc[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) acc[c] = 0.0;
+  const int64_t ntile = N / BK_ROWS;
+  const int64_t mytiles = ntile > blockIdx.x ? (ntile - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int per = ncol + 1;                         // items per tile: w, Q_0 .. Q_{ncol-1}
+  const int64_t nitem = mytiles * per;
+  // item -> source: tile blockIdx.x + (it / per) * gridDim.x, column it % per - 1 (-1: w)
+  auto issue = [&](int64_t it, int slot) {
+    const int64_t lt = it / per;
+    const int c = (int)(it - lt * per) - 1;
+    const int64_t row = (blockIdx.x + lt * gridDim.x) * BK_ROWS;
+    const double* src = (c < 0 ? w : Q.p[c]) + row;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bk_smem(bar + slot)),
+                 "r"(BK_BYTES)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            bk_smem(ring + (size_t)slot * (BK_ROWS / 2))),
+        "l"(src), "r"(BK_BYTES), "r"(bk_smem(bar + slot))
+        : "memory");
+  };
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < BK_SLOTS; ++q)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bk_smem(bar + q)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int q = 0; q < BK_SLOTS && q < nitem; ++q) issue(q, q);
+  }
+  __syncthreads();
+  int slot = 0;
+  uint32_t phase = 0;
+  int64_t it = 0;
+  // consume item `it` in `slot`; refill the slot with item it + BK_SLOTS
+  auto next = [&]() {
+    __syncthreads();   // every thread is done with the slot
+    if (threadIdx.x == 0 && it + BK_SLOTS < nitem) issue(it + BK_SLOTS, slot);
+    ++it;
+    if (++slot == BK_SLOTS) {
+      slot = 0;
+      phase ^= 1;
+    }
+  };
+#pragma unroll 1
+  for (int64_t lt = 0; lt < mytiles; ++lt) {
+    while (!bk_try(bar + slot, phase)) {
+    }
+    double2 wv[BK_ROWS / 512];
+    const double2* sl = ring + (size_t)slot * (BK_ROWS / 2);
+#pragma unroll
+    for (int v = 0; v < BK_ROWS / 512; ++v) wv[v] = sl[threadIdx.x + 256 * v];
+    next();
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      if (c < ncol) {
+        while (!bk_try(bar + slot, phase)) {
+        }
+        const double2* qs = ring + (size_t)slot * (BK_ROWS / 2);
+#pragma unroll
+        for (int v = 0; v < BK_ROWS / 512; ++v) {
+          const double2 q = qs[threadIdx.x + 256 * v];
+          acc[c] = fma(q.x, wv[v].x, acc[c]);
+          acc[c] = fma(q.y, wv[v].y, acc[c]);
+        }
+        next();
+      }
+    }
+  }
+  // tail rows (N even)
+  for (int64_t r = ntile * BK_ROWS + 2 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x); r < N;
+       r += 2 * (int64_t)gridDim.x * blockDim.x) {
+    const Vec<2> wt = ldv_ro<2>(w + r);
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+      if (c < ncol) {
+        const Vec<2> a = ldv_stream<2>(Q.p[c] + r);
+        acc[c] = fma(a.v[0], wt.v[0], acc[c]);
+        acc[c] = fma(a.v[1], wt.v[1], acc[c]);
+      }
+  }
+  block_reduce_store<NC>(acc, ncol, ra);
+}
+
 // Two right-hand sides: [Q^T w, Q^T v] in one read of Q (the Gram-corrected
 // CGS2 of reading R19 needs Q_j^T v_j, the lagged Gram row of the newest basis
 // vector, next to the projection coefficients Q_j^T w).  Values 0..NC-1 go to
@@ -549,6 +666,18 @@ __global__ void __launch_bounds__(256) rotate_kernel(ColPtrs Qc, int k, int kout
 
 
 // =================================================================== host
+namespace {
+// one CTA per SM (the ring fills the shared memory), grid = #SMs
+template <typename... KArgs, typename... Args>
+void launch_bulk(rk_ctx* ctx, void (*kern)(KArgs...), Args&&... args) {
+  auto it = ctx->occ_cache.find((const void*)kern);
+  if (it == ctx->occ_cache.end()) {
+    RK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BK_SMEM));
+    ctx->occ_cache[(const void*)kern] = 1;
+  }
+  launch_pdl(ctx, kern, dim3(ctx->sms), dim3(256), BK_SMEM, std::forward<Args>(args)...);
+}
+}  // namespace
 // bdot launches cover <= 40 columns each (register budget: 40 accumulators).
 void bdot(rk_ctx* ctx, const std::vector<const double*>& cols_all, const double* w, int64_t N,
           double* out) {
@@ -564,8 +693,15 @@ void bdot(rk_ctx* ctx, const std::vector<const double*>& cols_all, const double*
     ColPtrs Q = make_cols_padded(cols, nc);
     const int64_t work = N / vec;
     Launch L(ctx, "bdot", 8.0 * N * (ncol + 1));
+    // bulk-copy path: 16-byte aligned columns and even N (vec == 2), a tile per
+    // SM, >= 4 columns (measured at N = 2^21: equal to the register-tile
+    // kernel at 20 columns, -5 % at 8, -17 % at 40; slower for 1-2 columns)
+    const bool bulk = vec == 2 && (ctx->bdot_bulk == 2 ||
+                                   (ctx->bdot_bulk == 1 && ncol >= 4 && N >= (int64_t)BK_ROWS * ctx->sms));
 #define RK_BDOT(NCV)                                                                          \
-  if (vec == 2)                                                                                     \
+  if (bulk)                                                                                         \
+    launch_bulk(ctx, bdot_bulk_kernel<NCV>, Q, ncol, w, N, ra);                                     \
+  else if (vec == 2)                                                                                \
     launch_k(ctx, bdot_tile_kernel<NCV, 256>, work / DRV, dim3(256), Q, ncol, w, N, ra);            \
   else launch_k(ctx, bdot_kernel<NCV, 1>, work, dim3(256), Q, ncol, w, N, ra);
     switch (nc) {

@@ -140,6 +140,7 @@ struct rk_ctx {
   int pdl_mode = 3;             // RK_PDL_MODE (chain.cu): default 3 = the chain overlaps its predecessor, its successor does not
   bool pdl_skip_next = false;   // set by a chain launch (mode 2)
   const double* gate = nullptr; // copied into the kernels launched while set (rBiCGStab lookahead)
+  int bdot_bulk = 1;             // bulk-copy-fed bdot: 0 off, 1 large N, 2 always (RK_BDOT_BULK)
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   double* partials = nullptr;

@@ -416,6 +416,27 @@ def test_sequence_parity_fused_chain(rk, ctx, monkeypatch):
     compare_sequences(w, gpu, ora, w.params.method)
 
 
+@pytest.mark.parametrize("name", ["c3m", "c2s"])
+def test_sequence_parity_bulk_bdot(rk, name, monkeypatch):
+    """Every block dot product through the bulk-copy-fed kernel (forced
+    below its size threshold: CTAs without a whole 2048-row tile, the ragged
+    tail rows by direct loads), hybrid / rGCROT sequence vs the oracle, and
+    two runs bit-identical (the shared-memory ring is mbarrier ordered)."""
+    w = get_workload(name)
+    ora = run_sequence(w)
+    monkeypatch.setenv("RK_BDOT_BULK", "2")
+    c = rk.Context(0)
+    try:
+        a, _ = gpu_sequence(rk, c, w)
+        b, _ = gpu_sequence(rk, c, w)
+    finally:
+        c.close()
+    compare_sequences(w, a, ora, w.params.method)
+    for (ra, xa), (rb, xb) in zip(a, b):
+        assert np.array_equal(xa, xb)
+        assert ra["krylov_matvecs"] == rb["krylov_matvecs"]
+
+
 def test_gmres_stagnation_parity(rk, ctx):
     """GMRES(12) stagnates on the shrunken channel (PAPER P:782-784 reports
     GMRES(m < 50) stagnation on the channel): both sides exhaust the 2000
