@@ -421,16 +421,58 @@ __global__ void __launch_bounds__(256) bupd_gram_kernel(ColPtrs Q, int ncol, int
   block_reduce_store<1>(acc, 1, ra);
 }
 
+// g_c = sum_b part[c G + b] for c < ncol, in a fixed order that every CTA
+// repeats: thread t sums partials t, t + 256, ..., a warp shuffle tree, then
+// the 8 warp sums in order.  gsh[c] = gs g_c; CTA 0 stores g_c.
+template <int NC>
+__device__ __forceinline__ void coef_from_partials(const CoefIn& cin, int ncol, double gs, double* gsh) {
+  __shared__ double wsum[NC][8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int c0 = 0; c0 < NC; c0 += 8) {
+    if (c0 < ncol) {
+      double a[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a[u] = 0.0;
+      for (int b = threadIdx.x; b < cin.G; b += 256) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (c0 + u < ncol) a[u] += __ldcg(cin.part + (int64_t)(c0 + u) * cin.G + b);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) a[u] += __shfl_down_sync(0xffffffffu, a[u], o);
+        if (lane == 0) wsum[c0 + u][warp] = a[u];
+      }
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < NC; c += blockDim.x) {
+    double s = 0.0;
+    if (c < ncol) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) s += wsum[c][q];
+      if (blockIdx.x == 0) cin.store[c] = s;
+    }
+    gsh[c] = c < ncol ? gs * s : 0.0;
+  }
+}
+
 template <int NC, int ND>
 __global__ void __launch_bounds__(256) bupd_tile_kernel(ColPtrs Q, int ncol, const double* __restrict__ g,
                                                         double gs, double* __restrict__ w, int64_t N,
                                                         const double* d0, const double* d1,
-                                                        const double* d2, RedArgs ra) {
+                                                        const double* d2, RedArgs ra, CoefIn cin) {
   RK_PDL_ENTRY();
   RK_GATE(ra.gate);
   constexpr int RV = TRV, G = TG;
   __shared__ double gsh[NC];
-  for (int c = threadIdx.x; c < NC; c += blockDim.x) gsh[c] = c < ncol ? gs * g[c] : 0.0;
+  if (cin.part) {
+    coef_from_partials<NC>(cin, ncol, gs, gsh);
+  } else {
+    for (int c = threadIdx.x; c < NC; c += blockDim.x) gsh[c] = c < ncol ? gs * g[c] : 0.0;
+  }
   __syncthreads();
   // volatile: re-read per group instead of hoisting NC coefficients into
   // registers for the whole tile loop (which cost occupancy)
@@ -669,15 +711,48 @@ __global__ void __launch_bounds__(256) rotate_kernel(ColPtrs Qc, int k, int kout
 namespace {
 // one CTA per SM (the ring fills the shared memory), grid = #SMs
 template <typename... KArgs, typename... Args>
-void launch_bulk(rk_ctx* ctx, void (*kern)(KArgs...), Args&&... args) {
+int launch_bulk(rk_ctx* ctx, void (*kern)(KArgs...), Args&&... args) {
   auto it = ctx->occ_cache.find((const void*)kern);
   if (it == ctx->occ_cache.end()) {
     RK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BK_SMEM));
     ctx->occ_cache[(const void*)kern] = 1;
   }
   launch_pdl(ctx, kern, dim3(ctx->sms), dim3(256), BK_SMEM, std::forward<Args>(args)...);
+  return ctx->sms;
 }
 }  // namespace
+// One block-dot launch over <= 40 columns; returns its grid (the number of
+// per-CTA partials of every value).
+static int bdot_launch(rk_ctx* ctx, const std::vector<const double*>& cols, const double* w,
+                       int64_t N, RedArgs ra) {
+  const int ncol = (int)cols.size();
+  const int nc = nc_round(ncol);
+  const int vec = pick_vec(N, {w}, cols);
+  ColPtrs Q = make_cols_padded(cols, nc);
+  const int64_t work = N / vec;
+  // bulk-copy path: 16-byte aligned columns and even N (vec == 2), a tile per
+  // SM, >= 4 columns (measured at N = 2^21: equal to the register-tile
+  // kernel at 20 columns, -5 % at 8, -17 % at 40; slower for 1-2 columns)
+  const bool bulk = vec == 2 && (ctx->bdot_bulk == 2 ||
+                                 (ctx->bdot_bulk == 1 && ncol >= 4 && N >= (int64_t)BK_ROWS * ctx->sms));
+  int grid = 0;
+#define RK_BDOT(NCV)                                                                          \
+  if (bulk)                                                                                         \
+    grid = launch_bulk(ctx, bdot_bulk_kernel<NCV>, Q, ncol, w, N, ra);                              \
+  else if (vec == 2)                                                                                \
+    grid = launch_k(ctx, bdot_tile_kernel<NCV, 256>, work / DRV, dim3(256), Q, ncol, w, N, ra);     \
+  else grid = launch_k(ctx, bdot_kernel<NCV, 1>, work, dim3(256), Q, ncol, w, N, ra);
+  switch (nc) {
+    case 8: RK_BDOT(8); break;
+    case 16: RK_BDOT(16); break;
+    case 24: RK_BDOT(24); break;
+    case 32: RK_BDOT(32); break;
+    default: RK_BDOT(40); break;
+  }
+#undef RK_BDOT
+  return grid;
+}
+
 // bdot launches cover <= 40 columns each (register budget: 40 accumulators).
 void bdot(rk_ctx* ctx, const std::vector<const double*>& cols_all, const double* w, int64_t N,
           double* out) {
@@ -687,38 +762,40 @@ void bdot(rk_ctx* ctx, const std::vector<const double*>& cols_all, const double*
     std::vector<const double*> cols(cols_all.begin() + off,
                                     cols_all.begin() + std::min(total, off + 40));
     const int ncol = (int)cols.size();
-    const int nc = nc_round(ncol);
-    const int vec = pick_vec(N, {w}, cols);
-    RedArgs ra = red_args(ctx, out + off);
-    ColPtrs Q = make_cols_padded(cols, nc);
-    const int64_t work = N / vec;
     Launch L(ctx, "bdot", 8.0 * N * (ncol + 1));
-    // bulk-copy path: 16-byte aligned columns and even N (vec == 2), a tile per
-    // SM, >= 4 columns (measured at N = 2^21: equal to the register-tile
-    // kernel at 20 columns, -5 % at 8, -17 % at 40; slower for 1-2 columns)
-    const bool bulk = vec == 2 && (ctx->bdot_bulk == 2 ||
-                                   (ctx->bdot_bulk == 1 && ncol >= 4 && N >= (int64_t)BK_ROWS * ctx->sms));
-#define RK_BDOT(NCV)                                                                          \
-  if (bulk)                                                                                         \
-    launch_bulk(ctx, bdot_bulk_kernel<NCV>, Q, ncol, w, N, ra);                                     \
-  else if (vec == 2)                                                                                \
-    launch_k(ctx, bdot_tile_kernel<NCV, 256>, work / DRV, dim3(256), Q, ncol, w, N, ra);            \
-  else launch_k(ctx, bdot_kernel<NCV, 1>, work, dim3(256), Q, ncol, w, N, ra);
-    switch (nc) {
-      case 8: RK_BDOT(8); break;
-      case 16: RK_BDOT(16); break;
-      case 24: RK_BDOT(24); break;
-      case 32: RK_BDOT(32); break;
-      default: RK_BDOT(40); break;
-    }
-#undef RK_BDOT
+    bdot_launch(ctx, cols, w, N, red_args(ctx, out + off));
     L.done();
     allreduce(ctx, out + off, ncol);
   }
 }
 
+void bproject(rk_ctx* ctx, const std::vector<const double*>& cols, double* w, int64_t N,
+              double* eta, const std::vector<const double*>& dots, double* red_out) {
+  const int ncol = (int)cols.size();
+  const int nd = (int)dots.size();
+  const bool defer = ctx->defer_coef && ctx->nranks == 1 && ncol >= 1 && ncol <= 40 && nd <= 3 &&
+                     pick_vec(N, {w, nd > 0 ? dots[0] : nullptr, nd > 1 ? dots[1] : nullptr,
+                                  nd > 2 ? dots[2] : nullptr}, cols) == 2;
+  if (!defer) {
+    bdot(ctx, cols, w, N, eta);
+    bupd(ctx, cols, eta, 1.0, w, N, dots, red_out);
+    return;
+  }
+  RedArgs ra = red_args(ctx, nullptr);
+  ra.partials = ctx->dpartials;
+  ra.defer = 1;
+  Launch L(ctx, "bdot", 8.0 * N * (ncol + 1));
+  CoefIn cin;
+  cin.G = bdot_launch(ctx, cols, w, N, ra);
+  L.done();
+  cin.part = ctx->dpartials;
+  cin.store = eta;
+  bupd(ctx, cols, eta, 1.0, w, N, dots, red_out, cin);
+}
+
 void bupd(rk_ctx* ctx, const std::vector<const double*>& cols, const double* g, double gscale,
-          double* w, int64_t N, const std::vector<const double*>& dots, double* red_out) {
+          double* w, int64_t N, const std::vector<const double*>& dots, double* red_out,
+          CoefIn cin) {
   const int ncol = (int)cols.size();
   const int nd = (int)dots.size();
   RK_REQUIRE(nd <= 3, RK_EINVAL, "bupd: at most 3 dots");
@@ -728,6 +805,7 @@ void bupd(rk_ctx* ctx, const std::vector<const double*>& cols, const double* g, 
                                nd > 2 ? dots[2] : nullptr}, cols);
   RedArgs ra = nd ? red_args(ctx, red_out) : RedArgs{nullptr, nullptr, nullptr};
   ra.gate = ctx->gate;
+  RK_REQUIRE(!cin.part || (vec == 2 && nc <= 40), RK_ESTATE, "deferred coefficients need the tiled update");
   ColPtrs Q = make_cols_padded(cols, nc);
   const double* d[3] = {nullptr, nullptr, nullptr};
   for (int q = 0; q < nd; ++q) d[q] = dots[q];
@@ -738,7 +816,7 @@ void bupd(rk_ctx* ctx, const std::vector<const double*>& cols, const double* g, 
 #define RK_BUPD(NCV, NDV)                                                                      \
   if (vec == 2)                                                                                \
     launch_k(ctx, bupd_tile_kernel<NCV, NDV>, work / TRV, dim3(256), Q, ncol, g, gscale, w, N,  \
-             d[0], d[1], d[2], ra);                                                            \
+             d[0], d[1], d[2], ra, cin);                                                       \
   else                                                                                         \
     launch_k(ctx, bupd_kernel<NCV, NDV, 1>, work, dim3(256), Q, ncol, g, gscale, w, N, d[0],   \
              d[1], d[2], ra);

@@ -133,6 +133,7 @@ __device__ __forceinline__ void block_reduce_store(const double (&v)[NV], int nv
     for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
     if (lane == 0) ra.partials[(int64_t)q * G + blockIdx.x] = s;
   }
+  if (ra.defer) return;   // the consuming kernel sums the partials (CoefIn)
 #ifdef RK_EXP_NO_FINAL   // experiment only: per-CTA partials, no cross-CTA finalisation
   return;
 #endif
@@ -220,8 +221,8 @@ namespace {
 
 // Grid = min(work / CTA, SMs x resident CTAs of this instantiation).
 template <typename... KArgs, typename... Args>
-void launch_k(rk_ctx* ctx, void (*kern)(KArgs...), int64_t work_threads, dim3 blk,
-              Args&&... args) {
+int launch_k(rk_ctx* ctx, void (*kern)(KArgs...), int64_t work_threads, dim3 blk,
+             Args&&... args) {
   const int threads = (int)(blk.x * blk.y);
   auto it = ctx->occ_cache.find((const void*)kern);
   int occ;
@@ -235,6 +236,7 @@ void launch_k(rk_ctx* ctx, void (*kern)(KArgs...), int64_t work_threads, dim3 bl
   const int64_t want = std::max<int64_t>(1, (work_threads + threads - 1) / threads);
   const int grid = (int)std::min<int64_t>(want, (int64_t)ctx->sms * occ);
   launch_pdl(ctx, kern, dim3(grid), blk, 0, std::forward<Args>(args)...);
+  return grid;
 }
 
 inline RedArgs red_args(rk_ctx* ctx, double* out) {

@@ -565,8 +565,7 @@ struct rk_solver {
         } else {
           bdot(ctx, Qw, w, N, g1);                            // lines 6a-9, CGS pass 1 (+ ||w||^2)
           bupd(ctx, Q, g1, 1.0, w, N, {}, nullptr);
-          bdot(ctx, Q, w, N, g2);                             // CGS pass 2 [D8]
-          bupd(ctx, Q, g2, 1.0, w, N, {nullptr}, g1 + 2 * (MAXCOL + 1));
+          bproject(ctx, Q, w, N, g2, {nullptr}, g1 + 2 * (MAXCOL + 1));   // CGS pass 2 [D8]
         }
         normalize(ctx, w, N, g1 + 2 * (MAXCOL + 1), g1 + ncol, g1 + 2 * (MAXCOL + 1) + 1);  // line 10
       }
@@ -806,8 +805,7 @@ struct rk_solver {
         }
         // line 7a: eta1 = C^T v ; v -= C eta1 ; sigma = r~^T v
         if (k > 0) {
-          bdot(ctx, C, v, N, eta(0));
-          bupd(ctx, C, eta(0), 1.0, v, N, {rtl}, &cur->sigma);
+          bproject(ctx, C, v, N, eta(0), {rtl}, &cur->sigma);
         } else {
           bdot(ctx, {rtl}, v, N, &cur->sigma);
         }
@@ -820,8 +818,7 @@ struct rk_solver {
           stencil(op, SM_SPMV, sh, nullptr, tt, nullptr, 0.0, nullptr);
         }
         if (k > 0) {                                              // line 12a
-          bdot(ctx, C, tt, N, eta(1));
-          bupd(ctx, C, eta(1), 1.0, tt, N, {s, nullptr}, &cur->ts);
+          bproject(ctx, C, tt, N, eta(1), {s, nullptr}, &cur->ts);
         } else {
           bdot(ctx, {s, tt}, tt, N, &cur->ts);
         }
@@ -985,6 +982,7 @@ void rk_ctx_destroy(rk_ctx* c) {
   }
   for (auto e : c->pool) cudaEventDestroy(e);
   cudaFree(c->partials);
+  cudaFree(c->dpartials);
   cudaFree(c->counter);
 #ifdef RK_WITH_NCCL
   if (c->comm) ncclCommDestroy(c->comm);

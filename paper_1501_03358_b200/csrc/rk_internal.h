@@ -53,6 +53,16 @@ struct RedArgs {
   int split = 1 << 30;
   int valid = 1 << 30;  // only values with (q mod split) < valid are stored
   const double* gate = nullptr;   // kernel is a no-op when *gate != 0 (rBiCGStab lookahead)
+  int defer = 0;                  // 1: store the per-CTA partials only (the consumer sums them)
+};
+
+// Block-update coefficients still as per-CTA partials of a deferred block dot
+// (part[c * G + b], b < G); every CTA of the consumer sums them in the same
+// fixed order and CTA 0 stores the sums to `store`.
+struct CoefIn {
+  const double* part = nullptr;
+  int G = 0;
+  double* store = nullptr;
 };
 
 // Stencil kernel modes (K1/K2 of SURVEY §2.4)
@@ -140,10 +150,12 @@ struct rk_ctx {
   int pdl_mode = 3;             // RK_PDL_MODE (chain.cu): default 3 = the chain overlaps its predecessor, its successor does not
   bool pdl_skip_next = false;   // set by a chain launch (mode 2)
   const double* gate = nullptr; // copied into the kernels launched while set (rBiCGStab lookahead)
+  bool defer_coef = true;        // bproject: deferred block-dot finalisation (RK_DEFER_COEF=0: off)
   int bdot_bulk = 1;             // bulk-copy-fed bdot: 0 off, 1 large N, 2 always (RK_BDOT_BULK)
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   double* partials = nullptr;
+  double* dpartials = nullptr;  // deferred block-dot partials (read by the next kernel)
   size_t partials_cap = 0;      // doubles
   unsigned* counter = nullptr;
   int64_t launches = 0;
@@ -290,7 +302,14 @@ void stencil(rk_op* op, int mode, const double* x, const double* r, double* out0
 void bdot(rk_ctx* ctx, const std::vector<const double*>& cols, const double* w, int64_t N,
           double* out);
 void bupd(rk_ctx* ctx, const std::vector<const double*>& cols, const double* g, double gscale,
-          double* w, int64_t N, const std::vector<const double*>& dots, double* red_out);
+          double* w, int64_t N, const std::vector<const double*>& dots, double* red_out,
+          CoefIn cin = CoefIn{});
+// Recycle projection w <- w - C (C^T w) (+ dots of the new w, as bupd);
+// eta <- C^T w.  One rank: the block dot leaves per-CTA partials and the
+// update kernel sums them (no last-CTA finalisation between the two);
+// otherwise bdot + allreduce + bupd.
+void bproject(rk_ctx* ctx, const std::vector<const double*>& cols, double* w, int64_t N,
+              double* eta, const std::vector<const double*>& dots, double* red_out);
 // [Q^T w, Q^T v] in one read of Q (Gram-corrected CGS2, R19)
 void bdot2(rk_ctx* ctx, const std::vector<const double*>& cols, const double* w, const double* v,
            int64_t N, double* out_w, double* out_v);
