@@ -421,41 +421,13 @@ __global__ void __launch_bounds__(256) bupd_gram_kernel(ColPtrs Q, int ncol, int
   block_reduce_store<1>(acc, 1, ra);
 }
 
-// g_c = sum_b part[c G + b] for c < ncol, in a fixed order that every CTA
-// repeats: thread t sums partials t, t + 256, ..., a warp shuffle tree, then
-// the 8 warp sums in order.  gsh[c] = gs g_c; CTA 0 stores g_c.
+// gsh[c] = gs g_c with g_c the deferred block-dot sums; CTA 0 stores g_c
 template <int NC>
 __device__ __forceinline__ void coef_from_partials(const CoefIn& cin, int ncol, double gs, double* gsh) {
-  __shared__ double wsum[NC][8];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int c0 = 0; c0 < NC; c0 += 8) {
-    if (c0 < ncol) {
-      double a[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) a[u] = 0.0;
-      for (int b = threadIdx.x; b < cin.G; b += 256) {
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (c0 + u < ncol) a[u] += __ldcg(cin.part + (int64_t)(c0 + u) * cin.G + b);
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) a[u] += __shfl_down_sync(0xffffffffu, a[u], o);
-        if (lane == 0) wsum[c0 + u][warp] = a[u];
-      }
-    }
-  }
-  __syncthreads();
+  block_sum_partials<NC>(cin.part, cin.G, ncol, gsh);
   for (int c = threadIdx.x; c < NC; c += blockDim.x) {
-    double s = 0.0;
-    if (c < ncol) {
-#pragma unroll
-      for (int q = 0; q < 8; ++q) s += wsum[c][q];
-      if (blockIdx.x == 0) cin.store[c] = s;
-    }
-    gsh[c] = c < ncol ? gs * s : 0.0;
+    if (c < ncol && blockIdx.x == 0) cin.store[c] = gsh[c];
+    gsh[c] = c < ncol ? gs * gsh[c] : 0.0;
   }
 }
 

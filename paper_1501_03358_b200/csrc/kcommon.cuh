@@ -210,6 +210,46 @@ __device__ __forceinline__ void block_reduce_store(const double (&v)[NV], int nv
 }
 
 
+// Deferred finalisation (one rank): the consumer of a reduction sums its
+// per-CTA partials part[q * G + b] (b < G) itself, in a fixed order that every
+// CTA repeats (thread t sums partials t, t + 256, ...; a warp shuffle tree;
+// the 8 warp sums in order), instead of the producer's last CTA doing it
+// behind a fence and an atomic.  256-thread CTAs; dst (shared) gets the nv
+// sums; ends with a barrier.
+template <int NV>
+__device__ __forceinline__ void block_sum_partials(const double* part, int G, int nv, double* dst) {
+  __shared__ double wsum[NV][8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int c0 = 0; c0 < NV; c0 += 8) {
+    if (c0 < nv) {
+      constexpr int U = NV < 8 ? NV : 8;
+      double a[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) a[u] = 0.0;
+      for (int b = threadIdx.x; b < G; b += 256) {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (c0 + u < nv) a[u] += __ldcg(part + (int64_t)(c0 + u) * G + b);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) a[u] += __shfl_down_sync(0xffffffffu, a[u], o);
+        if (lane == 0 && c0 + u < NV) wsum[c0 + u][warp] = a[u];
+      }
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < nv; c += blockDim.x) {
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s += wsum[c][q];
+    dst[c] = s;
+  }
+  __syncthreads();
+}
+
 // Columns are processed in groups of 8 with unguarded loads (the host pads
 // the last group with a duplicate pointer and zero coefficients), so every
 // thread keeps 8 x VEC loads in flight per group.
