@@ -24,9 +24,9 @@ def cls_of(name, grid=None):
     m = re.search(r"chain_kernel(_x2)?<(\d+), (\d+)", name)
     if m:
         return "chain"
-    for k in ("bdot", "bupd", "normalize", "lincomb", "proj", "rotate", "bicg_p", "bicg_s",
+    for k in ("bdot2", "bupd_gram", "bdot", "bupd", "normalize", "lincomb", "proj", "rotate", "bicg_p", "bicg_s",
               "bicg_xr", "bicg_setup", "validate", "chain", "invdiag", "colour_sweep"):
-        if re.search(rf"\b{k}_tile_kernel\b", name):
+        if re.search(rf"\b{k}_(tile_|bulk_)?kernel\b", name):
             return k
         if re.search(rf"\b{k}(_kernel)?\b", name) or f"{k}_kernel" in name:
             return k
