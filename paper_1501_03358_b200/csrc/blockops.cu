@@ -183,27 +183,29 @@ __device__ __forceinline__ bool bk_try(uint64_t* b, uint32_t parity) {
 constexpr int BK_ROWS = 2048, BK_SLOTS = 8, BK_BYTES = BK_ROWS * 8;
 constexpr size_t BK_SMEM = (size_t)BK_SLOTS * BK_BYTES + BK_SLOTS * sizeof(uint64_t);
 
-template <int NC>
+// NR = 1: Q^T w; NR = 2: [Q^T w, Q^T v] (values NC.. for v, as bdot2_tile_kernel)
+template <int NC, int NR>
 __global__ void __launch_bounds__(256, 1) bdot_bulk_kernel(ColPtrs Q, int ncol, const double* __restrict__ w,
-                                                           int64_t N, RedArgs ra) {
+                                                           const double* __restrict__ v, int64_t N, RedArgs ra) {
   RK_PDL_ENTRY();
   RK_GATE(ra.gate);
   extern __shared__ __align__(128) unsigned char bk_sm[];
   double2* ring = reinterpret_cast<double2*>(bk_sm);
   uint64_t* bar = reinterpret_cast<uint64_t*>(bk_sm + (size_t)BK_SLOTS * BK_BYTES);
-  double acc[NC];
+  constexpr int RV = BK_ROWS / 512;   // double2 per thread per tile
+  double acc[NR * NC];
 #pragma unroll
-  for (int c = 0; c < NC; ++c) acc[c] = 0.0;
+  for (int c = 0; c < NR * NC; ++c) acc[c] = 0.0;
   const int64_t ntile = N / BK_ROWS;
   const int64_t mytiles = ntile > blockIdx.x ? (ntile - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const int per = ncol + 1;                         // items per tile: w, Q_0 .. Q_{ncol-1}
+  const int per = ncol + NR;                        // items per tile: w (, v), Q_0 .. Q_{ncol-1}
   const int64_t nitem = mytiles * per;
-  // item -> source: tile blockIdx.x + (it / per) * gridDim.x, column it % per - 1 (-1: w)
+  // item -> source: tile blockIdx.x + (it / per) * gridDim.x, column it % per - NR (< 0: w, v)
   auto issue = [&](int64_t it, int slot) {
     const int64_t lt = it / per;
-    const int c = (int)(it - lt * per) - 1;
+    const int c = (int)(it - lt * per) - NR;
     const int64_t row = (blockIdx.x + lt * gridDim.x) * BK_ROWS;
-    const double* src = (c < 0 ? w : Q.p[c]) + row;
+    const double* src = (c < 0 ? (c + NR == 0 ? w : v) : Q.p[c]) + row;
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bk_smem(bar + slot)),
                  "r"(BK_BYTES)
                  : "memory");
@@ -235,13 +237,16 @@ __global__ void __launch_bounds__(256, 1) bdot_bulk_kernel(ColPtrs Q, int ncol, 
   };
 #pragma unroll 1
   for (int64_t lt = 0; lt < mytiles; ++lt) {
-    while (!bk_try(bar + slot, phase)) {
-    }
-    double2 wv[BK_ROWS / 512];
-    const double2* sl = ring + (size_t)slot * (BK_ROWS / 2);
+    double2 wv[NR][RV];
 #pragma unroll
-    for (int v = 0; v < BK_ROWS / 512; ++v) wv[v] = sl[threadIdx.x + 256 * v];
-    next();
+    for (int h = 0; h < NR; ++h) {
+      while (!bk_try(bar + slot, phase)) {
+      }
+      const double2* sl = ring + (size_t)slot * (BK_ROWS / 2);
+#pragma unroll
+      for (int u = 0; u < RV; ++u) wv[h][u] = sl[threadIdx.x + 256 * u];
+      next();
+    }
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
       if (c < ncol) {
@@ -249,10 +254,13 @@ __global__ void __launch_bounds__(256, 1) bdot_bulk_kernel(ColPtrs Q, int ncol, 
         }
         const double2* qs = ring + (size_t)slot * (BK_ROWS / 2);
 #pragma unroll
-        for (int v = 0; v < BK_ROWS / 512; ++v) {
-          const double2 q = qs[threadIdx.x + 256 * v];
-          acc[c] = fma(q.x, wv[v].x, acc[c]);
-          acc[c] = fma(q.y, wv[v].y, acc[c]);
+        for (int u = 0; u < RV; ++u) {
+          const double2 q = qs[threadIdx.x + 256 * u];
+#pragma unroll
+          for (int h = 0; h < NR; ++h) {
+            acc[h * NC + c] = fma(q.x, wv[h][u].x, acc[h * NC + c]);
+            acc[h * NC + c] = fma(q.y, wv[h][u].y, acc[h * NC + c]);
+          }
         }
         next();
       }
@@ -261,16 +269,21 @@ __global__ void __launch_bounds__(256, 1) bdot_bulk_kernel(ColPtrs Q, int ncol, 
   // tail rows (N even)
   for (int64_t r = ntile * BK_ROWS + 2 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x); r < N;
        r += 2 * (int64_t)gridDim.x * blockDim.x) {
-    const Vec<2> wt = ldv_ro<2>(w + r);
+    Vec<2> wt[NR];
+    wt[0] = ldv_ro<2>(w + r);
+    if (NR == 2) wt[NR - 1] = ldv_ro<2>(v + r);
 #pragma unroll
     for (int c = 0; c < NC; ++c)
       if (c < ncol) {
         const Vec<2> a = ldv_stream<2>(Q.p[c] + r);
-        acc[c] = fma(a.v[0], wt.v[0], acc[c]);
-        acc[c] = fma(a.v[1], wt.v[1], acc[c]);
+#pragma unroll
+        for (int h = 0; h < NR; ++h) {
+          acc[h * NC + c] = fma(a.v[0], wt[h].v[0], acc[h * NC + c]);
+          acc[h * NC + c] = fma(a.v[1], wt[h].v[1], acc[h * NC + c]);
+        }
       }
   }
-  block_reduce_store<NC>(acc, ncol, ra);
+  block_reduce_store<NR * NC>(acc, NR == 1 ? ncol : NR * NC, ra);
 }
 
 // Two right-hand sides: [Q^T w, Q^T v] in one read of Q (the Gram-corrected
@@ -710,7 +723,7 @@ static int bdot_launch(rk_ctx* ctx, const std::vector<const double*>& cols, cons
   int grid = 0;
 #define RK_BDOT(NCV)                                                                          \
   if (bulk)                                                                                         \
-    grid = launch_bulk(ctx, bdot_bulk_kernel<NCV>, Q, ncol, w, N, ra);                              \
+    grid = launch_bulk(ctx, bdot_bulk_kernel<NCV, 1>, Q, ncol, w, (const double*)nullptr, N, ra);   \
   else if (vec == 2)                                                                                \
     grid = launch_k(ctx, bdot_tile_kernel<NCV, 256>, work / DRV, dim3(256), Q, ncol, w, N, ra);     \
   else grid = launch_k(ctx, bdot_kernel<NCV, 1>, work, dim3(256), Q, ncol, w, N, ra);
@@ -825,6 +838,28 @@ void bdot2(rk_ctx* ctx, const std::vector<const double*>& cols_all, const double
   if (!tiled) {   // odd sizes / misaligned: two single-RHS block dots
     bdot(ctx, cols_all, w, N, out_w);
     bdot(ctx, cols_all, v, N, out_v);
+    return;
+  }
+  // bulk-copy path: one launch for up to 32 columns (one CTA per SM leaves
+  // registers for 64 accumulators), else <= 24 columns per tiled launch
+  if (total <= 32 && (ctx->bdot_bulk == 2 ||
+                      (ctx->bdot_bulk == 1 && total >= 4 && N >= (int64_t)BK_ROWS * ctx->sms))) {
+    const int nc = nc_round(total);
+    RedArgs ra = red_args(ctx, out_w);
+    ra.out2 = out_v;
+    ra.split = nc;
+    ra.valid = total;
+    ColPtrs Q = make_cols_padded(cols_all, nc);
+    Launch L(ctx, "bdot", 8.0 * N * (total + 2));
+    switch (nc) {
+      case 8: launch_bulk(ctx, bdot_bulk_kernel<8, 2>, Q, total, w, v, N, ra); break;
+      case 16: launch_bulk(ctx, bdot_bulk_kernel<16, 2>, Q, total, w, v, N, ra); break;
+      case 24: launch_bulk(ctx, bdot_bulk_kernel<24, 2>, Q, total, w, v, N, ra); break;
+      default: launch_bulk(ctx, bdot_bulk_kernel<32, 2>, Q, total, w, v, N, ra); break;
+    }
+    L.done();
+    allreduce(ctx, out_w, total);
+    allreduce(ctx, out_v, total);
     return;
   }
   for (int off = 0; off < total; off += 24) {
