@@ -437,6 +437,52 @@ def test_sequence_parity_bulk_bdot(rk, name, monkeypatch):
         assert ra["krylov_matvecs"] == rb["krylov_matvecs"]
 
 
+@pytest.mark.parametrize("name", ["c3m", "c3s"])
+def test_bicg_lookahead_bitwise(rk, ctx, name, monkeypatch):
+    """The one-iteration rBiCGStab lookahead changes no
+    arithmetic: with and without it every system's x, matvec count, outcome
+    and residuals are bit-identical (the speculative iteration after the last
+    one is always gated off on the device)."""
+    w = get_workload(name)
+    monkeypatch.setenv("RK_BICG_LOOKAHEAD", "0")
+    a, _ = gpu_sequence(rk, ctx, w)
+    monkeypatch.setenv("RK_BICG_LOOKAHEAD", "1")
+    b, _ = gpu_sequence(rk, ctx, w)
+    assert [r["tag"] for r, _ in a] == [r["tag"] for r, _ in b]
+    for (ra, xa), (rb, xb) in zip(a, b):
+        assert np.array_equal(xa, xb)
+        for key in ("krylov_matvecs", "cycles_or_iters", "outcome", "final_true_res",
+                    "final_updated_res"):
+            assert ra[key] == rb[key], key
+
+
+@pytest.mark.parametrize("method,budget", [("bicgstab", 7), ("bicgstab", 10), ("rbicgstab", 9)])
+def test_bicg_lookahead_matvec_budget(rk, ctx, method, budget, monkeypatch):
+    """Lookahead at the matvec budget: the host enqueues iteration i+1 only
+    when i's normal end leaves budget for it, so a MAX_MATVECS stop (odd or
+    even budget) gives the same x and counts as the unspeculated loop (an
+    iteration starts while the count is below the budget and spends two)."""
+    prob = porous7(16, 5)
+    b = prob.rhs(0).reshape(-1)
+    cfg = dict(m=8, k_max=4, k_keep=4, select_count=0, sweeps=3, tol=1e-14, max_matvecs=budget)
+    out = []
+    for la in ("0", "1"):
+        monkeypatch.setenv("RK_BICG_LOOKAHEAD", la)
+        op = make_op(rk, ctx, prob)
+        s = rk.Solver(op, rk.make_config(method, **cfg))
+        if method == "rbicgstab":
+            U0 = np.random.default_rng(3).uniform(-1, 1, (prob.N, 4))
+            s.recycle_set(dev(U0.T.copy()))
+        x, r = s.solve(dev(b))
+        out.append((x.cpu().numpy(), r))
+        s.close()
+        op.close()
+    (xa, ra), (xb, rb) = out
+    assert np.array_equal(xa, xb)
+    assert ra["krylov_matvecs"] == rb["krylov_matvecs"] in (budget, budget + 1)
+    assert ra["outcome"] == rb["outcome"] == "MAX_MATVECS"
+
+
 def test_gmres_stagnation_parity(rk, ctx):
     """GMRES(12) stagnates on the shrunken channel (PAPER P:782-784 reports
     GMRES(m < 50) stagnation on the channel): both sides exhaust the 2000
