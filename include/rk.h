@@ -187,6 +187,24 @@ rk_status rk_solve_host(rk_solver* s, const double* b_host, double* x_host, doub
  * (written on exit; may alias x0_host).  Copies are part of the call. */
 rk_status rk_solve_host_ex(rk_solver* s, const double* b_host, const double* x0_host,
                            double* x_host, double tol, rk_report* rep);
+/* Pipelined host-buffer solves for a sequence of systems (x0 = 0):
+ * the upload of the next right-hand side and the download of the previous
+ * solution run on the context's copy engine while the current system solves.
+ *   rk_stage_rhs    queues the copy of b_host (N_local doubles, pinned for
+ *                   overlap) into the solver's staging slot `slot` (0 or 1)
+ *                   and returns at once.  A slot may be restaged once the
+ *                   rk_solve_staged call that used it has returned.
+ *   rk_solve_staged solves with the right-hand side staged in `slot` (it
+ *                   waits for that copy on the device), then queues the copy
+ *                   of x to x_host and returns without waiting for it.
+ *   rk_host_sync    waits for every queued copy; afterwards the x_host
+ *                   buffers hold the solutions, and work queued later on the
+ *                   library stream is ordered after the copies.
+ * b_host and x_host must stay valid, and x_host unread, until rk_host_sync.
+ * Errors: RK_EINVAL (NULL, slot not 0/1, slot never staged). */
+rk_status rk_stage_rhs(rk_solver* s, int slot, const double* b_host);
+rk_status rk_solve_staged(rk_solver* s, int slot, double* x_host, double tol, rk_report* rep);
+rk_status rk_host_sync(rk_solver* s);
 /* Residual history of the last solve: rows (krylov_matvecs, ||b-Ax|| or NaN,
  * preconditioned / updated ||r||).  out is HOST [cap][3]. */
 rk_status rk_history(rk_solver* s, double* out, int64_t cap, int64_t* len);

@@ -80,6 +80,9 @@ def lib():
         "rk_solve": ([vp, vp, vp, dbl, P(rk_report)], i32),
         "rk_solve_host": ([vp, vp, vp, dbl, P(rk_report)], i32),
         "rk_solve_host_ex": ([vp, vp, vp, vp, dbl, P(rk_report)], i32),
+        "rk_stage_rhs": ([vp, i32, vp], i32),
+        "rk_solve_staged": ([vp, i32, vp, dbl, P(rk_report)], i32),
+        "rk_host_sync": ([vp], i32),
         "rk_history": ([vp, vp, i64, P(i64)], i32),
         "rk_solver_workspace": ([vp, P(i64)], i32),
         "rk_launch_count": ([vp, P(i64)], i32),
@@ -106,5 +109,6 @@ EXPORTED = ["rk_last_error", "rk_version", "rk_nccl_unique_id", "rk_ctx_create",
             "rk_ctx_destroy", "rk_op_create", "rk_op_update_bands", "rk_op_destroy",
             "rk_op_apply", "rk_precond_apply", "rk_solver_create", "rk_solver_destroy",
             "rk_solver_set_method", "rk_recycle_set", "rk_recycle_dim", "rk_recycle_export",
-            "rk_solve", "rk_solve_host", "rk_solve_host_ex", "rk_history", "rk_solver_workspace", "rk_launch_count",
+            "rk_solve", "rk_solve_host", "rk_solve_host_ex", "rk_stage_rhs", "rk_solve_staged",
+            "rk_host_sync", "rk_history", "rk_solver_workspace", "rk_launch_count",
             "rk_profile_enable", "rk_profile_every", "rk_profile_read"]

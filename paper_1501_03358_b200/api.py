@@ -177,6 +177,20 @@ class Solver:
                                          _p(x_host), tol, C.byref(rep)), "rk_solve_host_ex")
         return x_host, _report(rep)
 
+    def stage_rhs(self, slot, b_host):
+        """Queue the upload of b_host (pinned CPU float64) into staging slot 0/1."""
+        L.check(L.lib().rk_stage_rhs(self.h, slot, _p(b_host)), "rk_stage_rhs")
+
+    def solve_staged(self, slot, x_host, tol=0.0):
+        """Solve with the right-hand side staged in `slot` (x0 = 0); the download
+        of x into x_host (pinned) is queued, complete after host_sync()."""
+        rep = L.rk_report()
+        L.check(L.lib().rk_solve_staged(self.h, slot, _p(x_host), tol, C.byref(rep)), "rk_solve_staged")
+        return x_host, _report(rep)
+
+    def host_sync(self):
+        L.check(L.lib().rk_host_sync(self.h), "rk_host_sync")
+
     def recycle_dim(self):
         k = C.c_int()
         L.check(L.lib().rk_recycle_dim(self.h, C.byref(k)), "rk_recycle_dim")
@@ -225,7 +239,7 @@ class Solver:
 
 def solve_sequence(solver, rhs, n, method, n_sw=0, epoch_of=None, bands_for_epoch=None,
                    tol=0.0, host=False, x_out=None, switchback=False, refresh_on_epoch=False,
-                   refresh_every=0):
+                   refresh_every=0, pipeline=True):
     """Sequence controller (reading D3): for the hybrid,
     systems t < n_sw use rGCROT and later ones rBiCGStab with the recycle
     space frozen; a new A epoch uploads its bands (librk then invalidates C
@@ -236,7 +250,13 @@ def solve_sequence(solver, rhs, n, method, n_sw=0, epoch_of=None, bands_for_epoc
     `refresh_every` = n solves every n-th post-switch system by rGCROT.
     rhs(t) -> b_t (device tensor, or pinned host tensor if host=True).
     Returns the reports; solutions go to x_out[t] when given.  The operator
-    must hold the bands of epoch_of(0) on entry."""
+    must hold the bands of epoch_of(0) on entry.  host=True with pipeline:
+    b_{t+1} is uploaded and x_{t-1} downloaded while system t solves
+    (rk_stage_rhs / rk_solve_staged / rk_host_sync); every x_out[t] is
+    complete on return."""
+    if host and pipeline:
+        return _solve_sequence_pipelined(solver, rhs, n, method, n_sw, epoch_of, bands_for_epoch, tol,
+                                         x_out, switchback, refresh_on_epoch, refresh_every)
     reps = []
     cur = epoch_of(0) if epoch_of else 0
     for t in range(n):
@@ -269,6 +289,45 @@ def solve_sequence(solver, rhs, n, method, n_sw=0, epoch_of=None, bands_for_epoc
             tag = "rbicgstab+rgcrot"
         r["tag"] = tag
         reps.append(r)
+    return reps
+
+
+def _solve_sequence_pipelined(solver, rhs, n, method, n_sw, epoch_of, bands_for_epoch, tol, x_out,
+                              switchback, refresh_on_epoch, refresh_every):
+    """solve_sequence(host=True): the same controller over staged slots."""
+    reps = []
+    cur = epoch_of(0) if epoch_of else 0
+    bs = [rhs(0)] if n else []
+    xs = []
+    if n:
+        solver.stage_rhs(0, bs[0])
+    for t in range(n):
+        if t + 1 < n:   # upload b_{t+1} while t solves
+            bs.append(rhs(t + 1))
+            solver.stage_rhs((t + 1) % 2, bs[t + 1])
+        e = epoch_of(t) if epoch_of else 0
+        changed = e != cur
+        if changed:
+            solver.op.update_bands(bands_for_epoch(e))
+            cur = e
+        tag = method
+        if method == "hybrid":
+            tag = "rgcrot" if _hybrid_uses_rgcrot(t, n_sw, changed, refresh_on_epoch,
+                                                  refresh_every) else "rbicgstab"
+            solver.set_method(tag)
+        x = x_out[t] if x_out is not None else torch.zeros(bs[t].shape, dtype=torch.float64).pin_memory()
+        xs.append(x)
+        _, r = solver.solve_staged(t % 2, x, tol)
+        if method == "hybrid" and tag == "rbicgstab" and switchback and r["outcome"] != "CONVERGED":
+            solver.set_method("rgcrot")
+            _, r2 = solver.solve_staged(t % 2, x, tol)
+            for key in ("krylov_matvecs", "operator_applications", "seconds"):
+                r2[key] += r[key]
+            r = r2
+            tag = "rbicgstab+rgcrot"
+        r["tag"] = tag
+        reps.append(r)
+    solver.host_sync()
     return reps
 
 

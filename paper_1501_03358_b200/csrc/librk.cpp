@@ -275,6 +275,38 @@ struct rk_solver {
   std::vector<std::array<double, 3>> history;
   rk_report last{};
   cudaEvent_t bev[2] = {nullptr, nullptr};    // rBiCGStab lookahead: iteration records landed
+  // pipelined host solves (rk_stage_rhs / rk_solve_staged / rk_host_sync)
+  cudaStream_t cstream = nullptr;             // copy stream
+  double* bstage[2] = {nullptr, nullptr};     // staged right-hand sides
+  cudaEvent_t staged_ev[2] = {nullptr, nullptr};
+  bool staged_ok[2] = {false, false};
+  double* xstage = nullptr;                   // x snapshot being downloaded
+  cudaEvent_t xready = nullptr, xcopied = nullptr;
+  bool xcopy_pending = false;
+  void ensure_pipeline() {
+    if (cstream) return;
+    RK_CUDA(cudaStreamCreateWithFlags(&cstream, cudaStreamNonBlocking));
+    for (int q = 0; q < 2; ++q) {
+      RK_CUDA(cudaMalloc(&bstage[q], sizeof(double) * N));
+      RK_CUDA(cudaEventCreateWithFlags(&staged_ev[q], cudaEventDisableTiming));
+    }
+    RK_CUDA(cudaMalloc(&xstage, sizeof(double) * N));
+    RK_CUDA(cudaEventCreateWithFlags(&xready, cudaEventDisableTiming));
+    RK_CUDA(cudaEventCreateWithFlags(&xcopied, cudaEventDisableTiming));
+  }
+  void free_pipeline() {
+    if (!cstream) return;
+    cudaStreamSynchronize(cstream);
+    for (int q = 0; q < 2; ++q) {
+      cudaFree(bstage[q]);
+      cudaEventDestroy(staged_ev[q]);
+    }
+    cudaFree(xstage);
+    cudaEventDestroy(xready);
+    cudaEventDestroy(xcopied);
+    cudaStreamDestroy(cstream);
+    cstream = nullptr;
+  }
   bool lookahead = true;                      // RK_BICG_LOOKAHEAD=0 disables
 
   static constexpr size_t STEP = 2 * (MAXCOL + 1) + 2;  // g1[81] g2[81] nrm2 brk
@@ -1207,6 +1239,7 @@ void rk_solver_destroy(rk_solver* s) {
   cudaStreamSynchronize(s->ctx->stream);
   for (auto b : s->bases) cudaFree(b);
   cudaFree(s->bdev);
+  s->free_pipeline();
   cudaFree(s->dsc);
   cudaFreeHost(s->hsc);
   for (auto e : s->bev)
@@ -1347,6 +1380,64 @@ rk_status rk_solve_host_ex(rk_solver* s, const double* bh, const double* x0h, do
 
 rk_status rk_solve_host(rk_solver* s, const double* bh, double* xh, double tol, rk_report* rep) {
   return rk_solve_host_ex(s, bh, xh, xh, tol, rep);
+}
+
+rk_status rk_stage_rhs(rk_solver* s, int slot, const double* bh) {
+  return guarded([&] {
+    RK_REQUIRE(s && bh, RK_EINVAL, "NULL argument");
+    RK_REQUIRE(slot == 0 || slot == 1, RK_EINVAL, "slot must be 0 or 1");
+    RK_CUDA(cudaSetDevice(s->ctx->device));
+    s->ensure_pipeline();
+    RK_CUDA(cudaMemcpyAsync(s->bstage[slot], bh, sizeof(double) * s->N, cudaMemcpyHostToDevice,
+                            s->cstream));
+    RK_CUDA(cudaEventRecord(s->staged_ev[slot], s->cstream));
+    s->staged_ok[slot] = true;
+  });
+}
+
+rk_status rk_solve_staged(rk_solver* s, int slot, double* xh, double tol, rk_report* rep) {
+  return guarded([&] {
+    RK_REQUIRE(s && xh, RK_EINVAL, "NULL argument");
+    RK_REQUIRE(slot == 0 || slot == 1, RK_EINVAL, "slot must be 0 or 1");
+    RK_REQUIRE(s->cstream && s->staged_ok[slot], RK_EINVAL, "slot was never staged");
+    RK_CUDA(cudaSetDevice(s->ctx->device));
+    const auto t0 = std::chrono::steady_clock::now();
+    cudaStream_t ls = s->ctx->stream;
+    RK_CUDA(cudaStreamWaitEvent(ls, s->staged_ev[slot], 0));   // b has landed
+    RK_CUDA(cudaMemsetAsync(s->x, 0, sizeof(double) * s->N, ls));   // x_hat = 0
+    if (!(tol > 0)) tol = s->cfg.tol;
+    rk_report r;
+    std::memset(&r, 0, sizeof(r));
+    s->history.clear();
+    if (s->method == RK_RGCROT || s->method == RK_GMRES) s->solve_rgcrot(s->bstage[slot], tol, r);
+    else s->solve_rbicgstab(s->bstage[slot], tol, r);
+    // snapshot x (after the previous download finished with the snapshot
+    // buffer) and download it on the copy stream; the next solve overlaps it
+    if (s->xcopy_pending) RK_CUDA(cudaStreamWaitEvent(ls, s->xcopied, 0));
+    RK_CUDA(cudaMemcpyAsync(s->xstage, s->x, sizeof(double) * s->N, cudaMemcpyDeviceToDevice, ls));
+    RK_CUDA(cudaEventRecord(s->xready, ls));
+    RK_CUDA(cudaStreamWaitEvent(s->cstream, s->xready, 0));
+    RK_CUDA(cudaMemcpyAsync(xh, s->xstage, sizeof(double) * s->N, cudaMemcpyDeviceToHost,
+                            s->cstream));
+    RK_CUDA(cudaEventRecord(s->xcopied, s->cstream));
+    s->xcopy_pending = true;
+    r.k_after = (int)s->order.size();
+    r.history_len = (int64_t)s->history.size();
+    r.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    s->last = r;
+    if (rep) *rep = r;
+  });
+}
+
+rk_status rk_host_sync(rk_solver* s) {
+  return guarded([&] {
+    RK_REQUIRE(s, RK_EINVAL, "NULL argument");
+    if (!s->cstream) return;
+    RK_CUDA(cudaSetDevice(s->ctx->device));
+    if (s->xcopy_pending) RK_CUDA(cudaStreamWaitEvent(s->ctx->stream, s->xcopied, 0));
+    RK_CUDA(cudaStreamSynchronize(s->cstream));
+    s->xcopy_pending = false;
+  });
 }
 
 rk_status rk_history(rk_solver* s, double* out, int64_t cap, int64_t* len) {

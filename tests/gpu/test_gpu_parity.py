@@ -505,6 +505,44 @@ def test_sequence_parity_host_buffers(rk, ctx):
     compare_sequences(w, gpu, ora, w.params.method)
 
 
+@pytest.mark.parametrize("name,kw", [("c3s", {}), ("c2s", {}), ("c4s", {"switchback": True})])
+def test_pipelined_host_sequence_bitwise(rk, ctx, name, kw):
+    """rk_stage_rhs / rk_solve_staged / rk_host_sync (uploads of b_{t+1} and
+    downloads of x_{t-1} overlapping solve t) give bit for bit the solutions
+    and reports of the one-call rk_solve_host_ex path, also across A epochs
+    and a switch-back re-solve from the same staged slot."""
+    w = get_workload(name)
+    a, _ = gpu_sequence(rk, ctx, w, host=True, pipeline=True, **kw)
+    b, _ = gpu_sequence(rk, ctx, w, host=True, pipeline=False, **kw)
+    assert [r["tag"] for r, _ in a] == [r["tag"] for r, _ in b]
+    for (ra, xa), (rb, xb) in zip(a, b):
+        assert np.array_equal(xa, xb)
+        for key in ("krylov_matvecs", "outcome", "final_true_res"):
+            assert ra[key] == rb[key], key
+
+
+def test_staged_solve_rejects_unstaged_slot(rk, ctx):
+    prob = porous7(16, 5)
+    op = make_op(rk, ctx, prob)
+    s = rk.Solver(op, rk.make_config("bicgstab", sweeps=3))
+    x = torch.zeros(prob.N, dtype=torch.float64).pin_memory()
+    with pytest.raises(rk.RkError, match="EINVAL"):
+        s.solve_staged(0, x)
+    b = torch.from_numpy(prob.rhs(0).reshape(-1)).pin_memory()
+    s.stage_rhs(1, b)
+    with pytest.raises(rk.RkError, match="EINVAL"):
+        s.solve_staged(0, x)
+    with pytest.raises(rk.RkError, match="EINVAL"):
+        s.stage_rhs(2, b)
+    _, r = s.solve_staged(1, x)
+    s.host_sync()
+    ref = Operator.from_problem(prob)
+    bn = b.numpy()
+    assert np.linalg.norm(bn - ref.apply(x.numpy())) <= 1e-7 * np.linalg.norm(bn)
+    s.close()
+    op.close()
+
+
 def test_solve_host_ex_nonzero_x0(rk, ctx):
     """rk_solve_host_ex with a HOST initial guess (reading R6) equals the
     device rk_solve from the same x0; x0 = NULL equals x0 = 0."""
