@@ -531,6 +531,111 @@ __global__ void __launch_bounds__(256) bupd_tile_kernel(ColPtrs Q, int ncol, con
   if constexpr (ND > 0) block_reduce_store<(ND > 0 ? ND : 1)>(acc, ND, ra);
 }
 
+// rBiCGStab lines 7a + 8 fused (one rank, reading R20): the block dot before
+// this kernel produced the per-CTA partials of [C, r~]^T v (k + 1 values);
+// every CTA sums them (eta = C^T v, r~^T v), forms
+//   sigma = r~^T v - (C^T r~)^T eta  (= r~^T (v - C eta); ctr = C^T r~ is
+//   computed once per solve) and alpha = rho / sigma,
+// then streams v <- v - C eta (bupd_tile_kernel's order and FMAs) and, with
+// the new v rows still in registers, bicg_s: s = r - alpha v, z = w_l s / D,
+// ||s||^2.  CTA 0 stores eta and sigma.
+template <int NC>
+__global__ void __launch_bounds__(256) bproj_s_kernel(ColPtrs Q, int k, double* __restrict__ v, int64_t N,
+                                                      CoefIn cin, const double* __restrict__ ctr,
+                                                      const double* __restrict__ r, double* __restrict__ s,
+                                                      double* __restrict__ z, const double* __restrict__ D,
+                                                      double wl, BiIter* cur, RedArgs ra) {
+  RK_PDL_ENTRY();
+  RK_GATE(ra.gate);
+  constexpr int RV = TRV, G = TG;
+  __shared__ double gsh[NC];
+  __shared__ double sig_alpha[2];
+  block_sum_partials<NC>(cin.part, cin.G, k + 1, gsh);
+  if (threadIdx.x == 0) {
+    double corr = 0.0;
+    for (int c = 0; c < k; ++c) corr = fma(ctr[c], gsh[c], corr);
+    const double sigma = gsh[k] - corr;
+    sig_alpha[0] = sigma;
+    sig_alpha[1] = cur->rho / sigma;
+    if (blockIdx.x == 0) cur->sigma = sigma;
+  }
+  if (blockIdx.x == 0)
+    for (int c = threadIdx.x; c < k; c += blockDim.x) cin.store[c] = gsh[c];
+  __syncthreads();
+  if (threadIdx.x == 0) gsh[k] = 0.0;   // r~ is not an update column
+  for (int c = k + 1 + threadIdx.x; c < NC; c += blockDim.x) gsh[c] = 0.0;
+  __syncthreads();
+  const double alpha = sig_alpha[1];
+  const volatile double* gshv = gsh;
+  double acc[1] = {0.0};
+  auto epi = [&](int64_t n, const double2& vn) {
+    const double2 rn = *reinterpret_cast<const double2*>(r + n);
+    double2 sn, zn;
+    sn.x = rn.x - alpha * vn.x;
+    sn.y = rn.y - alpha * vn.y;
+    acc[0] = fma(sn.x, sn.x, acc[0]);
+    acc[0] = fma(sn.y, sn.y, acc[0]);
+    zn = sn;
+    if (D) {
+      const Vec<2> dn = ldv_stream<2>(D + n);
+      zn.x = (wl * sn.x) * dn.v[0];
+      zn.y = (wl * sn.y) * dn.v[1];
+    }
+    *reinterpret_cast<double2*>(s + n) = sn;
+    *reinterpret_cast<double2*>(z + n) = zn;
+  };
+  const int64_t ntile = N / TILE_ROWS;
+#pragma unroll 1
+  for (int64_t t = blockIdx.x; t < ntile; t += gridDim.x) {
+    const int64_t r0 = t * TILE_ROWS + 2 * threadIdx.x;
+    double2 wv[RV];
+#pragma unroll
+    for (int u = 0; u < RV; ++u) wv[u] = *reinterpret_cast<const double2*>(v + r0 + 512 * u);
+#pragma unroll
+    for (int c = 0; c < NC; c += G) {
+      if (c < k) {
+        double gc[G];
+#pragma unroll
+        for (int u = 0; u < G; ++u) gc[u] = gshv[c + u];
+        double2 q[G][RV];
+#pragma unroll
+        for (int u = 0; u < G; ++u)
+#pragma unroll
+          for (int vv = 0; vv < RV; ++vv) {
+            const Vec<2> a = ldv_stream<2>(Q.p[c + u] + r0 + 512 * vv);
+            q[u][vv] = make_double2(a.v[0], a.v[1]);
+          }
+#pragma unroll
+        for (int u = 0; u < G; ++u) {
+#pragma unroll
+          for (int vv = 0; vv < RV; ++vv) {
+            wv[vv].x = fma(-gc[u], q[u][vv].x, wv[vv].x);
+            wv[vv].y = fma(-gc[u], q[u][vv].y, wv[vv].y);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < RV; ++u) {
+      *reinterpret_cast<double2*>(v + r0 + 512 * u) = wv[u];
+      epi(r0 + 512 * u, wv[u]);
+    }
+  }
+  for (int64_t n = ntile * TILE_ROWS + 2 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x); n < N;
+       n += 2 * (int64_t)gridDim.x * blockDim.x) {
+    double2 wn = *reinterpret_cast<const double2*>(v + n);
+#pragma unroll 1
+    for (int c = 0; c < k; ++c) {
+      const Vec<2> a = ldv_stream<2>(Q.p[c] + n);
+      wn.x = fma(-gsh[c], a.v[0], wn.x);
+      wn.y = fma(-gsh[c], a.v[1], wn.y);
+    }
+    *reinterpret_cast<double2*>(v + n) = wn;
+    epi(n, wn);
+  }
+  block_reduce_store<1>(acc, 1, ra);
+}
+
 // v_{j+1} = w / h_{j+1,j}, with the happy-breakdown test h <= 1e-14 ||A_hat v_j||
 // (reading D18): on breakdown v_{j+1} = 0 and *flag = 1.
 template <int VEC>
@@ -776,6 +881,48 @@ void bproject(rk_ctx* ctx, const std::vector<const double*>& cols, double* w, in
   cin.part = ctx->dpartials;
   cin.store = eta;
   bupd(ctx, cols, eta, 1.0, w, N, dots, red_out, cin);
+}
+
+bool bicg_proj_s(rk_op* op, const std::vector<const double*>& C, double* v, const double* rtl,
+                 const double* ctr, double* eta, const double* r, double* s, double* z, double wl,
+                 bool jacobi, BiIter* cur) {
+  rk_ctx* ctx = op->ctx;
+  const int64_t N = op->N;
+  const int k = (int)C.size();
+  const double* D = jacobi ? op->invd() : nullptr;
+  if (!ctx->defer_coef || ctx->nranks != 1 || k < 1 || k + 1 > 40 ||
+      pick_vec(N, {v, rtl, r, s, z, D}, C) != 2)
+    return false;
+  std::vector<const double*> cols(C);
+  cols.push_back(rtl);
+  RedArgs ra = red_args(ctx, nullptr);
+  ra.partials = ctx->dpartials;
+  ra.defer = 1;
+  Launch L(ctx, "bdot", 8.0 * N * (k + 2));
+  CoefIn cin;
+  cin.G = bdot_launch(ctx, cols, v, N, ra);
+  L.done();
+  cin.part = ctx->dpartials;
+  cin.store = eta;
+  const int nc = nc_round(k + 1);
+  ColPtrs Q = make_cols_padded(C, nc_round(k));
+  RedArgs rs = red_args(ctx, &cur->ss);
+  Launch L2(ctx, "bupd", 8.0 * N * (k + 2 + 3 + (jacobi ? 1 : 0)));
+  switch (nc) {
+#define RK_BPS(NCV)                                                                                  \
+  case NCV:                                                                                          \
+    launch_k(ctx, bproj_s_kernel<NCV>, N / (2 * TRV), dim3(256), Q, k, v, N, cin, ctr, r, s, z, D, wl, \
+             cur, rs);                                                                               \
+    break;
+    RK_BPS(8)
+    RK_BPS(16)
+    RK_BPS(24)
+    RK_BPS(32)
+    default: RK_BPS(40)
+#undef RK_BPS
+  }
+  L2.done();
+  return true;
 }
 
 void bupd(rk_ctx* ctx, const std::vector<const double*>& cols, const double* g, double gscale,

@@ -806,6 +806,7 @@ struct rk_solver {
       }
       bicg_setup(ctx, xi, eta(2), k, bi(0));
       RK_CUDA(cudaMemcpyAsync(rtl, r, sizeof(double) * N, cudaMemcpyDeviceToDevice, ctx->stream));
+      if (k > 0 && ctx->nranks == 1) bdot(ctx, C, rtl, N, eta(3));   // C^T r~ for bicg_proj_s [R20]
       fetch(o_bi, 8);
       sync();
       double rr = hbi(0)->rr;
@@ -836,13 +837,17 @@ struct rk_solver {
           stencil(op, SM_SPMV, ph, nullptr, v, nullptr, 0.0, nullptr);
         }
         // line 7a: eta1 = C^T v ; v -= C eta1 ; sigma = r~^T v
-        if (k > 0) {
-          bproject(ctx, C, v, N, eta(0), {rtl}, &cur->sigma);
-        } else {
-          bdot(ctx, {rtl}, v, N, &cur->sigma);
-        }
         // line 8: alpha = rho / sigma ; s = r - alpha v (+ first sweep of s_hat)
-        bicg_s(op, r, v, s, jac() ? za : sh, wl, jac(), cur);
+        const bool fused = k > 0 && ctx->nranks == 1 &&
+                           bicg_proj_s(op, C, v, rtl, eta(3), eta(0), r, s, jac() ? za : sh, wl, jac(), cur);
+        if (!fused) {
+          if (k > 0) {
+            bproject(ctx, C, v, N, eta(0), {rtl}, &cur->sigma);
+          } else {
+            bdot(ctx, {rtl}, v, N, &cur->sigma);
+          }
+          bicg_s(op, r, v, s, jac() ? za : sh, wl, jac(), cur);
+        }
         if (jac()) {
           apply_right(s, sh, tt);               // s_hat = M^-1 s ; t = A s_hat (line 12)
         } else {
@@ -1211,7 +1216,7 @@ rk_status rk_solver_create(rk_op* op, const rk_config* cfg, rk_solver** out) {
       s->o_bi = o;
       o += 8 * (size_t)(s->max_it + 2);
       s->o_eta = o;
-      o += 3 * (size_t)MAXCOL;
+      o += 4 * (size_t)MAXCOL;   // eta(0..2) + C^T r~ (rBiCGStab)
       s->nsc = o;
       RK_CUDA(cudaMalloc(&s->dsc, o * sizeof(double)));
       RK_CUDA(cudaMemsetAsync(s->dsc, 0, o * sizeof(double), s->ctx->stream));

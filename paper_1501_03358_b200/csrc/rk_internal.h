@@ -331,6 +331,13 @@ void rotate(rk_ctx* ctx, const std::vector<double*>& cols, const double* T, int6
 // the rest of the iteration's kernels
 void bicg_p(rk_op* op, const double* r, double* p, const double* v, double* z, double wl,
             bool jacobi, BiIter* cur, const BiIter* prev, int first, double thr_conv, double thr_div);
+// rBiCGStab lines 7a + 8 in two launches (one rank; reading R20): the block
+// dot of [C, r~] with v, then one kernel for sigma, v -= C eta, alpha, s, the
+// first sweep of s_hat (z) and ||s||^2.  ctr = C^T r~ (k values, per solve).
+// Returns false (nothing launched) where it does not apply.
+bool bicg_proj_s(rk_op* op, const std::vector<const double*>& C, double* v, const double* rtl,
+                 const double* ctr, double* eta, const double* r, double* s, double* z, double wl,
+                 bool jacobi, BiIter* cur);
 void bicg_s(rk_op* op, const double* r, const double* v, double* s, double* z, double wl,
             bool jacobi, BiIter* cur);
 void bicg_xr(rk_ctx* ctx, double* x, double* r, const double* s, const double* t, const double* ph,
