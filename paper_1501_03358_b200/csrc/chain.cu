@@ -35,6 +35,11 @@
 // 1/D: recomputed from the diagonal band (1.0 / D is correctly rounded, so
 // the bits equal librk's precomputed 1/D band used by the unfused kernels);
 // RK_CHAIN_TMA_INVD = 1 streams that band instead (one more array per plane).
+// RK_CHAIN_XLEAD = 1: the x-pair kernel's TMA batches carry the input tile one
+// plane ahead of the bands (chain_x2.cuh); 0: the same plane.
+#ifndef RK_CHAIN_XLEAD
+#define RK_CHAIN_XLEAD 1
+#endif
 #ifndef RK_CHAIN_TMA_INVD
 #define RK_CHAIN_TMA_INVD 1
 #endif

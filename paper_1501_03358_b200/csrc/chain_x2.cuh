@@ -183,6 +183,12 @@ chain_kernel_x2(const __grid_constant__ CUtensorMap map_b, const __grid_constant
   auto xtile = [&](int xs) {
     return reinterpret_cast<const double*>(smem + G::X_BASE + xs * G::XSLOT) + xoff;
   };
+  // Batch q (one mbarrier, on the input tile's slot): the bands / rhs of
+  // plane q and, with RK_CHAIN_XLEAD, the input tile of plane q + 1 (else of
+  // plane q).  Step tau waits for the batch holding tile tau + 1; with the
+  // input tile one plane ahead that batch was issued PD steps earlier
+  // instead of PD - 1 (the bands of plane tau + 1 are not needed until the
+  // next step), so a TMA round trip gets two steps to land.
   auto issue = [&](int q, int xs, int bs) {
     unsigned char* bbase = smem + bs * G::BSLOT;
     unsigned char* xbase = smem + G::X_BASE + xs * G::XSLOT;
@@ -191,7 +197,7 @@ chain_kernel_x2(const __grid_constant__ CUtensorMap map_b, const __grid_constant
     mbar_expect_tx(&bars[xs], tx_bytes);
     tma_load_4d(bbase, &map_b, &bars[xs], gx0 - PADB, gy0, pl, 0);
     if (LOAD_R) tma_load_3d(bbase + G::R_OFF, &map_r, &bars[xs], gx0 - PADB, gy0, pl);
-    tma_load_3d(xbase, &map_x, &bars[xs], gx0 - 1 - PADX, gy0 - 1, pl + 1);
+    tma_load_3d(xbase, &map_x, &bars[xs], gx0 - 1 - PADX, gy0 - 1, (RK_CHAIN_XLEAD ? pl_of(q + 1) : pl) + 1);
   };
 
   if (tid == 0) {
@@ -199,14 +205,24 @@ chain_kernel_x2(const __grid_constant__ CUtensorMap map_b, const __grid_constant
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (tid == 0)
-    for (int q = qfirst; q <= min(qfirst + PD, qlast); ++q) issue(q, (q - qfirst) % NXB, (q - qfirst) % NB);
+  if (tid == 0) {
+    if (RK_CHAIN_XLEAD) {
+      // the first tile alone, then batches qfirst .. qfirst + PD
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(&bars[0], G::X_BYTES);
+      tma_load_3d(smem + G::X_BASE, &map_x, &bars[0], gx0 - 1 - PADX, gy0 - 1, pl_of(qfirst) + 1);
+      for (int q = qfirst; q <= min(qfirst + PD, qlast); ++q)
+        issue(q, (q + 1 - qfirst) % NXB, (q - qfirst) % NB);
+    } else {
+      for (int q = qfirst; q <= min(qfirst + PD, qlast); ++q) issue(q, (q - qfirst) % NXB, (q - qfirst) % NB);
+    }
+  }
   mbar_wait(&bars[0], 0);
-  if (qfirst + 1 <= qlast) mbar_wait(&bars[1], 0);
+  if (RK_CHAIN_XLEAD || qfirst + 1 <= qlast) mbar_wait(&bars[1], 0);
   int xsm = 0, xs0 = 1, xsp = 2 % NXB;
   uint32_t parp = 0;
   int bs0 = 1 % NB;
-  int xsi = (PD + 1) % NXB, bsi = (PD + 1) % NB;
+  int xsi = (PD + 1 + RK_CHAIN_XLEAD) % NXB, bsi = (PD + 1) % NB;
   auto adv = [](int& v, int n) { v = (v + 1 == n) ? 0 : v + 1; };
 
   double2 bnd[3][ST], rr[3], inv[3];
@@ -219,6 +235,7 @@ chain_kernel_x2(const __grid_constant__ CUtensorMap map_b, const __grid_constant
   // z-column registers: input pair at planes tau, tau-1 (tiles of slots 1, 0
   // at tau0) and the stage outputs of the two previous steps
   double2 xc = *reinterpret_cast<const double2*>(xtile(1)), xm = *reinterpret_cast<const double2*>(xtile(0));
+  if (RK_CHAIN_XLEAD) __syncthreads();   // slot 0 (tile qfirst) is refilled at the first step
   const double2 zero2 = make_double2(0.0, 0.0);
   double2 h1c = zero2, h1m = zero2, h2c = zero2, h2m = zero2;
   const int tau_end = z1 + HALO;
