@@ -37,6 +37,12 @@
 // RK_CHAIN_TMA_INVD = 1 streams that band instead (one more array per plane).
 // RK_CHAIN_XLEAD = 1: the x-pair kernel's TMA batches carry the input tile one
 // plane ahead of the bands (chain_x2.cuh); 0: the same plane.
+// RK_CHAIN_MIDSYNC = 1 (needs RK_CHAIN_XLEAD): the x-pair kernel's barrier sits
+// after stage 0's shared-memory loads and the next batch is issued right
+// after it, one plane further ahead (chain_x2.cuh).
+#ifndef RK_CHAIN_MIDSYNC
+#define RK_CHAIN_MIDSYNC 1
+#endif
 #ifndef RK_CHAIN_XLEAD
 #define RK_CHAIN_XLEAD 1
 #endif

@@ -51,14 +51,16 @@ struct ChainStepX2 {
     return make_double2(a0 + b0, a1 + b1);
   }
 
-  // xc / xm: this thread's input pair at planes tau and tau-1 (registers,
-  // z-column reuse); the pair at tau+1 is read from the tile and becomes xc
-  static __device__ __forceinline__ double2 stage0(bool st_ok, int pl_tau, const unsigned char* sb,
-                                                   const double* x0, const double* xp,
-                                                   double2& xc, double2& xm, double* ring,
-                                                   double2 (&bnd)[3][ST], double2 (&rr)[3],
-                                                   double2 (&inv)[3], int64_t cxy, int boff,
-                                                   int roff, const ChainParams& cp) {
+  // stage 0's shared-memory operands of plane tau: the bands / 1/D / rhs go
+  // to this phase's registers, the input tile's in-plane neighbours of the
+  // pair and the pair at tau+1 (from the next tile) to X0
+  struct X0 {
+    double l, r;
+    double2 ym, yp, xnext;
+  };
+  static __device__ __forceinline__ X0 load0(const unsigned char* sb, const double* x0, const double* xp,
+                                             double2 (&bnd)[3][ST], double2 (&rr)[3], double2 (&inv)[3],
+                                             int boff) {
     constexpr bool LOAD_R = (K0 != CK_SPMV1);
     const double* bs = reinterpret_cast<const double*>(sb) + boff;
 #pragma unroll
@@ -70,6 +72,21 @@ struct ChainStepX2 {
       inv[PH].y = bnd[PH][0].y != 0.0 ? 1.0 / bnd[PH][0].y : 0.0;
     }
     if (LOAD_R) rr[PH] = ld2(reinterpret_cast<const double*>(sb + G::R_OFF) + boff);
+    X0 n;
+    n.l = x0[-1];
+    n.r = x0[2];
+    n.ym = ld2(x0 - XX);
+    n.yp = ld2(x0 + XX);
+    n.xnext = ld2(xp);
+    return n;
+  }
+
+  // xc / xm: this thread's input pair at planes tau and tau-1 (registers,
+  // z-column reuse); the pair at tau+1 (n.xnext) becomes xc
+  static __device__ __forceinline__ double2 compute0(bool st_ok, int pl_tau, double2& xc, double2& xm,
+                                                     double* ring, double2 (&bnd)[3][ST], double2 (&rr)[3],
+                                                     double2 (&inv)[3], int64_t cxy, int roff,
+                                                     const ChainParams& cp, const X0& n) {
     bool cut_m = false, cut_p = false;   // block-Jacobi local sweep (R17)
     if (cp.zb > 0 && cp.local[0]) {
       const int g = cp.zg0 + pl_tau;
@@ -77,14 +94,11 @@ struct ChainStepX2 {
       cut_p = ((g + 1) % cp.zb) == 0;
     }
     const double2 c = xc;
-    const double l = x0[-1], r = x0[2];
-    const double2 ym = ld2(x0 - XX), yp = ld2(x0 + XX);
-    const double2 xnext = ld2(xp);
     const double2 zm = cut_m ? make_double2(0.0, 0.0) : xm;
-    const double2 zp = cut_p ? make_double2(0.0, 0.0) : xnext;
+    const double2 zp = cut_p ? make_double2(0.0, 0.0) : n.xnext;
     xm = xc;
-    xc = xnext;
-    const double2 y = apply7(bnd[PH], c, l, r, ym, yp, zm, zp);
+    xc = n.xnext;
+    const double2 y = apply7(bnd[PH], c, n.l, n.r, n.ym, n.yp, zm, zp);
     double2 val;
     if (K0 == CK_SPMV1) {
       rr[PH] = y;
@@ -96,13 +110,23 @@ struct ChainStepX2 {
       val = y;
     }
     if (st_ok) {
-      const int64_t n = (int64_t)pl_tau * cp.P + cxy;
-      if (K0 == CK_SPMV1 && cp.out_t) st2(cp.out_t + n, y);
-      if (NST == 1) st2(cp.out + n, val);
-      if (NST == 2 && cp.out_mid) st2(cp.out_mid + n, val);
+      const int64_t nn = (int64_t)pl_tau * cp.P + cxy;
+      if (K0 == CK_SPMV1 && cp.out_t) st2(cp.out_t + nn, y);
+      if (NST == 1) st2(cp.out + nn, val);
+      if (NST == 2 && cp.out_mid) st2(cp.out_mid + nn, val);
     }
     if (NST > 1) st2(ring + PH * RPL + roff, val);
     return val;
+  }
+
+  static __device__ __forceinline__ double2 stage0(bool st_ok, int pl_tau, const unsigned char* sb,
+                                                   const double* x0, const double* xp,
+                                                   double2& xc, double2& xm, double* ring,
+                                                   double2 (&bnd)[3][ST], double2 (&rr)[3],
+                                                   double2 (&inv)[3], int64_t cxy, int boff,
+                                                   int roff, const ChainParams& cp) {
+    const X0 n = load0(sb, x0, xp, bnd, rr, inv, boff);
+    return compute0(st_ok, pl_tau, xc, xm, ring, bnd, rr, inv, cxy, roff, cp, n);
   }
 
   // hc / hm: stage S-1's outputs for this thread at planes q and q-1
@@ -175,6 +199,9 @@ chain_kernel_x2(const __grid_constant__ CUtensorMap map_b, const __grid_constant
   const int tau0 = z0 - HALO;
   const int qfirst = tau0 - 1;
   const int qlast = z1 + HALO;
+  // last batch to issue: every issued batch is waited for before the CTA
+  // exits (no bulk copy may land in shared memory after it is released)
+  const int qiss = RK_CHAIN_XLEAD ? qlast - 1 : qlast;
   const uint32_t tx_bytes = G::B_BYTES + (LOAD_R ? G::R_BYTES : 0) + G::X_BYTES;
   const int xoff = (ty + 1) * XX + tx + 1 + PADX;
   const int boff = ty * SX + tx + PADB;
@@ -206,12 +233,23 @@ chain_kernel_x2(const __grid_constant__ CUtensorMap map_b, const __grid_constant
   }
   __syncthreads();
   if (tid == 0) {
-    if (RK_CHAIN_XLEAD) {
+    if (RK_CHAIN_MIDSYNC) {
+      // tiles qfirst and tau0 alone, then batches tau0 .. tau0 + PD - 1 (the
+      // bands of qfirst are never used); batch tau0 + PD follows the barrier
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(&bars[0], G::X_BYTES);
+      tma_load_3d(smem + G::X_BASE, &map_x, &bars[0], gx0 - 1 - PADX, gy0 - 1, pl_of(qfirst) + 1);
+      mbar_expect_tx(&bars[1], G::X_BYTES);
+      tma_load_3d(smem + G::X_BASE + G::XSLOT, &map_x, &bars[1], gx0 - 1 - PADX, gy0 - 1,
+                  pl_of(qfirst + 1) + 1);
+      for (int q = qfirst + 1; q <= min(qfirst + PD, qiss); ++q)
+        issue(q, (q + 1 - qfirst) % NXB, (q - qfirst - 1) % NB);
+    } else if (RK_CHAIN_XLEAD) {
       // the first tile alone, then batches qfirst .. qfirst + PD
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_expect_tx(&bars[0], G::X_BYTES);
       tma_load_3d(smem + G::X_BASE, &map_x, &bars[0], gx0 - 1 - PADX, gy0 - 1, pl_of(qfirst) + 1);
-      for (int q = qfirst; q <= min(qfirst + PD, qlast); ++q)
+      for (int q = qfirst; q <= min(qfirst + PD, qiss); ++q)
         issue(q, (q + 1 - qfirst) % NXB, (q - qfirst) % NB);
     } else {
       for (int q = qfirst; q <= min(qfirst + PD, qlast); ++q) issue(q, (q - qfirst) % NXB, (q - qfirst) % NB);
@@ -221,7 +259,7 @@ chain_kernel_x2(const __grid_constant__ CUtensorMap map_b, const __grid_constant
   if (RK_CHAIN_XLEAD || qfirst + 1 <= qlast) mbar_wait(&bars[1], 0);
   int xsm = 0, xs0 = 1, xsp = 2 % NXB;
   uint32_t parp = 0;
-  int bs0 = 1 % NB;
+  int bs0 = RK_CHAIN_MIDSYNC ? 0 : 1 % NB;
   int xsi = (PD + 1 + RK_CHAIN_XLEAD) % NXB, bsi = (PD + 1) % NB;
   auto adv = [](int& v, int n) { v = (v + 1 == n) ? 0 : v + 1; };
 
@@ -236,13 +274,15 @@ chain_kernel_x2(const __grid_constant__ CUtensorMap map_b, const __grid_constant
   // at tau0) and the stage outputs of the two previous steps
   double2 xc = *reinterpret_cast<const double2*>(xtile(1)), xm = *reinterpret_cast<const double2*>(xtile(0));
   if (RK_CHAIN_XLEAD) __syncthreads();   // slot 0 (tile qfirst) is refilled at the first step
+  if (RK_CHAIN_MIDSYNC && tid == 0 && tau0 + PD <= qiss)
+    issue(tau0 + PD, (tau0 + PD + 1 - qfirst) % NXB, PD % NB);
   const double2 zero2 = make_double2(0.0, 0.0);
   double2 h1c = zero2, h1m = zero2, h2c = zero2, h2m = zero2;
   const int tau_end = z1 + HALO;
 #define RK_CHAIN2_STEP(PHV)                                                                        \
   {                                                                                                \
     if (tau >= tau_end) break;                                                                     \
-    if (!RK_CHAIN_COMPUTEONLY && tid == 0 && tau + PD <= qlast) issue(tau + PD, xsi, bsi);         \
+    if (!RK_CHAIN_COMPUTEONLY && tid == 0 && tau + PD <= qiss) issue(tau + PD, xsi, bsi);          \
     if (!RK_CHAIN_COMPUTEONLY && tau + 1 <= qlast) mbar_wait(&bars[xsp], parp);                    \
     using SP = ChainStepX2<ST, NST, TX, TY, PD, K0, K1, K2, PHV>;                                  \
     if (RK_CHAIN_LOADONLY) {                                                                       \
@@ -289,11 +329,62 @@ chain_kernel_x2(const __grid_constant__ CUtensorMap map_b, const __grid_constant
     adv(bsi, NB);                                                                                  \
     ++tau;                                                                                         \
   }
-  for (int tau = tau0; tau < tau_end;) {
-    RK_CHAIN2_STEP(0)
-    RK_CHAIN2_STEP(1)
-    RK_CHAIN2_STEP(2)
+// RK_CHAIN_MIDSYNC: one barrier per step placed after stage 0's shared-memory
+// loads; right after it the slots of plane tau's bands and tile are free and
+// batch tau + PD + 1 is issued into them (a TMA lead of ~PD + 1 steps with
+// the same slots).  The barrier also orders the previous step's ring writes
+// before stages 1-2 read them, and every ring slot written in this step was
+// last read two barriers earlier.
+#define RK_CHAIN2_STEP_MS(PHV)                                                                     \
+  {                                                                                                \
+    if (tau >= tau_end) break;                                                                     \
+    if (!RK_CHAIN_COMPUTEONLY && tau + 1 <= qlast) mbar_wait(&bars[xsp], parp);                    \
+    using SP = ChainStepX2<ST, NST, TX, TY, PD, K0, K1, K2, PHV>;                                  \
+    const typename SP::X0 n0 = SP::load0(smem + bs0 * G::BSLOT, xtile(xs0), xtile(xsp), bnd, rr,   \
+                                         inv, boff);                                               \
+    __syncthreads();                                                                               \
+    if (!RK_CHAIN_COMPUTEONLY && tid == 0 && tau + PD + 1 <= qiss) issue(tau + PD + 1, xs0, bs0);  \
+    const double2 v0 = SP::compute0(interior && tau >= z0 && tau < z1 && (pz || tau < nz),        \
+                                    pl_of(tau), xc, xm, ring, bnd, rr, inv, cxy, roff, cp, n0);    \
+    if constexpr (NST >= 2) {                                                                      \
+      double2 v1 = zero2;                                                                          \
+      if (tau >= tau0 + 2) {                                                                       \
+        const int q = tau - 1;                                                                     \
+        v1 = SP::template stage<1>(interior && q >= z0 && q < z1, pl_of(q), ring, bnd, rr, inv,    \
+                                   cxy, roff, h1c, h1m, v0, cp);                                   \
+      }                                                                                            \
+      if constexpr (NST >= 3) {                                                                    \
+        if (tau >= tau0 + 4) {                                                                     \
+          const int q = tau - 2;                                                                   \
+          SP::template stage<2>(interior && q >= z0 && q < z1, pl_of(q), ring, bnd, rr, inv, cxy, \
+                                roff, h2c, h2m, v1, cp);                                           \
+        }                                                                                          \
+        h2m = h2c;                                                                                 \
+        h2c = v1;                                                                                  \
+      }                                                                                            \
+      h1m = h1c;                                                                                   \
+      h1c = v0;                                                                                    \
+    }                                                                                              \
+    xs0 = xsp;                                                                                     \
+    adv(xsp, NXB);                                                                                 \
+    if (xsp == 0) parp ^= 1u;                                                                      \
+    adv(bs0, NB);                                                                                  \
+    ++tau;                                                                                         \
   }
+  if constexpr (RK_CHAIN_MIDSYNC) {
+    for (int tau = tau0; tau < tau_end;) {
+      RK_CHAIN2_STEP_MS(0)
+      RK_CHAIN2_STEP_MS(1)
+      RK_CHAIN2_STEP_MS(2)
+    }
+  } else {
+    for (int tau = tau0; tau < tau_end;) {
+      RK_CHAIN2_STEP(0)
+      RK_CHAIN2_STEP(1)
+      RK_CHAIN2_STEP(2)
+    }
+  }
+#undef RK_CHAIN2_STEP_MS
 #undef RK_CHAIN2_STEP
 }
 
