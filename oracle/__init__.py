@@ -9,10 +9,14 @@ reference` legs may import it.  The product package
 two meet only on the seeded inputs from `problems/`.
 
 Pins (what ties each function to something other than itself) are listed
-in each module header and in DESIGN.md "Oracle and pins".  One function is
-"parity unpinned" beyond properties: the line-14a recycle-space update
-rule (krylov.gcrot_update), because the paper names it without giving an
-algorithm (P:337-338).
+in each module header and in DESIGN.md "Oracle and pins".  The line-14a
+recycle-space update (krylov.gcrot_update) is pinned by what one cycle
+fixes -- every added column comes from the cycle's search space (the
+post-cycle residual is orthogonal to all of C), u1 is parallel to the
+cycle's correction, A_hat U = C, C^T C = I, T1 keeps the newest columns --
+but the paper names the step without an algorithm, so which
+second candidate p1 = 2 picks (argmax |y_j|, reading D11) is a choice no
+passage can pin.
 """
 from .stencil import Operator, shifted, to_dense, jacobi, Jacobi
 from .krylov import (

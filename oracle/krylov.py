@@ -16,8 +16,11 @@ rGCROT to GMRES(m) and rBiCGStab to BiCGStab; BiCGStab
 iterates equal scipy.sparse.linalg.bicgstab's; rBiCGStab's pre-17a
 iterates equal scipy's BiCGStab run on A_C = (I - C C^T) A (eq. (8)-(9));
 invariants C^T C = I, A_hat U = C, V _|_ C, eq. (5); dense direct solves.
-The line-14a update rule itself is PARITY UNPINNED beyond those
-invariants (the paper gives no algorithm).
+The line-14a update is pinned by what one cycle fixes (every added
+column from the cycle's search space: the post-cycle residual is
+orthogonal to all of C; u1 parallel to the cycle's correction; the
+invariants above); the choice of the p1 = 2 candidate is a reading (D11)
+the paper gives no algorithm for.
 """
 from dataclasses import dataclass, field
 
@@ -73,7 +76,10 @@ def refresh_space(apply_op, U):
 # ----------------------------------------------------------------- line 14a
 def gcrot_update(U, C, V, H, B, y, dx, rho, prm):
     """Alg. 3 line 14a "Update U and C if desired" -- reading
-    [D11], PARITY UNPINNED beyond the invariants A_hat U = C, C^T C = I.
+    [D11].  Pinned by test_gcrot_update_columns_from_the_cycle (added
+    columns from the cycle's search space, u1 parallel to the correction,
+    A_hat U = C, C^T C = I) and test_gcrot_update_truncation_T1; the p1 = 2
+    candidate choice is the reading's, not the paper's.
 
     Extension by the normalised cycle correction: with zeta = H_ y and
     gamma = ||zeta||, u1 = dx/gamma and c1 = V_{m+1} zeta/gamma, so that

@@ -320,6 +320,40 @@ def test_gcrot_update_truncation_T1():
     assert abs(C2[:, 1] @ C2[:, 2]) <= 1e-14
 
 
+@pytest.mark.parametrize("p1", [1, 2])
+def test_gcrot_update_columns_from_the_cycle(p1):
+    """Line 14a (reading D11) against what one rGCROT cycle fixes, not
+    against its own formulas: the cycle's correction minimises the residual
+    over range(U) + K_m (eqs. (6)-(7)), so the post-cycle preconditioned
+    residual is orthogonal to A_hat of the whole search space.  Every column
+    the update adds comes from that space (c1 = A_hat u1 with u1 the
+    normalised correction; c2 = A_hat u2, u2 in span(V_j*, U)), hence
+    C_new^T r_new = 0; u1 is parallel to the cycle's correction itself (x
+    minus line 1b's projection U C^T r_hat0, x0 = 0); A_hat U = C and
+    C^T C = I.  A new column taken from the Krylov
+    basis itself (V rather than V_{m+1} h) or from the uncorrected x would
+    fail the first two checks."""
+    prob = channel19(6)
+    op, pc, b = _setup(prob)
+    U, C = _random_space(op, pc, 3, seed=5)
+    m = 5
+    prm = SolverParams(m=m, k_max=6, k_t=4, p1=p1, tol=1e-30, max_mv=m)
+    x, U2, C2, rep = rgcrot(op, pc, b, U.copy(), C.copy(), prm)
+    assert rep.cycles == 1 and U2.shape[1] == 3 + p1
+    rn = pc(b - op.apply(x))
+    assert np.linalg.norm(C2.T @ rn) <= 1e-10 * np.linalg.norm(rn)
+    # the cycle's own correction: x minus line 1b's projection U C^T r_hat0
+    dx = x - U @ (C.T @ pc(b))
+    u1 = U2[:, 3]
+    cos = abs(u1 @ dx) / (np.linalg.norm(u1) * np.linalg.norm(dx))
+    assert abs(cos - 1.0) <= 1e-12
+    AU = np.column_stack([pc(op.apply(U2[:, i])) for i in range(U2.shape[1])])
+    assert np.linalg.norm(AU - C2) <= 1e-11 * np.linalg.norm(U2)
+    assert np.linalg.norm(C2.T @ C2 - np.eye(C2.shape[1])) <= 1e-12
+    # the old columns are kept as they were (no truncation at k = 3 + p1 <= k_max)
+    assert np.array_equal(U2[:, :3], U) and np.array_equal(C2[:, :3], C)
+
+
 def test_t2_directions_are_principal_vectors():
     """T2 (reading R13): the kept directions C W are the principal vectors
     of range(C) w.r.t. the cycle's image space [C V_{m+1}] [B; H_]
