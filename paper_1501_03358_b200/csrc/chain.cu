@@ -439,10 +439,23 @@ void launch_one(rk_op* op, ChainParams cp, dim3 grid) {
   static_assert(G::SMEM <= 232448, "chain tile exceeds 227 KB of shared memory");
   using KernFn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, ChainParams);
   KernFn kern;
-  if constexpr (X2 != 0) kern = chain_kernel_x2<ST, NST, TX, TY, PD, K0, K1, K2>;
-  else kern = chain_kernel<ST, NST, TX, TY, PD, K0, K1, K2>;
+  int fl = 0;   // x-pair kernel flavour: block-Jacobi cuts (1), periodic z (2)
+  if constexpr (X2 != 0) {
+    bool cuts = false;
+    for (int s = 0; s < NST; ++s) cuts = cuts || (cp.zb > 0 && cp.local[s]);
+    fl = (cuts ? 1 : 0) | (cp.pz ? 2 : 0);
+    switch (fl) {
+      case 0: kern = chain_kernel_x2<ST, NST, TX, TY, PD, K0, K1, K2, 0>; break;
+      case 1: kern = chain_kernel_x2<ST, NST, TX, TY, PD, K0, K1, K2, 1>; break;
+      case 2: kern = chain_kernel_x2<ST, NST, TX, TY, PD, K0, K1, K2, 2>; break;
+      default: kern = chain_kernel_x2<ST, NST, TX, TY, PD, K0, K1, K2, 3>; break;
+    }
+  } else {
+    kern = chain_kernel<ST, NST, TX, TY, PD, K0, K1, K2>;
+  }
   const int nthr = X2 ? G::NTHR / 2 : G::NTHR;
-  static int occ = 0;   // resident CTAs per SM of this instantiation
+  static int occs[4] = {0, 0, 0, 0};   // resident CTAs per SM of each instantiation
+  int& occ = occs[fl];
   if (!occ) {
     RK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
     RK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nthr, G::SMEM));

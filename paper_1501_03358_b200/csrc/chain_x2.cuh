@@ -16,7 +16,9 @@
 
 namespace rk {
 
-template <int ST, int NST, int TX, int TY, int PD, int K0, int K1, int K2, int PH>
+// FL bit 0: block-Jacobi cuts may apply (cp.zb > 0 and a local stage);
+// bit 1: periodic z.  Launches without them compile the checks out.
+template <int ST, int NST, int TX, int TY, int PD, int K0, int K1, int K2, int PH, int FL>
 struct ChainStepX2 {
   using G = ChainGeom<ST, NST, TX, TY, PD>;
   static constexpr int EX = G::EX, EY = G::EY, XX = G::XX, SX = G::SX, RPL = EY * EX;
@@ -88,7 +90,7 @@ struct ChainStepX2 {
                                                      double2 (&inv)[3], int64_t cxy, int roff,
                                                      const ChainParams& cp, const X0& n) {
     bool cut_m = false, cut_p = false;   // block-Jacobi local sweep (R17)
-    if (cp.zb > 0 && cp.local[0]) {
+    if ((FL & 1) && cp.zb > 0 && cp.local[0]) {
       const int g = cp.zg0 + pl_tau;
       cut_m = (g % cp.zb) == 0;
       cut_p = ((g + 1) % cp.zb) == 0;
@@ -143,7 +145,7 @@ struct ChainStepX2 {
     const double* rb = ring + (S - 1) * 3 * RPL + roff;
     const double* r0 = rb + R * RPL;
     bool cut_m = false, cut_p = false;   // block-Jacobi local sweep (R17)
-    if (cp.zb > 0 && cp.local[S]) {
+    if ((FL & 1) && cp.zb > 0 && cp.local[S]) {
       const int g = cp.zg0 + pl_q;
       cut_m = (g % cp.zb) == 0;
       cut_p = ((g + 1) % cp.zb) == 0;
@@ -168,7 +170,7 @@ struct ChainStepX2 {
   }
 };
 
-template <int ST, int NST, int TX, int TY, int PD, int K0, int K1, int K2>
+template <int ST, int NST, int TX, int TY, int PD, int K0, int K1, int K2, int FL>
 __global__ void __launch_bounds__((TX + 2 * (NST - 1)) * (TY + 2 * (NST - 1)) / 2, 1)
 chain_kernel_x2(const __grid_constant__ CUtensorMap map_b, const __grid_constant__ CUtensorMap map_r,
                 const __grid_constant__ CUtensorMap map_x, ChainParams cp) {
@@ -187,7 +189,7 @@ chain_kernel_x2(const __grid_constant__ CUtensorMap map_b, const __grid_constant
   const int tx = 2 * (int)threadIdx.x, ty = threadIdx.y;   // first cell of the pair
   const int tid = threadIdx.y * blockDim.x + threadIdx.x;
   const int nx = cp.nx, ny = cp.ny, nz = cp.nz;
-  const bool pz = cp.pz != 0;
+  constexpr bool pz = (FL & 2) != 0;   // periodic z (the host picks FL from cp.pz)
   const int gx0 = (int)blockIdx.x * TX - HALO, gy0 = (int)blockIdx.y * TY - HALO;
   const int gx = gx0 + tx, gy = gy0 + ty;
   // nx even and gx even: both cells of a pair are inside or outside together
@@ -284,7 +286,7 @@ chain_kernel_x2(const __grid_constant__ CUtensorMap map_b, const __grid_constant
     if (tau >= tau_end) break;                                                                     \
     if (!RK_CHAIN_COMPUTEONLY && tid == 0 && tau + PD <= qiss) issue(tau + PD, xsi, bsi);          \
     if (!RK_CHAIN_COMPUTEONLY && tau + 1 <= qlast) mbar_wait(&bars[xsp], parp);                    \
-    using SP = ChainStepX2<ST, NST, TX, TY, PD, K0, K1, K2, PHV>;                                  \
+    using SP = ChainStepX2<ST, NST, TX, TY, PD, K0, K1, K2, PHV, FL>;                                  \
     if (RK_CHAIN_LOADONLY) {                                                                       \
       __syncthreads();                                                                             \
       xsm = xs0;                                                                                   \
@@ -339,7 +341,7 @@ chain_kernel_x2(const __grid_constant__ CUtensorMap map_b, const __grid_constant
   {                                                                                                \
     if (tau >= tau_end) break;                                                                     \
     if (!RK_CHAIN_COMPUTEONLY && tau + 1 <= qlast) mbar_wait(&bars[xsp], parp);                    \
-    using SP = ChainStepX2<ST, NST, TX, TY, PD, K0, K1, K2, PHV>;                                  \
+    using SP = ChainStepX2<ST, NST, TX, TY, PD, K0, K1, K2, PHV, FL>;                                  \
     const typename SP::X0 n0 = SP::load0(smem + bs0 * G::BSLOT, xtile(xs0), xtile(xsp), bnd, rr,   \
                                          inv, boff);                                               \
     __syncthreads();                                                                               \
