@@ -200,12 +200,17 @@ __global__ void __launch_bounds__(256, 1) bdot_bulk_kernel(ColPtrs Q, int ncol, 
   const int64_t mytiles = ntile > blockIdx.x ? (ntile - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int per = ncol + NR;                        // items per tile: w (, v), Q_0 .. Q_{ncol-1}
   const int64_t nitem = mytiles * per;
-  // item -> source: tile blockIdx.x + (it / per) * gridDim.x, column it % per - NR (< 0: w, v)
-  auto issue = [&](int64_t it, int slot) {
-    const int64_t lt = it / per;
-    const int c = (int)(it - lt * per) - NR;
-    const int64_t row = (blockIdx.x + lt * gridDim.x) * BK_ROWS;
-    const double* src = (c < 0 ? (c + NR == 0 ? w : v) : Q.p[c]) + row;
+  // items in order: per tile (blockIdx.x, + gridDim.x, ...) w (, v), then
+  // Q_0 .. Q_{ncol-1}; thread 0 walks them with a cursor (no division on the
+  // issue path, which sits between two barriers)
+  int ic = -NR;
+  int64_t irow = (int64_t)blockIdx.x * BK_ROWS;
+  auto issue = [&](int64_t, int slot) {
+    const double* src = (ic < 0 ? (ic + NR == 0 ? w : v) : Q.p[ic]) + irow;
+    if (++ic == ncol) {
+      ic = -NR;
+      irow += (int64_t)gridDim.x * BK_ROWS;
+    }
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bk_smem(bar + slot)),
                  "r"(BK_BYTES)
                  : "memory");
