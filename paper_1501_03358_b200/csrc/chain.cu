@@ -46,6 +46,9 @@
 #ifndef RK_CHAIN_XLEAD
 #define RK_CHAIN_XLEAD 1
 #endif
+#if RK_CHAIN_MIDSYNC && !RK_CHAIN_XLEAD
+#error "RK_CHAIN_MIDSYNC needs RK_CHAIN_XLEAD (the batches carry the next plane's tile)"
+#endif
 #ifndef RK_CHAIN_TMA_INVD
 #define RK_CHAIN_TMA_INVD 1
 #endif
