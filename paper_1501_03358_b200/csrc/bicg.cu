@@ -15,6 +15,20 @@ __global__ void __launch_bounds__(256) bicg_p_kernel(const double* __restrict__ 
                                                      BiIter* cur, const BiIter* prev, int first,
                                                      double thr_conv, double thr_div) {
   RK_PDL_ENTRY();
+  // the first element's operands do not depend on the scalars below: their
+  // loads are issued before the scalar round trip
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t NE = N / VEC;
+  const int64_t e0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  Vec<VEC> r0v{}, p0v{}, v0v{}, d0v{};
+  if (e0 < NE) {
+    r0v = ldv_ro<VEC>(r + e0 * VEC);
+    if (!first) {
+      p0v = ldv<VEC>(p + e0 * VEC);
+      v0v = ldv_ro<VEC>(v + e0 * VEC);
+    }
+    if (D) d0v = ldv_stream<VEC>(D + e0 * VEC);
+  }
   // lookahead gate: every CTA takes the same decision from the records
   // written by the previous iteration (flag, sigma) and its bicg_xr (rho, rr)
   bool stop = false;
@@ -31,28 +45,34 @@ __global__ void __launch_bounds__(256) bicg_p_kernel(const double* __restrict__ 
     omega = prev->ts / prev->tt;
     beta = (cur->rho / prev->rho) * (alpha / omega);
   }
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const int64_t NE = N / VEC;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < NE; e += stride) {
-    const int64_t n = e * VEC;
-    const Vec<VEC> rn = ldv_ro<VEC>(r + n);
+  auto body = [&](int64_t n, const Vec<VEC>& rn, const Vec<VEC>& po, const Vec<VEC>& vn,
+                  const Vec<VEC>& dn) {
     Vec<VEC> pn;
     if (first) {
       pn = rn;
     } else {
-      const Vec<VEC> po = ldv<VEC>(p + n);
-      const Vec<VEC> vn = ldv_ro<VEC>(v + n);
 #pragma unroll
       for (int t = 0; t < VEC; ++t) pn.v[t] = rn.v[t] + beta * (po.v[t] - omega * vn.v[t]);
     }
     stv<VEC>(p + n, pn);
     Vec<VEC> zn = pn;
     if (D) {
-      const Vec<VEC> dn = ldv_stream<VEC>(D + n);
 #pragma unroll
       for (int t = 0; t < VEC; ++t) zn.v[t] = (wl * pn.v[t]) * dn.v[t];
     }
     stv<VEC>(z + n, zn);
+  };
+  if (e0 < NE) body(e0 * VEC, r0v, p0v, v0v, d0v);
+  for (int64_t e = e0 + stride; e < NE; e += stride) {
+    const int64_t n = e * VEC;
+    const Vec<VEC> rn = ldv_ro<VEC>(r + n);
+    Vec<VEC> po{}, vn{}, dn{};
+    if (!first) {
+      po = ldv<VEC>(p + n);
+      vn = ldv_ro<VEC>(v + n);
+    }
+    if (D) dn = ldv_stream<VEC>(D + n);
+    body(n, rn, po, vn, dn);
   }
 }
 
