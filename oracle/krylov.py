@@ -19,8 +19,19 @@ invariants C^T C = I, A_hat U = C, V _|_ C, eq. (5); dense direct solves.
 The line-14a update is pinned by what one cycle fixes (every added
 column from the cycle's search space: the post-cycle residual is
 orthogonal to all of C; u1 parallel to the cycle's correction; the
-invariants above); the choice of the p1 = 2 candidate is a reading (D11)
-the paper gives no algorithm for.
+invariants above).
+
+PARITY UNPINNED: the choice of the p1 = 2 candidate (j* = argmax |y_j|
+over j <= floor(m/2), reading D11) -- the paper gives no algorithm for
+line 14a, so nothing outside this oracle fixes which second
+column is added; only its properties (taken from the cycle's search
+space, A_hat U = C, C^T C = I) are pinned.
+
+Orthogonalisation (D8): `cgs2` (block classical Gram-Schmidt over
+[C V_j] applied twice, the default) or `mgs` (the literal loops of Alg. 3
+lines 6a-9).  librk's Gram-corrected CGS2 (R19) is NOT
+implemented here: the oracle stays the textbook scheme, and the GPU's
+one-update variant is checked against it.
 """
 from dataclasses import dataclass, field
 
@@ -204,7 +215,6 @@ def rgcrot(op, pc, b, U, C, prm, valid=True, hook=None):
         H = np.zeros((m + 1, m))
         Bm = np.zeros((k, m))
         V[:, 0] = r / rho                                  # line 4
-        Grow = np.zeros((k + m + 1, k + m + 1))            # cgs2g: lagged Gram rows
         m_eff = m
         for j in range(m):                                 # line 5
             w = ahat(V[:, j])                              # line 6
@@ -217,25 +227,6 @@ def rgcrot(op, pc, b, U, C, prm, valid=True, hook=None):
                 for l in range(j + 1):                     # lines 7-9
                     H[l, j] = V[:, l] @ w
                     w = w - V[:, l] * H[l, j]
-            elif prm.ortho == "cgs2g":
-                # [R19] CGS2 with the second pass taken from the Gram matrix:
-                # g = Q^T w, G = Q^T Q (C-block = I; the other rows are the
-                # lagged dots Q_j^T v_j of each step), h = g + (g - G g) =
-                # (2I - G) g -- CGS2's coefficients g1 + g2 in exact
-                # arithmetic -- and ONE update w -= Q h.
-                Q = np.column_stack([C, V[:, :j + 1]])
-                Grow[k + j, :k + j + 1] = Q.T @ V[:, j]      # lagged row of v_j
-                L = Grow[k:k + j + 1, :k + j + 1]                 # rows of v_0..v_j (lower part)
-                G = np.eye(k + j + 1)
-                G[k:, :] = L
-                G[:, k:] = L.T
-                Lv = L[:, k:]
-                G[k:, k:] = Lv + Lv.T - np.diag(np.diag(Lv))
-                g = Q.T @ w
-                h = 2.0 * g - G @ g
-                w = w - Q @ h
-                Bm[:, j] = h[:k]
-                H[:j + 1, j] = h[k:]
             else:
                 # [D8] block classical Gram-Schmidt over [C V_j], applied twice
                 Q = np.column_stack([C, V[:, :j + 1]])

@@ -126,8 +126,11 @@ def make_config(method="rgcrot", m=20, k_max=10, k_keep=5, select_count=1, preco
                        max_matvecs, divergence)
 
 
-def config_from_params(prm, method=None):
-    """rk_config from any object with SolverParams-like attributes."""
+def config_from_params(prm, method=None, ortho="cgs2g"):
+    """rk_config from any object with SolverParams-like attributes.  The
+    Arnoldi orthogonalisation is librk's own choice (`ortho`: the
+    Gram-corrected CGS2 of R19 by default, or "cgs2"); prm.ortho names the
+    oracle's scheme and is not used here."""
     meth = method or prm.method
     if meth == "hybrid":
         meth = "rgcrot"
@@ -139,7 +142,7 @@ def config_from_params(prm, method=None):
                        omega_g=prm.omega_g,
                        tol=prm.tol, max_matvecs=prm.max_mv, divergence=prm.divergence,
                        trunc=getattr(prm, "trunc", "T1"), zblocks=getattr(prm, "zblocks", 1),
-                       ortho=getattr(prm, "ortho", "cgs2g"))
+                       ortho=ortho)
 
 
 def _report(r):

@@ -25,7 +25,7 @@ class SolverParams:
     tol: float = 1e-8
     max_mv: int = 2000
     trunc: str = "T1"
-    ortho: str = "cgs2g"         # cgs2g (Gram-corrected CGS2, R19) | cgs2 (D8) | mgs (oracle only)
+    ortho: str = "cgs2"          # oracle: cgs2 (D8, block CGS applied twice) | mgs (Alg. 3 literal)
     sweeps: int = 5
     omega_l: float = 0.8
     omega_g: float = 1.0

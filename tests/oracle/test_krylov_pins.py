@@ -101,13 +101,13 @@ def test_rgcrot_cycle_is_optimal_over_U_plus_Krylov():
     assert np.linalg.norm(x - xb) <= 1e-8 * np.linalg.norm(xb)
 
 
-@pytest.mark.parametrize("ortho", ["cgs2", "cgs2g"])
+@pytest.mark.parametrize("ortho", ["cgs2"])
 def test_rgcrot_invariants_every_cycle(ortho):
     """Eq. (4) V _|_ C, eq. (5) A_hat V_m = C B + V_{m+1} H_, Arnoldi
     orthonormality, A_hat U = C and C^T C = I after line 14a,
-    residual _|_ C after each cycle (D20), monotone true residual -- for CGS2
-    (D8) and the Gram-corrected CGS2 (R19).  (The paper's MGS keeps V _|_ C
-    only to ~1e-9 here; it is compared in test_rgcrot_mgs_and_cgs2_agree.)"""
+    residual _|_ C after each cycle (D20), monotone true residual -- for the
+    oracle's CGS2 (D8).  (The paper's MGS keeps V orthonormal only to ~2e-12
+    here; it is compared in test_rgcrot_mgs_and_cgs2_agree.)"""
     w = get_workload("c2s")
     prob = w.problem()
     op, pc, _ = _setup(prob)
@@ -300,8 +300,11 @@ def test_recycling_reduces_matvecs_channel():
 
 
 def test_gcrot_update_truncation_T1():
-    """Line 14a bookkeeping: k never exceeds k_max, truncation keeps the
-    newest k_t - p old columns."""
+    """Line 14a bookkeeping under T1 ("drop the oldest"), checked
+    by properties only: k never exceeds k_max; the kept old columns are the
+    NEWEST k_t - p ones, untouched and in order; the new C columns lie in
+    range(V_{m+1}), have unit norm and are orthogonal to each other; u1 is
+    parallel to the cycle correction dx."""
     rng = np.random.default_rng(0)
     N, m, k = 40, 4, 5
     U = rng.standard_normal((N, k))
@@ -313,11 +316,44 @@ def test_gcrot_update_truncation_T1():
     dx = rng.standard_normal(N)
     prm = SolverParams(m=m, k_max=5, k_t=3, p1=2)
     U2, C2 = gcrot_update(U, C, V, H, B, y, dx, 1.0, prm)
-    assert U2.shape[1] == 3
-    assert np.array_equal(U2[:, 0], U[:, 4])
-    zeta = H @ y
-    assert np.allclose(C2[:, 1], V @ zeta / np.linalg.norm(zeta))
-    assert abs(C2[:, 1] @ C2[:, 2]) <= 1e-14
+    assert U2.shape[1] == 3 and C2.shape[1] == 3
+    assert np.array_equal(U2[:, 0], U[:, 4]) and np.array_equal(C2[:, 0], C[:, 4])
+    Cn = C2[:, 1:]
+    assert np.allclose(Cn.T @ Cn, np.eye(2), atol=1e-14)
+    assert np.linalg.norm(Cn - V @ (V.T @ Cn)) <= 1e-14
+    cos = abs(U2[:, 1] @ dx) / (np.linalg.norm(U2[:, 1]) * np.linalg.norm(dx))
+    assert abs(cos - 1.0) <= 1e-14
+    # without truncation (k_max large) every old column is kept
+    U3, C3 = gcrot_update(U, C, V, H, B, y, dx, 1.0, replace(prm, k_max=10, k_t=8))
+    assert U3.shape[1] == k + 2 and np.array_equal(U3[:, :k], U)
+
+
+def test_refresh_space_drops_dependent_column():
+    """Line 1a's rank-drop branch: when op(U) is rank deficient
+    (U's third column is a combination of the first two), the first column
+    whose QR pivot vanishes is dropped; the result still satisfies
+    op(U) = C, C^T C = I, and range(C) equals the column space of the
+    original op(U) (projectors compared against an SVD basis)."""
+    prob = convection_diffusion_c1(4)
+    op, pc, _ = _setup(prob)
+    rng = np.random.default_rng(3)
+    U0 = rng.standard_normal((op.N, 4))
+    U0[:, 2] = 0.5 * U0[:, 0] - 2.0 * U0[:, 1]
+    ahat = lambda v: pc(op.apply(v))
+    U, C, apps = refresh_space(ahat, U0.copy())
+    assert U.shape[1] == 3 and C.shape[1] == 3 and apps == 4 + 3
+    assert np.linalg.norm(C.T @ C - np.eye(3)) <= 1e-13
+    AU = np.column_stack([ahat(U[:, i]) for i in range(3)])
+    assert np.linalg.norm(AU - C) <= 1e-11 * np.linalg.norm(U)
+    AU0 = np.column_stack([ahat(U0[:, i]) for i in range(4)])
+    Us, sv, _ = np.linalg.svd(AU0, full_matrices=False)
+    assert sv[3] <= 1e-12 * sv[0]
+    P1 = Us[:, :3] @ Us[:, :3].T
+    assert np.linalg.norm(C @ C.T - P1) <= 1e-10
+    # the dropped column is the dependent one (index 2): columns 0, 1, 3 span U
+    Ukeep = U0[:, [0, 1, 3]]
+    coef = np.linalg.lstsq(Ukeep, U, rcond=None)[0]
+    assert np.linalg.norm(Ukeep @ coef - U) <= 1e-10 * np.linalg.norm(U)
 
 
 @pytest.mark.parametrize("p1", [1, 2])
