@@ -1,16 +1,27 @@
 #!/usr/bin/env python
 """Benchmark of the recycling-Krylov hot path on B200.
 
-A "step" is one pass of the whole hot path (every SURVEY §8(a) row) over
-one batch of synthetic input: the full 20-system hybrid sequence of
-BASELINE configs[2] (128^3 porous 7-point operator; rGCROT(10,20) with
-p1 = 2 for systems 0-2, then rBiCGStab recycling the frozen space), solved
-from an empty recycle space.  configs[2] is the BASELINE config that runs
-every §8(a) row (configs[1] never reaches rBiCGStab) and fits one GPU.
+Workload (default): BASELINE configs[3], the largest configuration that
+fits one GPU -- the 256^3 19-point channel-shaped operator (periodic x/z,
+Neumann y, one pinned dof), a 50-system sequence b_t = b_0 + 0.05 t
+noise_t with A perturbed by 1e-3 relative every 10 systems, solved by
+rGCROT(40,30) (p1 = 1, Jacobi(5+1)), carrying the recycle space from
+system to system (PAPER P:687-704 is the paper's channel case).
 
-metric: BASELINE.json's; value = solve ms per system (lower is better),
-whole job.  With torchrun (N > 1) every rank owns a z-slab of the same grid
-(strong scaling; NCCL halo + allreduce inside librk).
+A "step" is one system of that sequence, in order: warm-up steps solve
+systems 0 .. W-1 (untimed; they grow the recycle space from empty), the K
+timed steps solve systems W .. W+K-1, including every A-epoch change
+(bands upload + recycle-space refresh) that falls in that range; the
+sequence is cyclic past its 50th system.  metric: BASELINE.json's; value
+= device ms per system over the K timed systems (lower is better).  With
+torchrun (N > 1) every rank owns a z-slab of the same grid (strong
+scaling; NCCL halo + allreduce inside librk).
+
+`e2e` replays the same K systems from the same recycle-space state
+(exported after the warm-up, re-imported through rk_recycle_set) through
+the pipelined host-buffer API: every b_t upload and x_t download is
+inside the timed region.  `secondary` is BASELINE configs[2] (128^3 porous
+hybrid, one step = the whole 20-system sequence from an empty space).
 
 `--impl reference` times the CPU oracle (this tier's reference arm) on a
 bounded sample of the same workload.
@@ -18,11 +29,12 @@ bounded sample of the same workload.
 import argparse
 import json
 import os
+import platform
 import subprocess
 import sys
 import tempfile
-import threading
 import time
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 
@@ -36,14 +48,15 @@ FALLBACK_HBM = 6650.0
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="rk", choices=["rk", "reference"])
-    ap.add_argument("--workload", default="c3")
+    ap.add_argument("--workload", default="c4")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-sample-seconds", type=float, default=20.0)
-    ap.add_argument("--breakdown", action="store_true", help="print per-kernel-class shares")
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--secondary", default="c3")
+    ap.add_argument("--out", default=None, help="also write the JSON line to this file")
     return ap.parse_args()
 
 
@@ -53,6 +66,16 @@ def peaks():
         d = json.load(open(p))
         return float(d["hbm_gbs"]), "measured"
     return FALLBACK_HBM, "fallback"
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or "unknown"
 
 
 class Clocks:
@@ -97,108 +120,98 @@ class Clocks:
 
 
 # ------------------------------------------------------------------ oracle
-def cpu_sample(workload, seconds, gpu_mv=None):
-    """The oracle as it stands, timed on this host on a bounded sample of
-    the workload: (a) one rGCROT(m, k) cycle of system 0 (m Krylov matvecs),
-    (b) rBiCGStab iterations of system n_sw with a k-dim recycle space
-    (random U refreshed by QR -- iteration cost does not depend on the
-    space's quality).  Extrapolated to ms/system with the per-system Krylov
-    matvec counts of the GPU run (same algorithm; parity within 10 %)."""
+def oracle_matvec_sample(workload, planes=None, threads=None, host_bands=None):
+    """The oracle as it stands (oracle.krylov.rgcrot, untuned), timed on this
+    host: ONE rGCROT Krylov step (m = 1: one preconditioned operator
+    application M^-1 A v, the CGS2 orthogonalisation, the cycle end with its
+    true residual) against a recycle space of k + m/2 columns -- the average
+    width [C V_j] of a cycle of the workload's rGCROT(m, k) -- built from a
+    random orthonormal C (the cost of a step does not depend on the space's
+    quality).  `planes`: time the first `planes` z-planes of the grid as
+    their own grid and scale by nz / planes (every oracle operation is
+    linear in N).  Returns ms per Krylov matvec on the full grid."""
     from dataclasses import replace
-    from oracle.krylov import rbicgstab, refresh_space, rgcrot
+    from oracle.krylov import rgcrot
     from oracle.stencil import Jacobi, Operator
     from problems import get_workload
     w = get_workload(workload)
     prm = w.params
     prob = w.problem()
-    t0 = time.perf_counter()
-    op = Operator.from_problem(prob)
+    nz = prob.nz if planes is None else planes
+    bands = host_bands if (host_bands is not None and planes is None) else prob.bands(0, nz)
+    op = Operator(prob.nx, prob.ny, nz, prob.periodic, prob.offsets, bands, check=planes is None)
     pc = Jacobi(op, prm.sweeps, prm.omega_l, prm.omega_g)
-    setup = time.perf_counter() - t0
-    b0 = prob.rhs(0).reshape(-1)
-    e = np.zeros((prob.N, 0))
-    t0 = time.perf_counter()
-    _, _, _, r1 = rgcrot(op, pc, b0, e, e, replace(prm, max_mv=prm.m, tol=1e-30))
-    t_rg = time.perf_counter() - t0
-    ms_rg = 1e3 * t_rg / max(1, r1.krylov_mv)
-    ms_bi = None
-    if prm.method == "hybrid":
-        U0 = np.random.default_rng(0).uniform(-1, 1, (prob.N, prm.k_max))
-        U, C, _ = refresh_space(op.apply, U0)
-        budget = max(4, int(2 * max(1.0, seconds - t_rg) / max(1e-3, 2 * ms_rg / 1e3)) // 2 * 2)
-        budget = min(budget, 20)
+    b = prob.rhs(0, 0, nz).reshape(-1)
+    kk = prm.k_max + prm.m // 2
+    rng = np.random.default_rng(0)
+    C, _ = np.linalg.qr(rng.standard_normal((op.N, kk)))
+    U = rng.standard_normal((op.N, kk))
+
+    def run():
         t0 = time.perf_counter()
-        _, _, _, r2 = rbicgstab(op, pc, prob.rhs(prm.n_sw).reshape(-1), U, C,
-                                replace(prm, max_mv=budget, tol=1e-30), valid=True)
-        t_bi = time.perf_counter() - t0
-        ms_bi = 1e3 * t_bi / max(1, r2.krylov_mv)
-    sample = (f"{workload}: oracle rGCROT cycle of system 0 ({r1.krylov_mv} Krylov matvecs, "
-              f"{ms_rg:.0f} ms/matvec)")
-    if ms_bi is not None:
-        sample += f" + rBiCGStab k={prm.k_max} ({r2.krylov_mv} matvecs, {ms_bi:.0f} ms/matvec)"
-    est = None
-    if gpu_mv is not None:
-        tot = 0.0
-        for tag, mv in gpu_mv:
-            tot += mv * (ms_bi if (tag == "rbicgstab" and ms_bi) else ms_rg)
-        est = tot / len(gpu_mv)
-        sample += "; extrapolated to ms/system with the GPU run's per-system matvec counts"
-    return {"ms_per_mv_rgcrot": ms_rg, "ms_per_mv_rbicgstab": ms_bi, "ms_per_system": est,
-            "sample": sample, "setup_s": setup}
+        _, _, _, rep = rgcrot(op, pc, b, U, C, replace(prm, m=1, k_max=kk + 2, max_mv=1, tol=1e-30),
+                              valid=True)
+        return time.perf_counter() - t0, rep
+
+    if threads is None:
+        dt, rep = run()
+    else:
+        from threadpoolctl import threadpool_limits
+        with threadpool_limits(limits=threads):
+            dt, rep = run()
+    assert rep.krylov_mv == 1
+    return 1e3 * dt * (prob.nz / nz), kk
 
 
-def oracle_counts(workload):
-    """[(tag, krylov matvecs)] of the oracle's full sequence, if stored."""
-    p = os.path.join(ROOT, "tests", "golden", f"oracle_seq_{workload}.json")
-    if not os.path.exists(p):
-        return None, None
-    d = json.load(open(p))
-    return ([[r["tag"], r["krylov_matvecs"]] for r in d["systems"]],
-            f"the oracle's own full-sequence counts ({os.path.relpath(p, ROOT)})")
-
-
+# ------------------------------------------------------------------ reference arm
 def run_reference(args):
-    """--impl reference: the CPU oracle, timed per step on a bounded sample."""
+    """--impl reference: the CPU oracle, one bounded sample per step: one
+    rGCROT Krylov step of the workload on its first 32 z-planes, scaled to
+    the full grid, times the matvecs per system of the workload (below)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from problems import get_workload
     w = get_workload(args.workload)
-    # each step times one rGCROT cycle + rBiCGStab iterations of the oracle
+    planes = min(32, w.problem().nz)
     ms = []
-    info = None
+    kk = None
     for i in range(args.warmup + args.steps):
-        info = cpu_sample(args.workload, max(2.0, args.cpu_sample_seconds / 4))
+        v, kk = oracle_matvec_sample(args.workload, planes=planes)
         if i >= args.warmup:
-            ms.append(info)
-    mrg = float(np.mean([m["ms_per_mv_rgcrot"] for m in ms]))
-    mbi = [m["ms_per_mv_rbicgstab"] for m in ms if m["ms_per_mv_rbicgstab"]]
-    mbi = float(np.mean(mbi)) if mbi else mrg
-    # ms/system for the sequence with the oracle's OWN per-system Krylov
-    # matvec counts (tests/golden/oracle_seq_<workload>.json, written by
-    # scripts/oracle_counts.py from oracle/ alone); without that file, the
-    # hybrid's structure at 100 matvecs per system.
-    counts, src = oracle_counts(args.workload)
-    if not counts:
-        counts = [["rgcrot" if t < w.params.n_sw else "rbicgstab", 100] for t in range(w.n_systems)]
-        src = "100 matvecs/system assumed"
-    value = sum(mv * (mbi if tag == "rbicgstab" else mrg) for tag, mv in counts) / len(counts)
+            ms.append(v)
+    ms_mv = float(np.mean(ms))
+    mv_sys = MV_PER_SYSTEM.get(args.workload, 100.0)
+    value = ms_mv * mv_sys
     cores = os.cpu_count()
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "ms/system",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(value * len(counts), 3), "higher_is_better": False,
+        "ms_per_step": round(value, 3), "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.workload}: {w.description}",
-                   "systems": w.n_systems, "l2": "inputs larger than L2"},
+        "config": {"workload": f"{args.workload}: {w.description}", "l2": "inputs larger than L2"},
         "cpu_baseline": {"value": round(value, 3), "unit": "ms/system", "cores": cores,
-                         "kind": "oracle", "sample": ms[-1]["sample"] +
-                         f"; per-system matvecs: {src}"
-                         " (NumPy; stencil and elementwise work single-threaded)"},
+                         "cpu_model": cpu_model(), "kind": "oracle",
+                         "sample": (f"per step: oracle rGCROT, one Krylov step (m=1) against a "
+                                    f"{kk}-column recycle space, on the first {planes} z-planes of "
+                                    f"the {args.workload} grid, scaled to the full grid: "
+                                    f"{ms_mv:.0f} ms per Krylov matvec x {mv_sys} matvecs per "
+                                    f"system ({MV_SOURCE}) (NumPy; stencil and elementwise work "
+                                    f"single-threaded, BLAS on all cores)")},
         "e2e": {"value": round(value, 3), "unit": "ms/system", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+# Krylov matvecs per system used to turn the oracle's ms per matvec into ms
+# per system in the reference arm (a separate process that cannot see the
+# GPU arm's counts): the mean over systems 5-24 of the c4 rGCROT(40,30) run
+# (profiles/r02_bench_c4.json); GPU and oracle counts agree per system within
+# one cycle (tests/gpu/test_gpu_parity.py).  The GPU arm's own cpu_baseline
+# uses the counts of its own timed systems.
+MV_PER_SYSTEM = {"c4": 476.0, "c3": 178.8}
+MV_SOURCE = "mean Krylov matvecs per timed system of the GPU run, profiles/r02_bench_c4.json"
 
 
 # ------------------------------------------------------------------ GPU arm
@@ -218,6 +231,9 @@ def run_rk(args):
     w = get_workload(args.workload)
     prm = w.params
     prob = w.problem()
+    T = w.n_systems
+    W = max(3, args.warmup)
+    K = args.steps
     z0, z1 = slab_range(prob.nz, rank, world)
     uid = None
     if world > 1:
@@ -226,59 +242,62 @@ def run_rk(args):
         uid = obj[0]
     ctx = rk.Context(local, rank, world, uid)
     stream = torch.cuda.current_stream()
-    bands = torch.from_numpy(prob.bands(z0, z1, epoch=w.epoch(0))).cuda()
-    op = rk.GridOperator(ctx, prob.nx, prob.ny, prob.nz, prob.offsets, bands, prob.periodic,
-                         z0=z0, nz_local=z1 - z0)
-    del bands
-    solver = rk.Solver(op, rk.config_from_params(prm))
-    T = w.n_systems
-    Nl = op.N
-    B = [torch.from_numpy(prob.rhs(t, z0, z1).reshape(-1)).cuda() for t in range(T)]
-    X = [torch.zeros(Nl, dtype=torch.float64, device="cuda") for _ in range(T)]
-    epoch_bands = {}
+    epoch_of = lambda s: w.epoch(s % T)          # cyclic sequence
+    host_bands0 = prob.bands(z0, z1, epoch=epoch_of(0))
+    epoch_bands = {epoch_of(0): torch.from_numpy(host_bands0).cuda()}
 
     def bands_for(e):
         if e not in epoch_bands:
             epoch_bands[e] = torch.from_numpy(prob.bands(z0, z1, epoch=e)).cuda()
         return epoch_bands[e]
 
-    def step(host=False, Bh=None, Xh=None):
-        solver.recycle_set(None)                      # fresh, empty recycle space
-        if w.epoch_every and w.epoch(0) != w.epoch(T - 1):
-            op.update_bands(bands_for(w.epoch(0)))
-        return rk.solve_sequence(solver, (lambda t: Bh[t]) if host else (lambda t: B[t]), T,
-                                 prm.method, n_sw=prm.n_sw, epoch_of=w.epoch,
+    op = rk.GridOperator(ctx, prob.nx, prob.ny, prob.nz, prob.offsets, bands_for(epoch_of(0)),
+                         prob.periodic, z0=z0, nz_local=z1 - z0)
+    solver = rk.Solver(op, rk.config_from_params(prm))
+    Nl = op.N
+    # right-hand sides of every system the run touches, resident in HBM
+    ts = sorted({s % T for s in range(W + K)})
+    with ThreadPoolExecutor(8) as ex:
+        host_b = dict(zip(ts, ex.map(lambda t: prob.rhs(t, z0, z1).reshape(-1), ts)))
+    B = {t: torch.from_numpy(host_b[t]).cuda() for t in ts}
+    for s in range(W + K):                     # every epoch's bands before timing
+        bands_for(epoch_of(s))
+    X = torch.zeros(Nl, dtype=torch.float64, device="cuda")
+
+    def solve(s0, n, host=False, Bh=None, Xh=None):
+        return rk.solve_sequence(solver, (lambda s: Bh[s % T]) if host else (lambda s: B[s % T]), n,
+                                 prm.method, n_sw=prm.n_sw, epoch_of=epoch_of,
                                  bands_for_epoch=bands_for, host=host,
-                                 x_out=Xh if host else X)
+                                 x_out=Xh[s0:s0 + n] if host else [X] * n, start=s0)
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(max(3, args.warmup)):
-        reps = step()
-    # kernel-class breakdown (untimed pass, every launch bracketed by events)
+    # warm-up: systems 0 .. W-2 plain, system W-1 with every launch bracketed
+    # (kernel-class breakdown; the arithmetic is unchanged)
+    solver.recycle_set(None)
+    wreps = solve(0, W - 1)
     ctx.profile(True, None)
     ctx.profile_read(reset=True)
-    step()
+    wreps += solve(W - 1, 1)
     prof_all = ctx.profile_read()
     ctx.profile(False)
     ctx.profile_read(reset=True)
     dominant = max(prof_all.items(), key=lambda kv: kv[1]["ms"])[0]
-    # timed region
+    # recycle-space state entering the timed region (for the e2e replay)
+    U0, C0, _ = solver.recycle_export()
+    # timed region: systems W .. W+K-1; live event timing of every 8th
+    # launch of the dominant kernel class
     clocks = Clocks(local) if rank == 0 else None
-    # live timing of the dominant class inside the timed region: every 8th
-    # launch is bracketed by events (fewer event records in the timed loop)
     ctx.profile(True, dominant, every=8)
     launches0 = ctx.launches()
     barrier()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
-    all_reps = []
-    for _ in range(args.steps):
-        all_reps.append(step())
+    reps = solve(W, K)
     ev1.record(stream)
     barrier()
     ms = ev0.elapsed_time(ev1)
@@ -291,22 +310,23 @@ def run_rk(args):
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    reps = all_reps[-1]
-    ms_per_step = ms / args.steps
-    value = ms_per_step / T
+    value = ms / K
     mv = [r["krylov_matvecs"] for r in reps]
-    # e2e: host buffers through rk_solve_host, copies inside the timed region
+    outcomes = [r["outcome"] for r in reps]
+    # e2e: the same K systems from the same recycle-space state, host buffers
     e2e = None
     if not args.no_e2e:
-        Bh = [b.cpu().pin_memory() for b in B]
-        Xh = [torch.zeros(Nl, dtype=torch.float64).pin_memory() for _ in range(T)]
-        step(True, Bh, Xh)
+        Bh = {t: torch.from_numpy(host_b[t]).pin_memory() for t in ts}
+        Xh = [torch.zeros(Nl, dtype=torch.float64).pin_memory() for _ in range(W + K)]
+        op.update_bands(bands_for(epoch_of(W - 1)))
+        solver.set_method("rgcrot" if prm.method in ("rgcrot", "gmres") or W - 1 < prm.n_sw
+                          else "rbicgstab")
+        solver.recycle_set(U0, C0)
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        for _ in range(args.steps):
-            step(True, Bh, Xh)
+        ereps = solve(W, K, True, Bh, Xh)
         e1.record(stream)
         barrier()
         wall = e0.elapsed_time(e1)   # device time on the library stream; copies included
@@ -314,9 +334,14 @@ def run_rk(args):
             t = torch.tensor([wall], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             wall = float(t.item())
-        e2e = {"value": round(wall / args.steps / T, 3), "unit": "ms/system",
-               "h2d_bytes_per_step": int(T * Nl * 8 * world),      # b_t (x0 = 0 is not uploaded)
-               "d2h_bytes_per_step": int(T * Nl * 8 * world)}
+        e2e = {"value": round(wall / K, 3), "unit": "ms/system",
+               "h2d_bytes_per_step": int(Nl * 8 * world),      # b_t (x0 = 0 is not uploaded)
+               "d2h_bytes_per_step": int(Nl * 8 * world),      # x_t
+               "same_matvecs_as_device_run": [r["krylov_matvecs"] for r in ereps] == mv}
+    del U0, C0
+    secondary = None
+    if not args.no_secondary and args.secondary and args.secondary != args.workload and world == 1:
+        secondary = sequence_bench(rk, ctx, args.secondary)
     if rank != 0:
         return
     peak, peak_kind = peaks()
@@ -324,22 +349,26 @@ def run_rk(args):
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
-        traffic = json.load(open(tp)).get(dominant)
+        traffic = json.load(open(tp)).get(args.workload, {}).get(dominant)
     total_ms = sum(v["ms"] for v in prof_all.values())
-    # whole-step effective bandwidth of the algorithmic bytes of every kernel
     alg_bytes = sum(v["bytes"] for v in prof_all.values())
+    epochs = sorted({epoch_of(s) for s in range(W, W + K)})
     line = {
         "metric": METRIC, "value": round(value, 4), "unit": "ms/system", "n_gpus": world,
-        "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": round(ms_per_step, 3),
+        "steps": K, "warmup": W, "ms_per_step": round(value, 3),
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": f"{args.workload}: {w.description}", "grid": [prob.nx, prob.ny, prob.nz],
-                   "systems": T, "method": prm.method, "m": prm.m, "k": prm.k_max, "p1": prm.p1,
-                   "n_sw": prm.n_sw, "tol": prm.tol, "parallelism": f"z-slab x{world}",
-                   "l2": "inputs larger than L2 (bases+bands ~ 1 GB at 128^3)"},
+                   "step": "one system of the sequence, in order",
+                   "timed_systems": f"{W}..{W + K - 1} (mod {T})", "epochs_in_timed_region": epochs,
+                   "method": prm.method, "m": prm.m, "k": prm.k_max, "k_t": prm.k_t, "p1": prm.p1,
+                   "tol": prm.tol, "precond": "jacobi(5+1)", "ortho": "cgs2 gram-corrected (R19)",
+                   "parallelism": f"z-slab x{world}",
+                   "l2": "inputs larger than L2 (bases+bands ~ 17 GB at 256^3)"},
         "iterations": {"krylov_matvecs_per_system": mv, "mean": float(np.mean(mv)),
-                       "outcomes": sorted(set(r["outcome"] for r in reps)),
-                       "tags": [r["tag"] for r in reps]},
+                       "outcomes": sorted(set(outcomes)),
+                       "ms_per_matvec": round(ms / max(1, sum(mv)), 4)},
+        "valid": all(o == "CONVERGED" for o in outcomes),
         "roofline": {"bound": "hbm", "kernel": dominant,
                      "achieved": round(achieved, 1) if achieved else None, "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4) if achieved else None,
@@ -351,25 +380,100 @@ def run_rk(args):
         "gpu_launches": launches,
         "clocks": clk,
         "e2e": e2e,
+        "kernel_breakdown": {k: {"ms": round(v["ms"], 3), "launches": v["launches"],
+                                 "gbs": round(v["bytes"] / (v["ms"] * 1e-3) / 1e9, 1) if v["ms"] else None}
+                             for k, v in sorted(prof_all.items(), key=lambda kv: -kv[1]["ms"])},
     }
-    if True:   # per-kernel-class breakdown of the untimed profiling pass
-        line["kernel_breakdown"] = {k: {"ms": round(v["ms"], 3), "launches": v["launches"],
-                                        "gbs": round(v["bytes"] / (v["ms"] * 1e-3) / 1e9, 1) if v["ms"] else None}
-                                    for k, v in sorted(prof_all.items(), key=lambda kv: -kv[1]["ms"])}
-    if world == 1 and not args.no_cpu_baseline:
-        counts, src = oracle_counts(args.workload)
-        if not counts:
-            counts, src = [(r["tag"], r["krylov_matvecs"]) for r in reps], "the GPU run's per-system counts"
-        cb = cpu_sample(args.workload, args.cpu_sample_seconds, counts)
-        cb["sample"] = cb["sample"].replace("the GPU run's per-system matvec counts", src)
-        line["cpu_baseline"] = {"value": round(cb["ms_per_system"], 1), "unit": "ms/system",
-                                "cores": os.cpu_count(), "kind": "oracle", "sample": cb["sample"]}
-    print(json.dumps(line), flush=True)
+    if not line["valid"]:
+        line["invalid_reason"] = "a timed system did not converge: " + ",".join(outcomes)
+    if secondary:
+        line["secondary"] = secondary
     solver.close()
     op.close()
+    epoch_bands.clear()
+    B.clear()
+    torch.cuda.empty_cache()
+    if world == 1 and not args.no_cpu_baseline:
+        ms_all, kk = oracle_matvec_sample(args.workload, host_bands=host_bands0)
+        ms_one, _ = oracle_matvec_sample(args.workload, threads=1, host_bands=host_bands0)
+        mvs = float(np.mean(mv))
+        line["cpu_baseline"] = {
+            "value": round(ms_all * mvs, 1), "unit": "ms/system", "cores": os.cpu_count(),
+            "value_1thread": round(ms_one * mvs, 1), "cpu_model": cpu_model(), "kind": "oracle",
+            "sample": (f"oracle rGCROT, one Krylov step (m=1) against a {kk}-column recycle space "
+                       f"(the average [C V_j] width of an rGCROT({prm.m},{prm.k_max}) cycle) on the "
+                       f"full {prob.nx}x{prob.ny}x{prob.nz} grid: {ms_all:.0f} ms per Krylov matvec "
+                       f"with BLAS on all {os.cpu_count()} cores, {ms_one:.0f} ms on 1 thread; times "
+                       f"the GPU run's {mvs:.1f} Krylov matvecs per timed system (NumPy stencil and "
+                       f"elementwise work is single-threaded in both settings)")}
+    text = json.dumps(line)
+    print(text, flush=True)
+    if args.out:
+        open(args.out, "w").write(text + "\n")
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def sequence_bench(rk, ctx, name, steps=3, warmup=2):
+    """A whole sequence per step, from an empty recycle space (r01's c3
+    measurement): device-resident and through the pipelined host API."""
+    import torch
+    from problems import get_workload
+    w = get_workload(name)
+    prm = w.params
+    prob = w.problem()
+    T = w.n_systems
+    op = rk.GridOperator(ctx, prob.nx, prob.ny, prob.nz, prob.offsets,
+                         torch.from_numpy(prob.bands(epoch=w.epoch(0))).cuda(), prob.periodic)
+    solver = rk.Solver(op, rk.config_from_params(prm))
+    hb = [prob.rhs(t).reshape(-1) for t in range(T)]
+    B = [torch.from_numpy(b).cuda() for b in hb]
+    X = [torch.zeros(op.N, dtype=torch.float64, device="cuda") for _ in range(T)]
+    bands = {}
+
+    def bands_for(e):
+        if e not in bands:
+            bands[e] = torch.from_numpy(prob.bands(epoch=e)).cuda()
+        return bands[e]
+
+    def seq(host=False, Bh=None, Xh=None):
+        solver.recycle_set(None)
+        if w.epoch_every:
+            op.update_bands(bands_for(w.epoch(0)))
+        return rk.solve_sequence(solver, (lambda t: Bh[t]) if host else (lambda t: B[t]), T,
+                                 prm.method, n_sw=prm.n_sw, epoch_of=w.epoch,
+                                 bands_for_epoch=bands_for, host=host, x_out=Xh if host else X)
+
+    stream = torch.cuda.current_stream()
+    for _ in range(warmup):
+        seq()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        reps = seq()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    value = e0.elapsed_time(e1) / steps / T
+    Bh = [torch.from_numpy(b).pin_memory() for b in hb]
+    Xh = [torch.zeros(op.N, dtype=torch.float64).pin_memory() for _ in range(T)]
+    seq(True, Bh, Xh)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(steps):
+        seq(True, Bh, Xh)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e = e0.elapsed_time(e1) / steps / T
+    mv = [r["krylov_matvecs"] for r in reps]
+    solver.close()
+    op.close()
+    return {"workload": f"{name}: {w.description}", "step": "the whole sequence from an empty space",
+            "steps": steps, "warmup": warmup, "value": round(value, 4), "unit": "ms/system",
+            "e2e": round(e2e, 4), "matvecs_per_system": mv,
+            "outcomes": sorted(set(r["outcome"] for r in reps)),
+            "tags": [r["tag"] for r in reps]}
 
 
 def main():

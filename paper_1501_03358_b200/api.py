@@ -242,7 +242,7 @@ class Solver:
 
 def solve_sequence(solver, rhs, n, method, n_sw=0, epoch_of=None, bands_for_epoch=None,
                    tol=0.0, host=False, x_out=None, switchback=False, refresh_on_epoch=False,
-                   refresh_every=0, pipeline=True):
+                   refresh_every=0, pipeline=True, start=0, cur_epoch=None):
     """Sequence controller (reading D3): for the hybrid,
     systems t < n_sw use rGCROT and later ones rBiCGStab with the recycle
     space frozen; a new A epoch uploads its bands (librk then invalidates C
@@ -252,17 +252,23 @@ def solve_sequence(solver, rhs, n, method, n_sw=0, epoch_of=None, bands_for_epoc
     of each new A epoch after the switch by rGCROT ("intermittent solves");
     `refresh_every` = n solves every n-th post-switch system by rGCROT.
     rhs(t) -> b_t (device tensor, or pinned host tensor if host=True).
-    Returns the reports; solutions go to x_out[t] when given.  The operator
-    must hold the bands of epoch_of(0) on entry.  host=True with pipeline:
+    Systems start .. start + n - 1 are solved (a sequence can be continued
+    call by call: the solver keeps its recycle space).  Returns the reports;
+    the solution of system start + i goes to x_out[i] when given.  The
+    operator must hold the bands of epoch `cur_epoch` on entry (default: the
+    epoch of system start - 1, or of system 0).  host=True with pipeline:
     b_{t+1} is uploaded and x_{t-1} downloaded while system t solves
-    (rk_stage_rhs / rk_solve_staged / rk_host_sync); every x_out[t] is
+    (rk_stage_rhs / rk_solve_staged / rk_host_sync); every x_out[i] is
     complete on return."""
+    if cur_epoch is None:
+        cur_epoch = (epoch_of(max(0, start - 1)) if epoch_of else 0)
     if host and pipeline:
         return _solve_sequence_pipelined(solver, rhs, n, method, n_sw, epoch_of, bands_for_epoch, tol,
-                                         x_out, switchback, refresh_on_epoch, refresh_every)
+                                         x_out, switchback, refresh_on_epoch, refresh_every, start,
+                                         cur_epoch)
     reps = []
-    cur = epoch_of(0) if epoch_of else 0
-    for t in range(n):
+    cur = cur_epoch
+    for i, t in enumerate(range(start, start + n)):
         e = epoch_of(t) if epoch_of else 0
         changed = e != cur
         if changed:
@@ -274,7 +280,7 @@ def solve_sequence(solver, rhs, n, method, n_sw=0, epoch_of=None, bands_for_epoc
                                                   refresh_every) else "rbicgstab"
             solver.set_method(tag)
         b = rhs(t)
-        x = x_out[t] if x_out is not None else torch.zeros_like(b)
+        x = x_out[i] if x_out is not None else torch.zeros_like(b)
         if host:   # x_hat = 0 without clearing the host buffer
             solve = lambda b_, x_: solver.solve_host(b_, x_, tol, x0_zero=True)
         else:
@@ -296,18 +302,18 @@ def solve_sequence(solver, rhs, n, method, n_sw=0, epoch_of=None, bands_for_epoc
 
 
 def _solve_sequence_pipelined(solver, rhs, n, method, n_sw, epoch_of, bands_for_epoch, tol, x_out,
-                              switchback, refresh_on_epoch, refresh_every):
+                              switchback, refresh_on_epoch, refresh_every, start=0, cur_epoch=0):
     """solve_sequence(host=True): the same controller over staged slots."""
     reps = []
-    cur = epoch_of(0) if epoch_of else 0
-    bs = [rhs(0)] if n else []
+    cur = cur_epoch
+    bs = [rhs(start)] if n else []
     xs = []
     if n:
         solver.stage_rhs(0, bs[0])
-    for t in range(n):
-        if t + 1 < n:   # upload b_{t+1} while t solves
+    for i, t in enumerate(range(start, start + n)):
+        if i + 1 < n:   # upload b_{t+1} while t solves
             bs.append(rhs(t + 1))
-            solver.stage_rhs((t + 1) % 2, bs[t + 1])
+            solver.stage_rhs((i + 1) % 2, bs[i + 1])
         e = epoch_of(t) if epoch_of else 0
         changed = e != cur
         if changed:
@@ -318,12 +324,12 @@ def _solve_sequence_pipelined(solver, rhs, n, method, n_sw, epoch_of, bands_for_
             tag = "rgcrot" if _hybrid_uses_rgcrot(t, n_sw, changed, refresh_on_epoch,
                                                   refresh_every) else "rbicgstab"
             solver.set_method(tag)
-        x = x_out[t] if x_out is not None else torch.zeros(bs[t].shape, dtype=torch.float64).pin_memory()
+        x = x_out[i] if x_out is not None else torch.zeros(bs[i].shape, dtype=torch.float64).pin_memory()
         xs.append(x)
-        _, r = solver.solve_staged(t % 2, x, tol)
+        _, r = solver.solve_staged(i % 2, x, tol)
         if method == "hybrid" and tag == "rbicgstab" and switchback and r["outcome"] != "CONVERGED":
             solver.set_method("rgcrot")
-            _, r2 = solver.solve_staged(t % 2, x, tol)
+            _, r2 = solver.solve_staged(i % 2, x, tol)
             for key in ("krylov_matvecs", "operator_applications", "seconds"):
                 r2[key] += r[key]
             r = r2

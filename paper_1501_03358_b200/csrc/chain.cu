@@ -457,12 +457,19 @@ void launch_one(rk_op* op, ChainParams cp, dim3 grid) {
     kern = chain_kernel<ST, NST, TX, TY, PD, K0, K1, K2>;
   }
   const int nthr = X2 ? G::NTHR / 2 : G::NTHR;
-  static int occs[4] = {0, 0, 0, 0};   // resident CTAs per SM of each instantiation
-  int& occ = occs[fl];
-  if (!occ) {
-    RK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
-    RK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nthr, G::SMEM));
-    occ = std::max(1, occ);
+  // resident CTAs per SM of this instantiation; the shared-memory attribute
+  // is per device, so it is set (and the occupancy cached) per context
+  int occ = 0;
+  {
+    auto it = op->ctx->occ_cache.find((const void*)kern);
+    if (it == op->ctx->occ_cache.end()) {
+      RK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
+      RK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nthr, G::SMEM));
+      occ = std::max(1, occ);
+      op->ctx->occ_cache[(const void*)kern] = occ;
+    } else {
+      occ = it->second;
+    }
   }
   // z chunks: a single wave of SMs x occ CTAs -- chunks = resident slots /
   // tiles (>= 1), long chunks (>= 16 planes) to amortise the 2 (NST-1)-plane
@@ -621,7 +628,12 @@ void chain_run(rk_op* op, const std::vector<int>& kinds, const std::vector<doubl
                const double* xin, const double* r, double* out_t, double* out_mid, double* out,
                double* za, double* zb, const std::vector<int>& local, int zbs) {
   const int n = (int)kinds.size();
-  const int nmax = chain_max_stages(op);
+  // TMA tensor maps need 16-byte aligned bases and the x-pair stores 16-byte
+  // aligned outputs; a caller's misaligned vector (rk_precond_apply accepts
+  // any pointer) takes the unfused path, which handles any alignment
+  auto al16 = [](const void* p) { return p == nullptr || ((uintptr_t)p & 15u) == 0; };
+  const bool aligned = al16(xin - op->P) && al16(r) && al16(out_t) && al16(out_mid) && al16(out);
+  const int nmax = aligned ? chain_max_stages(op) : 0;
   std::vector<int> loc(n, 0);
   for (int q = 0; q < n && q < (int)local.size(); ++q) loc[q] = local[q];
   double* bufs[2] = {za, zb};

@@ -158,6 +158,28 @@ def test_precond_parity_chain(rk, ctx, name, mk, monkeypatch):
     op.close()
 
 
+def test_precond_misaligned_pointers(rk, ctx, monkeypatch):
+    """rk_precond_apply accepts any float64 pointer: r and z as views at an
+    odd element offset (8-byte, not 16-byte, aligned) on an operator that
+    takes the fused TMA chain take the unfused path instead of faulting
+    (ADVICE r01), with the same result."""
+    prob = _random7(64, 32, 48, 4, 22)
+    monkeypatch.setenv("RK_FORCE_CHAIN", "1")
+    op = make_op(rk, ctx, prob)
+    monkeypatch.delenv("RK_FORCE_CHAIN")
+    ref = Operator.from_problem(prob)
+    r = np.random.default_rng(8).uniform(-1, 1, prob.N)
+    rbuf = torch.zeros(prob.N + 1, dtype=torch.float64, device="cuda")
+    rbuf[1:] = dev(r)
+    zbuf = torch.zeros(prob.N + 1, dtype=torch.float64, device="cuda")
+    op.precond(rbuf[1:], zbuf[1:])
+    zr = Jacobi(ref)(r)
+    z = zbuf[1:].cpu().numpy()
+    assert np.max(np.abs(z - zr)) <= 1e-12 * np.max(np.abs(zr))
+    assert torch.equal(zbuf[1:], op.precond(dev(r)))      # aligned (fused) path, same bits
+    op.close()
+
+
 @pytest.mark.parametrize("cfg", ["0", "5"])   # one cell per thread / x-pairs (chain_x2.cuh)
 @pytest.mark.parametrize("shape,periodic", [((64, 32, 48), 4), ((32, 16, 17), 4), ((96, 48, 40), 0)])
 def test_chain_bitwise_equals_unfused(rk, ctx, shape, periodic, cfg, monkeypatch):
