@@ -170,8 +170,12 @@ rk_status rk_solver_set_method(rk_solver* s, rk_method method);
  * method.  k = 0 empties the space.  k <= k_max. */
 rk_status rk_recycle_set(rk_solver* s, int k, const double* U, const double* C,
                          const double* R, int64_t ld);
+/* Current recycle dimension k (query before rk_recycle_export). */
 rk_status rk_recycle_dim(rk_solver* s, int* k);
-/* Copies U, C (DEVICE, ld) and R (HOST k x k, always I after absorption). */
+/* Copies U, C (DEVICE, ld) and R (HOST k x k, always I after absorption):
+ * the RecycleSpace dump of SPEC S:293-294 ("so hybrid runs can be
+ * checkpointed"); rk_recycle_set with the exported U and C (and R = NULL)
+ * restores it bit for bit.  Any of U, C, R may be NULL. */
 rk_status rk_recycle_export(rk_solver* s, double* U, double* C, double* R, int64_t ld);
 
 /* Solve A x = b (rGCROT/GMRES: Alg. 3/1 left-preconditioned; rBiCGStab/
@@ -205,9 +209,22 @@ rk_status rk_solve_host_ex(rk_solver* s, const double* b_host, const double* x0_
 rk_status rk_stage_rhs(rk_solver* s, int slot, const double* b_host);
 rk_status rk_solve_staged(rk_solver* s, int slot, double* x_host, double tol, rk_report* rep);
 rk_status rk_host_sync(rk_solver* s);
-/* Residual history of the last solve: rows (krylov_matvecs, ||b-Ax|| or NaN,
- * preconditioned / updated ||r||).  out is HOST [cap][3]. */
+/* Residual history of the last solve (SolveReport
+ * residual_history): rows (krylov_matvecs, ||b-Ax|| or NaN,
+ * preconditioned / updated ||r||).  out is HOST [cap][3]; *len = rows. */
 rk_status rk_history(rk_solver* s, double* out, int64_t cap, int64_t* len);
+/* Per-step trace of the last solve, for per-kernel parity against a CPU
+ * reference (the values librk's kernels produced, as read by the host).
+ * what = 0: one record per rGCROT/GMRES cycle (Alg. 3 lines 4-12):
+ *   k, m_eff, rho = ||r|| (line 4), |g_{m+1}| (LS residual), then
+ *   H_ ((m_eff+1) x m_eff, column-major; lines 7-10), B (k x m_eff,
+ *   column-major; line 6b: B(:,j) = C^T w_j), y (m_eff; line 12).
+ * what = 1: six doubles per rBiCGStab/BiCGStab iteration (Alg. 4 lines
+ *   4-15): rho_i = r~^T r_i, sigma_i = r~^T v_i (v projected, line 7a),
+ *   ||s_i||^2, t_i^T s_i, t_i^T t_i (t projected, line 12a; omega_i =
+ *   t^T s / t^T t), ||r_{i+1}||^2.
+ * out: HOST [cap] doubles (NULL to query); *len = doubles available. */
+rk_status rk_trace(rk_solver* s, int what, double* out, int64_t cap, int64_t* len);
 /* Workspace audit: number of N_local-length vectors allocated. */
 rk_status rk_solver_workspace(rk_solver* s, int64_t* nvec);
 

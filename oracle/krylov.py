@@ -281,12 +281,14 @@ def gmres(op, pc, b, prm):
 
 
 # ------------------------------------------------------------ O5 rBiCGStab
-def rbicgstab(op, pc, b, U, C, prm, valid=True, x_hat=None):
+def rbicgstab(op, pc, b, U, C, prm, valid=True, x_hat=None, hook=None):
     """Alg. 4 rBiCGStab with one recycle space, right preconditioned
     (P:148 [D2]): the iterated operator is A_C M^-1 with A_C = (I - C C^T) A
     (eq. (8)); x-updates use p_hat = M^-1 p, s_hat = M^-1 s [D22]; U-updates
     deferred in xi and applied once at line 17a.
-    Returns (x, U, C, report); (U, C) are frozen (only refreshed if invalid)."""
+    Returns (x, U, C, report); (U, C) are frozen (only refreshed if invalid).
+    hook(dict) is called after every completed iteration with its scalars
+    (rho, sigma, ||s||^2, t^T s, t^T t, ||r_{i+1}||^2; tests compare them)."""
     N = b.size
     rep = Report(bnorm=_norm(b))
     tol = prm.tol
@@ -355,6 +357,9 @@ def rbicgstab(op, pc, b, U, C, prm, valid=True, x_hat=None):
             r = s - omega * t                              # line 15
             rho_old = rho                                  # line 16
             i += 1
+            if hook is not None:
+                hook(dict(rho=rho, sigma=sigma, ss=float(s @ s), ts=float(t @ s), tt=tau,
+                          rr=float(r @ r), vv=float(v @ v), x=x, xi=xi))
             rep.history.append((rep.krylov_mv, float("nan"), _norm(r)))
             if _norm(r) > prm.divergence * r0n:            # [D17] instability
                 status = UNSTABLE

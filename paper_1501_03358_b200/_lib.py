@@ -84,6 +84,7 @@ def lib():
         "rk_solve_staged": ([vp, i32, vp, dbl, P(rk_report)], i32),
         "rk_host_sync": ([vp], i32),
         "rk_history": ([vp, vp, i64, P(i64)], i32),
+        "rk_trace": ([vp, i32, vp, i64, P(i64)], i32),
         "rk_solver_workspace": ([vp, P(i64)], i32),
         "rk_launch_count": ([vp, P(i64)], i32),
         "rk_profile_enable": ([vp, i32, C.c_char_p], i32),
@@ -110,5 +111,5 @@ EXPORTED = ["rk_last_error", "rk_version", "rk_nccl_unique_id", "rk_ctx_create",
             "rk_op_apply", "rk_precond_apply", "rk_solver_create", "rk_solver_destroy",
             "rk_solver_set_method", "rk_recycle_set", "rk_recycle_dim", "rk_recycle_export",
             "rk_solve", "rk_solve_host", "rk_solve_host_ex", "rk_stage_rhs", "rk_solve_staged",
-            "rk_host_sync", "rk_history", "rk_solver_workspace", "rk_launch_count",
+            "rk_host_sync", "rk_history", "rk_trace", "rk_solver_workspace", "rk_launch_count",
             "rk_profile_enable", "rk_profile_every", "rk_profile_read"]

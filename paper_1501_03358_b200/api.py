@@ -229,6 +229,33 @@ class Solver:
                 "rk_history")
         return out
 
+    def trace(self):
+        """Per-step trace of the last solve (rk_trace): a list of rGCROT cycle
+        dicts (k, m_eff, rho, lsres, H, B, y) and an [iterations x 6] array of
+        rBiCGStab scalars (rho, sigma, ss, ts, tt, rr_next)."""
+        out = []
+        for what in (0, 1):
+            n = C.c_int64()
+            L.check(L.lib().rk_trace(self.h, what, None, 0, C.byref(n)), "rk_trace")
+            buf = np.zeros(n.value)
+            L.check(L.lib().rk_trace(self.h, what, buf.ctypes.data_as(C.c_void_p), n.value,
+                                     C.byref(n)), "rk_trace")
+            out.append(buf)
+        cyc, pos = [], 0
+        v = out[0]
+        while pos < len(v):
+            k, m = int(v[pos]), int(v[pos + 1])
+            rho, lsres = v[pos + 2], v[pos + 3]
+            pos += 4
+            H = v[pos:pos + (m + 1) * m].reshape(m, m + 1).T.copy()
+            pos += (m + 1) * m
+            B = v[pos:pos + k * m].reshape(m, k).T.copy()
+            pos += k * m
+            y = v[pos:pos + m].copy()
+            pos += m
+            cyc.append({"k": k, "m_eff": m, "rho": rho, "lsres": lsres, "H": H, "B": B, "y": y})
+        return cyc, out[1].reshape(-1, 6)
+
     def workspace(self):
         n = C.c_int64()
         L.check(L.lib().rk_solver_workspace(self.h, C.byref(n)), "rk_solver_workspace")

@@ -408,6 +408,7 @@ chain_kernel(const __grid_constant__ CUtensorMap map_b, const __grid_constant__ 
 }  // namespace rk
 
 #include "chain_x2.cuh"
+#include "chain19.cuh"
 
 namespace rk {
 
@@ -568,10 +569,123 @@ void chain_dispatch_cfg(int ci, rk_op* op, const int* k, const ChainParams& cp, 
   }
 }
 
+// ------------------------------------------------------- 19-point chain
+// Tile of the 19-point chain (chain19.cuh): 32 x TY19 interior cells, TMA
+// prefetch distance PD19.
+constexpr int TY19 = 8, PD19 = 2, NST19 = 2;
+
+// z chunks for a one-CTA-per-SM kernel with `tiles` x-y tiles: the chunk
+// count c (chunks of >= 16 planes) maximising the wave efficiency
+// tiles c / (slots ceil(tiles c / slots)) times the share of steps that are
+// not wavefront prologue, zc / (zc + 2 halo + 1).
+int pick_chunks(int tiles, int slots, int nzl, int halo) {
+  int best = 1;
+  double bv = -1.0;
+  for (int c = 1; c <= std::max(1, nzl / 16); ++c) {
+    const int zc = (nzl + c - 1) / c;
+    const int ctas = tiles * ((nzl + zc - 1) / zc);
+    const int waves = (ctas + slots - 1) / slots;
+    const double v = (double)ctas / ((double)slots * waves) * zc / (zc + 2.0 * halo + 1.0);
+    if (v > bv + 1e-9) {
+      bv = v;
+      best = c;
+    }
+  }
+  return best;
+}
+
+template <int NST, int TX, int TY, int PD, int K0, int K1, int K2>
+void launch19(rk_op* op, ChainParams cp) {
+  using G = C19Geom<NST, TX, TY, PD>;
+  static_assert(G::SMEM <= 232448, "19-point chain tile exceeds 227 KB of shared memory");
+  using KernFn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap,
+                          const CUtensorMap, const CUtensorMap, ChainParams);
+  bool cuts = false;
+  for (int s = 0; s < NST; ++s) cuts = cuts || (cp.zb > 0 && cp.local[s]);
+  const int fl = (cuts ? 1 : 0) | (cp.pz ? 2 : 0);
+  KernFn kern;
+  switch (fl) {
+    case 0: kern = chain19_kernel<NST, TX, TY, PD, K0, K1, K2, 0>; break;
+    case 1: kern = chain19_kernel<NST, TX, TY, PD, K0, K1, K2, 1>; break;
+    case 2: kern = chain19_kernel<NST, TX, TY, PD, K0, K1, K2, 2>; break;
+    default: kern = chain19_kernel<NST, TX, TY, PD, K0, K1, K2, 3>; break;
+  }
+  rk_ctx* ctx = op->ctx;
+  int occ = 0;
+  {
+    auto it = ctx->occ_cache.find((const void*)kern);
+    if (it == ctx->occ_cache.end()) {
+      RK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
+      RK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, G::NTHR, G::SMEM));
+      occ = std::max(1, occ);
+      ctx->occ_cache[(const void*)kern] = occ;
+    } else {
+      occ = it->second;
+    }
+  }
+  const int nzl = (int)op->g.nz_local;
+  dim3 grid((unsigned)(op->g.nx / TX), (unsigned)(op->g.ny / TY), 1);
+  const int chunks = pick_chunks((int)(grid.x * grid.y), ctx->sms * occ, nzl, G::H);
+  const int zc = (nzl + chunks - 1) / chunks;
+  cp.zc = zc;
+  grid.z = (unsigned)((nzl + zc - 1) / zc);
+  const cuuint64_t nx = op->g.nx, ny = op->g.ny, nz = op->g.nz_local;
+  CUtensorMap mbM, mbH, mrM, mrH, mxM, mxH;
+  {
+    cuuint64_t dims[4] = {nx, ny, nz, (cuuint64_t)G::NBAND};
+    cuuint64_t str[3] = {nx * 8, nx * ny * 8, (cuuint64_t)op->N * 8};
+    cuuint32_t boxM[4] = {(cuuint32_t)TX, (cuuint32_t)G::EY, 1, (cuuint32_t)G::NBAND};
+    cuuint32_t boxH[4] = {(cuuint32_t)G::HW, (cuuint32_t)G::EY, 1, (cuuint32_t)G::NBAND};
+    encode(&mbM, cp.bands, 4, dims, str, boxM);
+    encode(&mbH, cp.bands, 4, dims, str, boxH);
+  }
+  {
+    cuuint64_t dims[3] = {nx, ny, nz};
+    cuuint64_t str[2] = {nx * 8, nx * ny * 8};
+    cuuint32_t boxM[3] = {(cuuint32_t)TX, (cuuint32_t)G::EY, 1};
+    cuuint32_t boxH[3] = {(cuuint32_t)G::HW, (cuuint32_t)G::EY, 1};
+    encode(&mrM, cp.r ? cp.r : cp.bands, 3, dims, str, boxM);
+    encode(&mrH, cp.r ? cp.r : cp.bands, 3, dims, str, boxH);
+  }
+  {
+    cuuint64_t dims[3] = {nx, ny, nz + 2};   // padded: ghost planes at 0, nz + 1
+    cuuint64_t str[2] = {nx * 8, nx * ny * 8};
+    cuuint32_t boxM[3] = {(cuuint32_t)TX, (cuuint32_t)G::XROWS, 1};
+    cuuint32_t boxH[3] = {(cuuint32_t)G::HW, (cuuint32_t)G::XROWS, 1};
+    encode(&mxM, cp.xin - op->P, 3, dims, str, boxM);
+    encode(&mxH, cp.xin - op->P, 3, dims, str, boxH);
+  }
+  const bool allow = ctx->pdl && (ctx->pdl_mode == 0 || ctx->pdl_mode == 3) && !ctx->pdl_skip_next;
+  ctx->pdl_skip_next = ctx->pdl_mode >= 2;
+  launch_pdl_if(ctx, allow, kern, grid, dim3(G::NTHR), G::SMEM, mbM, mbH, mrM, mrH, mxM, mxH, cp);
+}
+
+void chain19_dispatch(rk_op* op, int nst, const int* k, const ChainParams& cp) {
+  constexpr int TX = 32, TY = TY19, PD = PD19;
+  if (nst == 2) {
+    if (k[0] == CK_SPMV1 && k[1] == CK_SWEEP) return launch19<2, TX, TY, PD, CK_SPMV1, CK_SWEEP, 0>(op, cp);
+    if (k[0] == CK_SWEEP && k[1] == CK_SWEEP) return launch19<2, TX, TY, PD, CK_SWEEP, CK_SWEEP, 0>(op, cp);
+    if (k[0] == CK_SWEEP && k[1] == CK_SPMV) return launch19<2, TX, TY, PD, CK_SWEEP, CK_SPMV, 0>(op, cp);
+  } else if (nst == 1) {
+    if (k[0] == CK_SPMV1) return launch19<1, TX, TY, PD, CK_SPMV1, 0, 0>(op, cp);
+    if (k[0] == CK_SWEEP) return launch19<1, TX, TY, PD, CK_SWEEP, 0, 0>(op, cp);
+    return launch19<1, TX, TY, PD, CK_SPMV, 0, 0>(op, cp);
+  }
+  throw Error(RK_EINVAL, "unsupported 19-point chain stage combination");
+}
+
 }  // namespace
 
 int chain_max_stages(const rk_op* op) {
   if (op->ctx->nranks != 1 || op->no_chain) return 0;      // deep halos not exchanged (yet)
+  if (op->S == 19) {
+    // chain19.cuh: x-region boxes wrap a periodic x axis; y must not be periodic
+    if (op->g.periodic_mask & 2) return 0;
+    if (op->g.nx % 32 != 0 || op->g.ny % TY19 != 0 || op->g.nz_local < 16) return 0;
+    if (!op->force_chain && (double)(op->S + 3) * 8.0 * (double)op->N <= (double)op->ctx->l2_bytes)
+      return 0;
+    return NST19;
+  }
   if (op->S != 7) return 0;
   if (op->g.periodic_mask & 3) return 0;                    // TMA boxes do not wrap in x/y
   const TileCfg tc = CFGS[cfg_index()];
@@ -599,7 +713,7 @@ void chain_launch(rk_op* op, int nst, const int* kinds, const double* omegas, co
   cp.nx = (int)op->g.nx;
   cp.ny = (int)op->g.ny;
   cp.nz = (int)op->g.nz_local;
-  cp.px = 0;
+  cp.px = (op->S == 19 && (op->g.periodic_mask & 1)) ? 1 : 0;   // only the 19-point kernel wraps x
   cp.py = 0;
   cp.pz = (op->g.periodic_mask & 4) ? 1 : 0;
   cp.xin = xin;
@@ -617,8 +731,9 @@ void chain_launch(rk_op* op, int nst, const int* kinds, const double* omegas, co
   // 1/D array is an implementation choice -- flops for bytes -- and not counted)
   const double words = op->S + 1 + ((kinds[0] != CK_SPMV1) ? 1 : 0) + 1 + (out_t ? 1 : 0) +
                        (out_mid ? 1 : 0);
-  Launch L(ctx, "chain", 8.0 * op->N * words);
-  if (nst == 3) chain_dispatch_cfg<3>(ci, op, kinds, cp, grid);
+  Launch L(ctx, op->S == 19 ? "chain19" : "chain", 8.0 * op->N * words);
+  if (op->S == 19) chain19_dispatch(op, nst, kinds, cp);
+  else if (nst == 3) chain_dispatch_cfg<3>(ci, op, kinds, cp, grid);
   else if (nst == 2) chain_dispatch_cfg<2>(ci, op, kinds, cp, grid);
   else chain_dispatch_cfg<1>(ci, op, kinds, cp, grid);
   L.done();

@@ -1,0 +1,387 @@
+// 19-point variant of the fused preconditioned-operator chain (included by
+// chain.cu).  The channel operators of BASELINE configs[1]/[3] are 19-point
+// (non-orthogonal grids) with periodic x and z, and their
+// preconditioned operator is again a chain of 6 stencil stages over the same
+// S + 1 = 20 band arrays, so fusing stages saves ~20 W per stage.
+//
+// What differs from the 7-point kernels:
+//  * A 19-point stage at plane q reads the previous stage's values at planes
+//    q-1 and q+1 with in-plane (+-x, +-y) neighbours, not only the centre, so
+//    stage s (plane tau - s at step tau) reads stage s-1's plane computed in
+//    the SAME step by other threads: a barrier separates consecutive stages
+//    of a step (NST - 1 barriers per step) and the stage rings hold 4 planes.
+//  * The bands of a plane (20 x 8 B per cell) are 2.5x the 7-point ones, so
+//    the band tiles are smaller (TX x TY = 32 x 8 by default) and stay in
+//    registers from stage 0 (which loads them from shared memory) through
+//    the later stages of the plane.
+//  * Periodic x: every tile is staged as three x regions -- the left halo
+//    columns [gx0 - HW, gx0), the interior [gx0, gx0 + TX) and the right halo
+//    [gx0 + TX, gx0 + TX + HW) -- each brought by its own TMA box.  On a
+//    periodic x axis the halo boxes of the first / last tile start at the
+//    wrapped coordinate; otherwise they lie outside the grid and TMA
+//    zero-fills them (the zero-ghost semantics of non-periodic boundaries).
+//    A TMA box lands densely, so each region is its own [rows][width] array
+//    and every thread computes its neighbours' addresses once.
+//  * Threads: one per cell.  Warps 0 .. EY-1 own the interior columns of one
+//    tile row each (32 lanes = TX columns: conflict-free, row-aligned shared
+//    loads); the last warps own the 2 H halo columns of every row.
+// Per-cell arithmetic (band order, two FMA chains, 1/D band) is that of
+// stencil_kernel<19>, so fused and unfused paths agree bit for bit.
+#pragma once
+
+namespace rk {
+
+template <int NST, int TX, int TY, int PD>
+struct C19Geom {
+  static constexpr int ST = 19, NBAND = 20;           // bands + 1/D
+  static constexpr int H = NST - 1;                    // recomputed halo of stage 0
+  static constexpr int EY = TY + 2 * H;                // stage-0 rows
+  static constexpr int EX = TX + 2 * H;                // stage-0 columns (ring pitch)
+  static constexpr int HW = (H + 2) / 2 * 2;           // halo region width: even, >= H + 1
+  static constexpr int XROWS = EY + 2;                 // input tile rows (+1 y halo)
+  static_assert(TX == 32, "one warp per tile row");
+  static constexpr int NWM = EY;                       // interior-column warps
+  static constexpr int NHALO = 2 * H * EY;             // halo-column cells
+  static constexpr int NWH = (NHALO + 31) / 32;
+  static constexpr int NTHR = 32 * (NWM + NWH);
+  static constexpr int NB = PD + 1;                    // band / rhs slots
+  static constexpr int NXB = PD + 3;                   // input-tile slots (planes tau-1 .. tau+PD+2)
+  __host__ __device__ static constexpr int al(int b) { return (b + 127) / 128 * 128; }
+  // band slot: regions L, M, R, each [NBAND][EY][w]
+  static constexpr int BL_BYTES = NBAND * EY * HW * 8, BM_BYTES = NBAND * EY * TX * 8;
+  static constexpr int B_BYTES = 2 * BL_BYTES + BM_BYTES;
+  static constexpr int RL_BYTES = EY * HW * 8, RM_BYTES = EY * TX * 8;
+  static constexpr int R_BYTES = 2 * RL_BYTES + RM_BYTES;
+  static constexpr int XL_BYTES = XROWS * HW * 8, XM_BYTES = XROWS * TX * 8;
+  static constexpr int X_BYTES = 2 * XL_BYTES + XM_BYTES;
+  // region offsets inside a slot (bytes): L at 0, M, R (16-byte aligned: TMA destinations)
+  static constexpr int B_M = al(BL_BYTES), B_R = B_M + al(BM_BYTES);
+  static constexpr int BSLOT = B_R + al(BL_BYTES);
+  static constexpr int R_M = al(RL_BYTES), R_R = R_M + al(RM_BYTES);
+  static constexpr int RSLOT = R_R + al(RL_BYTES);
+  static constexpr int X_M = al(XL_BYTES), X_R = X_M + al(XM_BYTES);
+  static constexpr int XSLOT = X_R + al(XL_BYTES);
+  static constexpr int RBASE = NB * BSLOT;                      // rhs slots
+  static constexpr int XBASE = RBASE + NB * RSLOT;              // input tiles
+  static constexpr int RING_BASE = XBASE + NXB * XSLOT;         // stage rings [NST-1][4][EY][EX]
+  static constexpr int RING = (NST > 1 ? NST - 1 : 1) * 4 * EY * EX * 8;
+  static constexpr int BAR_BASE = RING_BASE + al(RING);
+  static constexpr int SMEM = BAR_BASE + 8 * NXB + 128;
+};
+
+// Offsets (in doubles, within one slot) of a cell in a region-split tile:
+// column c relative to the tile's first interior column, row r.
+template <int TX, int HW>
+__device__ __forceinline__ int region_off(int c, int r, int m_off, int r_off) {
+  if (c < 0) return r * HW + (c + HW);
+  if (c >= TX) return r_off + r * HW + (c - TX);
+  return m_off + r * TX + c;
+}
+template <int TX, int HW>
+__device__ __forceinline__ int region_pitch(int c) {
+  return (c < 0 || c >= TX) ? HW : TX;
+}
+
+// KIND of stage s; FL bit 0: block-Jacobi cuts possible, bit 1: periodic z.
+template <int NST, int TX, int TY, int PD, int K0, int K1, int K2, int FL>
+__global__ void __launch_bounds__(C19Geom<NST, TX, TY, PD>::NTHR, 1)
+chain19_kernel(const __grid_constant__ CUtensorMap mbM, const __grid_constant__ CUtensorMap mbH,
+               const __grid_constant__ CUtensorMap mrM, const __grid_constant__ CUtensorMap mrH,
+               const __grid_constant__ CUtensorMap mxM, const __grid_constant__ CUtensorMap mxH,
+               ChainParams cp) {
+  RK_PDL_ENTRY();
+  RK_GATE(cp.gate);
+  using G = C19Geom<NST, TX, TY, PD>;
+  constexpr int H = G::H, EY = G::EY, EX = G::EX, HW = G::HW, NB = G::NB, NXB = G::NXB;
+  constexpr int NBAND = G::NBAND;
+  constexpr bool LOAD_R = (K0 != CK_SPMV1);
+  constexpr int KIND[3] = {K0, K1, K2};
+  constexpr bool pz = (FL & 2) != 0;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + G::BAR_BASE);
+  double* ring = reinterpret_cast<double*>(smem + G::RING_BASE);
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  // this thread's cell: column c (relative to the interior), row ry of the stage-0 region
+  int c, ry;
+  bool active;
+  if (warp < G::NWM) {
+    c = lane;
+    ry = warp;
+    active = true;
+  } else {
+    const int e = (warp - G::NWM) * 32 + lane;   // halo cell index
+    active = e < G::NHALO;
+    const int ee = active ? e : 0;
+    const int col = ee / EY;                     // 0 .. 2H-1
+    ry = ee - col * EY;
+    c = col < H ? col - H : TX + (col - H);      // -H .. -1, TX .. TX+H-1
+  }
+  const int nx = cp.nx, ny = cp.ny, nz = cp.nz;
+  const int gx0 = (int)blockIdx.x * TX, gy0 = (int)blockIdx.y * TY - H;
+  int gx = gx0 + c;
+  if (cp.px) gx = gx < 0 ? gx + nx : (gx >= nx ? gx - nx : gx);
+  const int gy = gy0 + ry;
+  const bool inside = gx >= 0 && gx < nx && gy >= 0 && gy < ny;
+  const bool interior = active && c >= 0 && c < TX && ry >= H && ry < H + TY && inside;
+  const int64_t cxy = inside ? (int64_t)gy * nx + gx : 0;
+  // shared-memory offsets (doubles) of the own cell in a band / rhs slot and
+  // of the 3 x 3 in-plane neighbourhood in an input tile
+  const int boff = region_off<TX, HW>(c, ry, G::B_M / 8, G::B_R / 8);   // band 0
+  const int bstr = EY * region_pitch<TX, HW>(c);                        // band stride
+  const int roff = region_off<TX, HW>(c, ry, G::R_M / 8, G::R_R / 8);
+  int xo[3][3];
+#pragma unroll
+  for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+    for (int dx = -1; dx <= 1; ++dx)
+      xo[dy + 1][dx + 1] = region_off<TX, HW>(c + dx, ry + 1 + dy, G::X_M / 8, G::X_R / 8);
+  const int gofs = ry * EX + (c + H);   // own cell in a ring plane
+
+  const int z0 = (int)blockIdx.z * cp.zc;
+  const int z1 = min(nz, z0 + cp.zc);
+  const int tau0 = z0 - H;
+  const int tau_end = z1 + H;
+  const int qfirst = tau0 - 1, qlast = tau_end;   // input planes read
+  const uint32_t tx_bytes = G::B_BYTES + (LOAD_R ? G::R_BYTES : 0) + G::X_BYTES;
+  auto pl_of = [&](int q) { return pz ? (q < 0 ? q + nz : (q >= nz ? q - nz : q)) : q; };
+  // x coordinates of the three region boxes (wrapped on a periodic x axis)
+  int xl = gx0 - HW, xr = gx0 + TX;
+  if (cp.px) {
+    xl = xl < 0 ? xl + nx : xl;
+    xr = xr >= nx ? xr - nx : xr;
+  }
+  auto issue_x = [&](int q, int xs) {   // input tile of plane q (padded vector: z = pl + 1)
+    unsigned char* xb = smem + G::XBASE + xs * G::XSLOT;
+    const int z = pl_of(q) + 1;
+    tma_load_3d(xb, &mxH, &bars[xs], xl, gy0 - 1, z);
+    tma_load_3d(xb + G::X_M, &mxM, &bars[xs], gx0, gy0 - 1, z);
+    tma_load_3d(xb + G::X_R, &mxH, &bars[xs], xr, gy0 - 1, z);
+  };
+  // batch q: bands / rhs of plane q and the input tile of plane q + 1, on
+  // the mbarrier of that tile's slot
+  auto issue = [&](int q, int xs, int bs) {
+    unsigned char* bb = smem + bs * G::BSLOT;
+    unsigned char* rb = smem + G::RBASE + bs * G::RSLOT;
+    const int pl = pl_of(q);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(&bars[xs], tx_bytes);
+    tma_load_4d(bb, &mbH, &bars[xs], xl, gy0, pl, 0);
+    tma_load_4d(bb + G::B_M, &mbM, &bars[xs], gx0, gy0, pl, 0);
+    tma_load_4d(bb + G::B_R, &mbH, &bars[xs], xr, gy0, pl, 0);
+    if (LOAD_R) {
+      tma_load_3d(rb, &mrH, &bars[xs], xl, gy0, pl);
+      tma_load_3d(rb + G::R_M, &mrM, &bars[xs], gx0, gy0, pl);
+      tma_load_3d(rb + G::R_R, &mrH, &bars[xs], xr, gy0, pl);
+    }
+    issue_x(q + 1, xs);
+  };
+
+  if (tid == 0) {
+    for (int s = 0; s < NXB; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // prologue: tiles qfirst (slot 0) and tau0 (slot 1) alone, then batches
+  // tau0 .. tau0 + PD (batch q's tile of plane q + 1 goes to slot q + 1 - qfirst)
+  if (tid == 0) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(&bars[0], G::X_BYTES);
+    issue_x(qfirst, 0);
+    mbar_expect_tx(&bars[1], G::X_BYTES);
+    issue_x(qfirst + 1, 1);
+    for (int q = tau0; q <= min(tau0 + PD, tau_end - 1); ++q) issue(q, (q + 1 - qfirst) % NXB, (q - tau0) % NB);
+  }
+  mbar_wait(&bars[0], 0);
+  mbar_wait(&bars[1], 0);
+  // slot state: x slots of planes tau-1, tau, tau+1; parity of plane tau+1's
+  // barrier; band slot of plane tau
+  int xsm = 0, xs0 = 1, xsp = 2 % NXB;
+  uint32_t parp = 0;
+  int bs0 = 0;
+  auto adv = [](int& v, int n) { v = (v + 1 == n) ? 0 : v + 1; };
+  const double* xslot = reinterpret_cast<const double*>(smem + G::XBASE);
+  constexpr int XS = G::XSLOT / 8;
+
+  double bnd[NST][NBAND];
+  double rr[NST];
+#pragma unroll
+  for (int s = 0; s < NST; ++s) {
+    rr[s] = 0.0;
+#pragma unroll
+    for (int d = 0; d < NBAND; ++d) bnd[s][d] = 0.0;
+  }
+  // own z-columns: input at planes tau-1, tau (registers); stage s-1's
+  // outputs at the two planes below the one stage s-1 produced last
+  double xcm = xslot[xsm * XS + xo[1][1]], xcc = xslot[xs0 * XS + xo[1][1]];
+  double hm[NST > 1 ? NST - 1 : 1], hc[NST > 1 ? NST - 1 : 1];
+#pragma unroll
+  for (int s = 0; s < NST - 1; ++s) hm[s] = hc[s] = 0.0;
+
+  // y = sum_d a_d v_d in stencil_kernel<19>'s order (even / odd FMA chains)
+  auto apply19 = [](const double (&a)[NBAND], const double (&v)[19]) {
+    double ya = 0.0, yb = 0.0;
+#pragma unroll
+    for (int d = 0; d < 19; ++d) {
+      if (d % 2 == 0) ya = fma(a[d], v[d], ya);
+      else yb = fma(a[d], v[d], yb);
+    }
+    return ya + yb;
+  };
+
+#define RK_C19_STEP(PH)                                                                           \
+  {                                                                                               \
+    if (tau >= tau_end) break;                                                                    \
+    if (tau + 1 <= qlast) mbar_wait(&bars[xsp], parp);                                            \
+    double v0 = 0.0;                                                                              \
+    if (active) {                                                                                 \
+      /* stage 0 at plane tau: bands / rhs to registers, input neighbours from the tiles */      \
+      const double* bsl = reinterpret_cast<const double*>(smem + bs0 * G::BSLOT) + boff;          \
+      _Pragma("unroll") for (int d = 0; d < NBAND; ++d) bnd[PH][d] = bsl[d * bstr];               \
+      if (LOAD_R) rr[PH] = reinterpret_cast<const double*>(smem + G::RBASE + bs0 * G::RSLOT)[roff]; \
+      const double* tm = xslot + xsm * XS;                                                        \
+      const double* t0 = xslot + xs0 * XS;                                                        \
+      const double* tp = xslot + xsp * XS;                                                        \
+      bool cut_m = false, cut_p = false;                                                          \
+      if ((FL & 1) && cp.zb > 0 && cp.local[0]) {                                                 \
+        const int g = cp.zg0 + pl_of(tau);                                                        \
+        cut_m = (g % cp.zb) == 0;                                                                 \
+        cut_p = ((g + 1) % cp.zb) == 0;                                                           \
+      }                                                                                           \
+      const double xn = tp[xo[1][1]];                                                             \
+      double v[19];                                                                               \
+      v[0] = xcc;                                                                                 \
+      v[1] = t0[xo[1][0]];                                                                        \
+      v[2] = t0[xo[1][2]];                                                                        \
+      v[3] = t0[xo[0][1]];                                                                        \
+      v[4] = t0[xo[2][1]];                                                                        \
+      v[5] = cut_m ? 0.0 : xcm;                                                                   \
+      v[6] = cut_p ? 0.0 : xn;                                                                    \
+      v[7] = t0[xo[0][0]];                                                                        \
+      v[8] = t0[xo[0][2]];                                                                        \
+      v[9] = t0[xo[2][0]];                                                                        \
+      v[10] = t0[xo[2][2]];                                                                       \
+      v[11] = cut_m ? 0.0 : tm[xo[0][1]];                                                         \
+      v[12] = cut_m ? 0.0 : tm[xo[2][1]];                                                         \
+      v[13] = cut_p ? 0.0 : tp[xo[0][1]];                                                         \
+      v[14] = cut_p ? 0.0 : tp[xo[2][1]];                                                         \
+      v[15] = cut_m ? 0.0 : tm[xo[1][0]];                                                         \
+      v[16] = cut_m ? 0.0 : tm[xo[1][2]];                                                         \
+      v[17] = cut_p ? 0.0 : tp[xo[1][0]];                                                         \
+      v[18] = cut_p ? 0.0 : tp[xo[1][2]];                                                         \
+      const double y = apply19(bnd[PH], v);                                                       \
+      const double inv = bnd[PH][19];                                                             \
+      if (K0 == CK_SPMV1) {                                                                       \
+        rr[PH] = y;                                                                               \
+        v0 = (cp.omega[0] * y) * inv;                                                             \
+      } else if (K0 == CK_SWEEP) {                                                                \
+        v0 = fma(cp.omega[0] * (rr[PH] - y), inv, xcc);                                           \
+      } else {                                                                                    \
+        v0 = y;                                                                                   \
+      }                                                                                           \
+      if (interior && tau >= z0 && tau < z1 && (pz || tau < nz)) {                                \
+        const int64_t nn = (int64_t)pl_of(tau) * cp.P + cxy;                                      \
+        if (K0 == CK_SPMV1 && cp.out_t) cp.out_t[nn] = y;                                         \
+        if (NST == 1) cp.out[nn] = v0;                                                            \
+        if (NST == 2 && cp.out_mid) cp.out_mid[nn] = v0;                                          \
+      }                                                                                           \
+      if (NST > 1) ring[(tau & 3) * EY * EX + gofs] = v0;                                         \
+      xcm = xcc;                                                                                  \
+      xcc = xn;                                                                                   \
+    }                                                                                             \
+    __syncthreads();                                                                              \
+    /* the slots of plane tau-1's tile and plane tau's bands / rhs are free */                    \
+    if (tid == 0 && tau + PD + 1 <= tau_end - 1) issue(tau + PD + 1, xsm, bs0);                  \
+    double up = v0;   /* stage s-1's value at the plane above stage s's, own cell */              \
+    RK_C19_LATER(PH, 1)                                                                           \
+    RK_C19_LATER(PH, 2)                                                                           \
+    xsm = xs0;                                                                                    \
+    xs0 = xsp;                                                                                    \
+    adv(xsp, NXB);                                                                                \
+    if (xsp == 0) parp ^= 1u;                                                                     \
+    adv(bs0, NB);                                                                                 \
+    ++tau;                                                                                        \
+  }
+
+  // stage S (1 <= S < NST) at plane q = tau - S: stage S-1's outputs at
+  // planes q-1, q, q+1 from ring S-1 (own column from registers hm / hc /
+  // up), the bands / rhs of plane q from register set (PH - S) mod NST
+#define RK_C19_LATER(PH, S)                                                                       \
+  if constexpr (NST > S) {                                                                        \
+    double vs = 0.0;                                                                              \
+    if constexpr (S > 1) __syncthreads();                                                         \
+    constexpr int R = ((PH) - (S) + 3 * NST) % NST;                                               \
+    const int q = tau - (S);                                                                      \
+    /* cells within NST-1-S of the interior (the next stage's stencil reach) */                 \
+    constexpr int RS = NST - 1 - (S);                                                             \
+    const bool act = (S == NST - 1) ? interior                                                    \
+                                    : (active && c >= -RS && c < TX + RS && ry >= H - RS &&       \
+                                       ry < H + TY + RS);                                         \
+    if (tau >= tau0 + 2 * (S) && act) {                                                           \
+      const double* rg = ring + ((S) - 1) * 4 * EY * EX + gofs;                                   \
+      const double* rm = rg + ((q - 1) & 3) * EY * EX;                                            \
+      const double* r0 = rg + (q & 3) * EY * EX;                                                  \
+      const double* rp = rg + ((q + 1) & 3) * EY * EX;                                            \
+      bool cut_m = false, cut_p = false;                                                          \
+      if ((FL & 1) && cp.zb > 0 && cp.local[S]) {                                                 \
+        const int g = cp.zg0 + pl_of(q);                                                          \
+        cut_m = (g % cp.zb) == 0;                                                                 \
+        cut_p = ((g + 1) % cp.zb) == 0;                                                           \
+      }                                                                                           \
+      const double cc = hc[(S) - 1];                                                              \
+      double v[19];                                                                               \
+      v[0] = cc;                                                                                  \
+      v[1] = r0[-1];                                                                              \
+      v[2] = r0[1];                                                                               \
+      v[3] = r0[-EX];                                                                             \
+      v[4] = r0[EX];                                                                              \
+      v[5] = cut_m ? 0.0 : hm[(S) - 1];                                                           \
+      v[6] = cut_p ? 0.0 : up;                                                                    \
+      v[7] = r0[-EX - 1];                                                                         \
+      v[8] = r0[-EX + 1];                                                                         \
+      v[9] = r0[EX - 1];                                                                          \
+      v[10] = r0[EX + 1];                                                                         \
+      v[11] = cut_m ? 0.0 : rm[-EX];                                                              \
+      v[12] = cut_m ? 0.0 : rm[EX];                                                               \
+      v[13] = cut_p ? 0.0 : rp[-EX];                                                              \
+      v[14] = cut_p ? 0.0 : rp[EX];                                                               \
+      v[15] = cut_m ? 0.0 : rm[-1];                                                               \
+      v[16] = cut_m ? 0.0 : rm[1];                                                                \
+      v[17] = cut_p ? 0.0 : rp[-1];                                                               \
+      v[18] = cut_p ? 0.0 : rp[1];                                                                \
+      const double y = apply19(bnd[R], v);                                                        \
+      vs = (KIND[S] == CK_SWEEP) ? fma(cp.omega[S] * (rr[R] - y), bnd[R][19], cc) : y;            \
+      if (interior && q >= z0 && q < z1) {                                                        \
+        const int64_t nq = (int64_t)pl_of(q) * cp.P + cxy;                                        \
+        if ((S) == NST - 1) cp.out[nq] = vs;                                                      \
+        else if ((S) == NST - 2 && cp.out_mid) cp.out_mid[nq] = vs;                               \
+      }                                                                                           \
+      if ((S) < NST - 1) ring[((S) * 4 + (q & 3)) * EY * EX + gofs] = vs;                         \
+    }                                                                                             \
+    hm[(S) - 1] = hc[(S) - 1];                                                                    \
+    hc[(S) - 1] = up;                                                                             \
+    up = vs;                                                                                      \
+  }
+
+  if constexpr (NST == 3) {
+    for (int tau = tau0; tau < tau_end;) {
+      RK_C19_STEP(0)
+      RK_C19_STEP(1)
+      RK_C19_STEP(2)
+    }
+  } else if constexpr (NST == 2) {
+    for (int tau = tau0; tau < tau_end;) {
+      RK_C19_STEP(0)
+      RK_C19_STEP(1)
+    }
+  } else {
+    for (int tau = tau0; tau < tau_end;) {
+      RK_C19_STEP(0)
+    }
+  }
+#undef RK_C19_LATER
+#undef RK_C19_STEP
+}
+
+}  // namespace rk

@@ -273,6 +273,10 @@ struct rk_solver {
   size_t o_arn = 0, o_misc = 0, o_coef = 0, o_gram = 0, o_T = 0, o_bi = 0, o_eta = 0, o_grow = 0;
   int max_it = 0;
   std::vector<std::array<double, 3>> history;
+  // per-step trace of the last solve (rk_trace): every rGCROT cycle's
+  // [k, m_eff, rho, LS residual, H_ (m_eff+1 x m_eff), B (k x m_eff), y] and
+  // every rBiCGStab iteration's [rho, sigma, ||s||^2, t^T s, t^T t, ||r_next||^2]
+  std::vector<double> tr_cyc, tr_bi;
   rk_report last{};
   cudaEvent_t bev[2] = {nullptr, nullptr};    // rBiCGStab lookahead: iteration records landed
   // pipelined host solves (rk_stage_rhs / rk_solve_staged / rk_host_sync)
@@ -625,6 +629,13 @@ struct rk_solver {
         H[j + 1 + (size_t)j * (m_eff + 1)] = std::sqrt(h1[2 * (MAXCOL + 1)]);
       }
       const double prec_res = ls_givens(H, m_eff, rho, y);   // line 12
+      tr_cyc.push_back(k);
+      tr_cyc.push_back(m_eff);
+      tr_cyc.push_back(rho);
+      tr_cyc.push_back(prec_res);
+      tr_cyc.insert(tr_cyc.end(), H.begin(), H.end());
+      tr_cyc.insert(tr_cyc.end(), B.begin(), B.begin() + (size_t)k * m_eff);
+      tr_cyc.insert(tr_cyc.end(), y.begin(), y.end());
       std::vector<double> z(k, 0.0);                          // line 12a: z = -B y
       for (int c = 0; c < k; ++c) {
         double v = 0.0;
@@ -900,6 +911,7 @@ struct rk_solver {
         }
         ++i;
         rr = hbi(i)->rr;
+        tr_bi.insert(tr_bi.end(), {hc.rho, hc.sigma, hc.ss, hc.ts, hc.tt, rr});
         record((double)rep.krylov_matvecs, std::numeric_limits<double>::quiet_NaN(), std::sqrt(rr));
         if (!(std::sqrt(rr) <= thr_div)) {   // [D17] instability
           status = RK_UNSTABLE;
@@ -1337,6 +1349,8 @@ rk_status rk_solve(rk_solver* s, const double* b, double* xu, double tol, rk_rep
     rep.final_true_res = std::numeric_limits<double>::quiet_NaN();
     rep.final_updated_res = std::numeric_limits<double>::quiet_NaN();
     s->history.clear();
+    s->tr_cyc.clear();
+    s->tr_bi.clear();
     RK_CUDA(cudaMemcpyAsync(s->x, xu, sizeof(double) * s->N, cudaMemcpyDeviceToDevice,
                             s->ctx->stream));
     if (s->method == RK_RGCROT || s->method == RK_GMRES) s->solve_rgcrot(b, tol, rep);
@@ -1370,6 +1384,8 @@ rk_status rk_solve_host_ex(rk_solver* s, const double* bh, const double* x0h, do
     rk_report r;
     std::memset(&r, 0, sizeof(r));
     s->history.clear();
+    s->tr_cyc.clear();
+    s->tr_bi.clear();
     if (s->method == RK_RGCROT || s->method == RK_GMRES) s->solve_rgcrot(s->bdev, tol, r);
     else s->solve_rbicgstab(s->bdev, tol, r);
     RK_CUDA(cudaMemcpyAsync(xh, s->x, sizeof(double) * s->N, cudaMemcpyDeviceToHost,
@@ -1414,6 +1430,8 @@ rk_status rk_solve_staged(rk_solver* s, int slot, double* xh, double tol, rk_rep
     rk_report r;
     std::memset(&r, 0, sizeof(r));
     s->history.clear();
+    s->tr_cyc.clear();
+    s->tr_bi.clear();
     if (s->method == RK_RGCROT || s->method == RK_GMRES) s->solve_rgcrot(s->bstage[slot], tol, r);
     else s->solve_rbicgstab(s->bstage[slot], tol, r);
     // snapshot x (after the previous download finished with the snapshot
@@ -1452,6 +1470,16 @@ rk_status rk_history(rk_solver* s, double* out, int64_t cap, int64_t* len) {
     if (out)
       for (int64_t i = 0; i < std::min<int64_t>(cap, *len); ++i)
         for (int q = 0; q < 3; ++q) out[3 * i + q] = s->history[i][q];
+  });
+}
+
+rk_status rk_trace(rk_solver* s, int what, double* out, int64_t cap, int64_t* len) {
+  return guarded([&] {
+    RK_REQUIRE(s && len, RK_EINVAL, "NULL argument");
+    RK_REQUIRE(what == 0 || what == 1, RK_EINVAL, "what: 0 (rGCROT cycles) or 1 (rBiCGStab iterations)");
+    const std::vector<double>& v = what == 0 ? s->tr_cyc : s->tr_bi;
+    *len = (int64_t)v.size();
+    if (out) std::memcpy(out, v.data(), sizeof(double) * (size_t)std::min<int64_t>(cap, *len));
   });
 }
 

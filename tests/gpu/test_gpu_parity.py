@@ -206,6 +206,62 @@ def test_chain_bitwise_equals_unfused(rk, ctx, shape, periodic, cfg, monkeypatch
     plain.close()
 
 
+# 19-point chain (chain19.cuh): 2 stages per launch, x staged as three TMA
+# regions so that a periodic x axis wraps; nx % 32 == 0, ny % 8 == 0, nz >= 16.
+@pytest.mark.parametrize("shape,periodic", [((64, 16, 40), 5), ((32, 24, 17), 1), ((96, 16, 33), 4),
+                                            ((64, 32, 20), 0), ((32, 8, 16), 1)])
+def test_chain19_bitwise_equals_unfused(rk, ctx, shape, periodic, monkeypatch):
+    """The 19-point fused chain against the one-stage-per-launch stencil path
+    on random 19-band operators: M^-1 r (the 5 sweeps after the first run
+    as launches of 2, 2 and 1 stages) and block-Jacobi local sweeps agree bit
+    for bit, and M^-1 r matches the oracle's Jacobi(5+1) to 1e-12."""
+    nx, ny, nz = shape
+    hb = random_op_problem(nx, ny, nz, periodic, OFFSETS19, 13 + nx + nz)
+    bands = dev(hb)
+    mk = lambda: rk.GridOperator(ctx, nx, ny, nz, OFFSETS19, bands, periodic)
+    monkeypatch.setenv("RK_FORCE_CHAIN", "1")
+    fused = mk()
+    monkeypatch.delenv("RK_FORCE_CHAIN")
+    monkeypatch.setenv("RK_NO_CHAIN", "1")
+    plain = mk()
+    monkeypatch.delenv("RK_NO_CHAIN")
+    rh = np.random.default_rng(4).uniform(-1, 1, nx * ny * nz)
+    r = dev(rh)
+    a, b = fused.precond(r), plain.precond(r)
+    assert torch.equal(a, b)
+    zb = 4 if nz % 4 == 0 else 1
+    if zb > 1:
+        assert torch.equal(fused.precond(r, zblocks=zb), plain.precond(r, zblocks=zb))
+    ref = Operator(nx, ny, nz, periodic, OFFSETS19, hb)
+    zr = Jacobi(ref)(rh)
+    assert np.max(np.abs(a.cpu().numpy() - zr)) <= 1e-12 * np.max(np.abs(zr))
+    fused.close()
+    plain.close()
+
+
+def test_chain19_solver_paths_bitwise(rk, ctx, monkeypatch):
+    """Every solver use of the 19-point chain -- rGCROT's A_hat v (stages
+    [SPMV1, SWEEP] [SWEEP, SWEEP] [SWEEP, SWEEP]), rBiCGStab's p_hat / v
+    ([SWEEP, SWEEP] x 2, [SWEEP, SPMV]), the refresh and the cycle-end M^-1
+    -- gives the same iterates, bit for bit, as the unfused path: one hybrid
+    sequence on a 32^3 channel operator (periodic x/z) with and without
+    RK_FORCE_CHAIN."""
+    from problems.workloads import Workload
+    from dataclasses import replace
+    w0 = get_workload("c2s")
+    w = Workload("c2m", lambda: channel19(32), replace(w0.params, method="hybrid", n_sw=2), 4, 2, "")
+    monkeypatch.setenv("RK_FORCE_CHAIN", "1")
+    g1, sp1 = gpu_sequence(rk, ctx, w)
+    monkeypatch.delenv("RK_FORCE_CHAIN")
+    g2, sp2 = gpu_sequence(rk, ctx, w)
+    for (r1, x1), (r2, x2) in zip(g1, g2):
+        assert r1["krylov_matvecs"] == r2["krylov_matvecs"] and r1["outcome"] == r2["outcome"]
+        assert np.array_equal(x1, x2)
+    assert np.array_equal(sp1[0], sp2[0]) and np.array_equal(sp1[1], sp2[1])
+    ora = run_sequence(w)
+    compare_sequences(w, g1, ora, w.params.method)
+
+
 # Block-Jacobi preconditioner (SURVEY §8(f) row 2, reading R17): the local
 # sweeps drop every coupling between z-blocks.  Unfused and fused (chain) paths.
 @pytest.mark.parametrize("name,mk,zblocks,force", [
