@@ -992,26 +992,33 @@ void bdot2(rk_ctx* ctx, const std::vector<const double*>& cols_all, const double
     bdot(ctx, cols_all, v, N, out_v);
     return;
   }
-  // bulk-copy path: one launch for up to 32 columns (one CTA per SM leaves
-  // registers for 64 accumulators), else <= 24 columns per tiled launch
-  if (total <= 32 && (ctx->bdot_bulk == 2 ||
-                      (ctx->bdot_bulk == 1 && total >= 4 && N >= (int64_t)BK_ROWS * ctx->sms))) {
-    const int nc = nc_round(total);
-    RedArgs ra = red_args(ctx, out_w);
-    ra.out2 = out_v;
-    ra.split = nc;
-    ra.valid = total;
-    ColPtrs Q = make_cols_padded(cols_all, nc);
-    Launch L(ctx, "bdot", 8.0 * N * (total + 2));
-    switch (nc) {
-      case 8: launch_bulk(ctx, bdot_bulk_kernel<8, 2>, Q, total, w, v, N, ra); break;
-      case 16: launch_bulk(ctx, bdot_bulk_kernel<16, 2>, Q, total, w, v, N, ra); break;
-      case 24: launch_bulk(ctx, bdot_bulk_kernel<24, 2>, Q, total, w, v, N, ra); break;
-      default: launch_bulk(ctx, bdot_bulk_kernel<32, 2>, Q, total, w, v, N, ra); break;
+  // bulk-copy path: launches of up to 32 columns (one CTA per SM leaves
+  // registers for 64 accumulators), balanced (72 columns: 3 x 24; each
+  // launch re-reads w and v, 2 W), else <= 24 columns per tiled launch
+  if (ctx->bdot_bulk == 2 ||
+      (ctx->bdot_bulk == 1 && total >= 4 && N >= (int64_t)BK_ROWS * ctx->sms)) {
+    const int nch = (total + 31) / 32;
+    const int per = (total + nch - 1) / nch;
+    for (int off = 0; off < total; off += per) {
+      const int ncol = std::min(per, total - off);
+      std::vector<const double*> cols(cols_all.begin() + off, cols_all.begin() + off + ncol);
+      const int nc = nc_round(ncol);
+      RedArgs ra = red_args(ctx, out_w + off);
+      ra.out2 = out_v + off;
+      ra.split = nc;
+      ra.valid = ncol;
+      ColPtrs Q = make_cols_padded(cols, nc);
+      Launch L(ctx, "bdot", 8.0 * N * (ncol + 2));
+      switch (nc) {
+        case 8: launch_bulk(ctx, bdot_bulk_kernel<8, 2>, Q, ncol, w, v, N, ra); break;
+        case 16: launch_bulk(ctx, bdot_bulk_kernel<16, 2>, Q, ncol, w, v, N, ra); break;
+        case 24: launch_bulk(ctx, bdot_bulk_kernel<24, 2>, Q, ncol, w, v, N, ra); break;
+        default: launch_bulk(ctx, bdot_bulk_kernel<32, 2>, Q, ncol, w, v, N, ra); break;
+      }
+      L.done();
+      allreduce(ctx, out_w + off, ncol);
+      allreduce(ctx, out_v + off, ncol);
     }
-    L.done();
-    allreduce(ctx, out_w, total);
-    allreduce(ctx, out_v, total);
     return;
   }
   for (int off = 0; off < total; off += 24) {

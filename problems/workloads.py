@@ -85,6 +85,12 @@ WORKLOADS = {
     "c3m": Workload("c3m", lambda: porous7(32, 3), _hy(8, 8, 2), 6),
     "c4s": Workload("c4s", lambda: channel19(16), _rg(12, 10, 1), 9, epoch_every=3),
     "c4hs": Workload("c4hs", lambda: channel19(16), _hy(12, 10, 1), 9, epoch_every=3),
+    # 64^3 analogues of c4 with c4's solver parameters (the oracle runs whole
+    # sequences in ~1 h; diagnosis of the c4 hybrid, profiles/r02_c4h_diag/)
+    "c4m": Workload("c4m", lambda: channel19(64), _rg(40, 30, 1), 30, epoch_every=10,
+                    description="64^3 19-pt channel, rGCROT(40,30), 30 RHS, A perturbed every 10"),
+    "c4hm": Workload("c4hm", lambda: channel19(64), _hy(40, 30, 1), 30, epoch_every=10,
+                     description="64^3 19-pt channel, hybrid(3) rGCROT(40,30)->rBiCGStab, 30 RHS"),
 }
 
 
