@@ -13,6 +13,9 @@ from collections import defaultdict
 
 tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
 src = sys.argv[2] if len(sys.argv) > 2 else "gpurun_out"
+workload = sys.argv[3] if len(sys.argv) > 3 else "c3"
+cmd = sys.argv[4] if len(sys.argv) > 4 else ("python bench.py --steps 1 --warmup 3 --no-cpu-baseline "
+                                             "--no-e2e --no-secondary")
 
 
 def cls_of(name, grid=None):
@@ -21,6 +24,8 @@ def cls_of(name, grid=None):
         mode = int(m.group(2))
         return {0: "stencil_spmv", 1: "stencil_spmv_sweep1", 2: "stencil_sweep", 3: "stencil_sweep",
                 4: "stencil_resid", 5: "stencil_resid_sweep1", 6: "stencil_scale"}[mode]
+    if "chain19_kernel" in name:
+        return "chain19"
     m = re.search(r"chain_kernel(_x2)?<(\d+), (\d+)", name)
     if m:
         return "chain"
@@ -48,8 +53,8 @@ for r in rows[hi + 1:]:
     agg[c][1] += v
     tot += v
 out = [f"# {tag}: ncu launch list (gpu__time_duration.sum, --clock-control none), "
-       f"first {sum(a[0] for a in agg.values())} launches of `python bench.py --steps 1 --warmup 3 "
-       f"--no-cpu-baseline --no-e2e` (c3 workload; cold-cache, serialised => compare SHARES)",
+       f"{sum(a[0] for a in agg.values())} launches of `{cmd}` ({workload} workload; cold-cache, "
+       f"serialised => compare SHARES)",
        f"{'class':24s} {'launches':>9s} {'total_us':>12s} {'share':>7s} {'us/launch':>10s}"]
 for c, (n, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
     out.append(f"{c:24s} {n:9d} {t / 1e3:12.1f} {t / tot:7.3f} {t / 1e3 / n:10.2f}")
@@ -94,6 +99,12 @@ for r in rr[2:]:
 open(f"profiles/{tag}_ncu_full_summary.txt", "w").write("\n".join(lines) + "\n")
 print("\n".join(lines))
 tj = {c: sum(v) / len(v) for c, v in traffic.items()}
-json.dump({"_note": f"{tag}: mean dram__bytes_read.sum + dram__bytes_write.sum per launch "
-                    "(bytes) from the ncu --set full capture; keyed by librk kernel class",
-           **{k: round(v) for k, v in tj.items()}}, open("profiles/ncu_traffic.json", "w"), indent=1)
+try:
+    old = json.load(open("profiles/ncu_traffic.json"))
+except (OSError, ValueError):
+    old = {}
+old = {k: v for k, v in old.items() if isinstance(v, dict)}
+old[workload] = {"_note": f"{tag}: mean dram__bytes_read.sum + dram__bytes_write.sum per launch "
+                          "(bytes) from the ncu --set full capture; keyed by librk kernel class",
+                 **{k: round(v) for k, v in tj.items()}}
+json.dump(old, open("profiles/ncu_traffic.json", "w"), indent=1)
