@@ -132,7 +132,12 @@ rk_status rk_nccl_unique_id(uint8_t out[128]);
 
 /* Create a context on CUDA device `device`.  cuda_stream: a cudaStream_t
  * (e.g. torch.cuda.current_stream().cuda_stream) or NULL for a library-
- * owned non-blocking stream.  uid must be NULL iff nranks == 1. */
+ * owned non-blocking stream.  uid must be NULL iff nranks == 1; it is the
+ * 128-byte NCCL unique id (one process per GPU, the product path), or the
+ * bytes "RKLOCAL:<name>" zero-padded: an in-process rank group <name> whose
+ * nranks contexts (one per host thread, any devices) exchange halos by
+ * device copies and sum all-reduces on the host in rank order -- the same
+ * multi-rank schedule without NCCL, for tests on a one-GPU box. */
 rk_status rk_ctx_create(int device, int rank, int nranks, const uint8_t* uid,
                         void* cuda_stream, rk_ctx** out);
 void rk_ctx_destroy(rk_ctx* ctx);

@@ -865,7 +865,7 @@ void bdot(rk_ctx* ctx, const std::vector<const double*>& cols_all, const double*
 }
 
 void bproject(rk_ctx* ctx, const std::vector<const double*>& cols, double* w, int64_t N,
-              double* eta, const std::vector<const double*>& dots, double* red_out) {
+              double* eta, const std::vector<const double*>& dots, double* red_out, bool reduce) {
   const int ncol = (int)cols.size();
   const int nd = (int)dots.size();
   const bool defer = ctx->defer_coef && ctx->nranks == 1 && ncol >= 1 && ncol <= 40 && nd <= 3 &&
@@ -873,7 +873,7 @@ void bproject(rk_ctx* ctx, const std::vector<const double*>& cols, double* w, in
                                   nd > 2 ? dots[2] : nullptr}, cols) == 2;
   if (!defer) {
     bdot(ctx, cols, w, N, eta);
-    bupd(ctx, cols, eta, 1.0, w, N, dots, red_out);
+    bupd(ctx, cols, eta, 1.0, w, N, dots, red_out, CoefIn{}, reduce);
     return;
   }
   RedArgs ra = red_args(ctx, nullptr);
@@ -885,30 +885,39 @@ void bproject(rk_ctx* ctx, const std::vector<const double*>& cols, double* w, in
   L.done();
   cin.part = ctx->dpartials;
   cin.store = eta;
-  bupd(ctx, cols, eta, 1.0, w, N, dots, red_out, cin);
+  bupd(ctx, cols, eta, 1.0, w, N, dots, red_out, cin, reduce);
 }
 
 bool bicg_proj_s(rk_op* op, const std::vector<const double*>& C, double* v, const double* rtl,
                  const double* ctr, double* eta, const double* r, double* s, double* z, double wl,
-                 bool jacobi, BiIter* cur) {
+                 bool jacobi, BiIter* cur, double* stage) {
   rk_ctx* ctx = op->ctx;
   const int64_t N = op->N;
   const int k = (int)C.size();
   const double* D = jacobi ? op->invd() : nullptr;
-  if (!ctx->defer_coef || ctx->nranks != 1 || k < 1 || k + 1 > 40 ||
-      pick_vec(N, {v, rtl, r, s, z, D}, C) != 2)
+  const bool one = ctx->nranks == 1;
+  if ((one && !ctx->defer_coef) || k < 1 || k + 1 > 40 || pick_vec(N, {v, rtl, r, s, z, D}, C) != 2)
     return false;
   std::vector<const double*> cols(C);
   cols.push_back(rtl);
-  RedArgs ra = red_args(ctx, nullptr);
-  ra.partials = ctx->dpartials;
-  ra.defer = 1;
-  Launch L(ctx, "bdot", 8.0 * N * (k + 2));
   CoefIn cin;
-  cin.G = bdot_launch(ctx, cols, v, N, ra);
-  L.done();
-  cin.part = ctx->dpartials;
   cin.store = eta;
+  if (one) {   // deferred: bproj_s sums the block dot's per-CTA partials
+    RedArgs ra = red_args(ctx, nullptr);
+    ra.partials = ctx->dpartials;
+    ra.defer = 1;
+    Launch L(ctx, "bdot", 8.0 * N * (k + 2));
+    cin.G = bdot_launch(ctx, cols, v, N, ra);
+    L.done();
+    cin.part = ctx->dpartials;
+  } else {     // finalised, one all-reduce of [C^T v, r~^T v], read as G = 1 partials
+    Launch L(ctx, "bdot", 8.0 * N * (k + 2));
+    bdot_launch(ctx, cols, v, N, red_args(ctx, stage));
+    L.done();
+    allreduce(ctx, stage, k + 1);
+    cin.part = stage;
+    cin.G = 1;
+  }
   const int nc = nc_round(k + 1);
   ColPtrs Q = make_cols_padded(C, nc_round(k));
   RedArgs rs = red_args(ctx, &cur->ss);
@@ -932,7 +941,7 @@ bool bicg_proj_s(rk_op* op, const std::vector<const double*>& C, double* v, cons
 
 void bupd(rk_ctx* ctx, const std::vector<const double*>& cols, const double* g, double gscale,
           double* w, int64_t N, const std::vector<const double*>& dots, double* red_out,
-          CoefIn cin) {
+          CoefIn cin, bool reduce) {
   const int ncol = (int)cols.size();
   const int nd = (int)dots.size();
   RK_REQUIRE(nd <= 3, RK_EINVAL, "bupd: at most 3 dots");
@@ -979,7 +988,7 @@ void bupd(rk_ctx* ctx, const std::vector<const double*>& cols, const double* g, 
 #undef RK_BUPD_NC
 #undef RK_BUPD
   L.done();
-  if (nd) allreduce(ctx, red_out, nd);
+  if (nd && reduce) allreduce(ctx, red_out, nd);
 }
 
 void bdot2(rk_ctx* ctx, const std::vector<const double*>& cols_all, const double* w, const double* v,
@@ -1016,8 +1025,7 @@ void bdot2(rk_ctx* ctx, const std::vector<const double*>& cols_all, const double
         default: launch_bulk(ctx, bdot_bulk_kernel<32, 2>, Q, ncol, w, v, N, ra); break;
       }
       L.done();
-      allreduce(ctx, out_w + off, ncol);
-      allreduce(ctx, out_v + off, ncol);
+      allreduce2(ctx, out_w + off, ncol, out_v + off, ncol);
     }
     return;
   }
@@ -1037,8 +1045,7 @@ void bdot2(rk_ctx* ctx, const std::vector<const double*>& cols_all, const double
       default: launch_k(ctx, bdot2_tile_kernel<24>, N / 4, dim3(256), Q, ncol, w, v, N, ra); break;
     }
     L.done();
-    allreduce(ctx, out_w + off, ncol);
-    allreduce(ctx, out_v + off, ncol);
+    allreduce2(ctx, out_w + off, ncol, out_v + off, ncol);
   }
 }
 

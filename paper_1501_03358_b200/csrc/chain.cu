@@ -318,9 +318,9 @@ chain_kernel(const __grid_constant__ CUtensorMap map_b, const __grid_constant__ 
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_expect_tx(&bars[xs], tx_bytes);
     tma_load_4d(bbase, &map_b, &bars[xs], gx0 - PADB, gy0, pl, 0);
-    if (LOAD_R) tma_load_3d(bbase + G::R_OFF, &map_r, &bars[xs], gx0 - PADB, gy0, pl);
-    // the input vector is padded: plane pl lives at z-coordinate pl + 1
-    tma_load_3d(xbase, &map_x, &bars[xs], gx0 - 1 - PADX, gy0 - 1, pl + 1);
+    if (LOAD_R) tma_load_3d(bbase + G::R_OFF, &map_r, &bars[xs], gx0 - PADB, gy0, pl + cp.rz);
+    // the input vector is padded: plane pl lives at z-coordinate pl + GHOST
+    tma_load_3d(xbase, &map_x, &bars[xs], gx0 - 1 - PADX, gy0 - 1, pl + GHOST);
   };
 
   if (tid == 0) {
@@ -437,37 +437,59 @@ void encode(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims,
   RK_REQUIRE(r == CUDA_SUCCESS, RK_ECUDA, "cuTensorMapEncodeTiled failed");
 }
 
+// The sweeps' right-hand side: the caller's unpadded vector on one rank;
+// on several ranks a padded vector whose ghost planes chain_run filled
+// (cp.rz = GHOST: plane pl at z-coordinate pl + GHOST).
+void encode_rhs(const rk_op* op, const ChainParams& cp, CUtensorMap* m, cuuint32_t bx, cuuint32_t by) {
+  const cuuint64_t nx = op->g.nx, ny = op->g.ny, nz = op->g.nz_local;
+  cuuint64_t str[2] = {nx * 8, nx * ny * 8};
+  cuuint32_t box[3] = {bx, by, 1};
+  if (cp.r && cp.rz) {
+    cuuint64_t dims[3] = {nx, ny, nz + 2 * GHOST};
+    encode(m, cp.r - GHOST * op->P, 3, dims, str, box);
+  } else {
+    cuuint64_t dims[3] = {nx, ny, nz};
+    encode(m, cp.r ? cp.r : cp.bands, 3, dims, str, box);
+  }
+}
+
 template <int ST, int NST, int TX, int TY, int PD, int K0, int K1, int K2, int X2>
 void launch_one(rk_op* op, ChainParams cp, dim3 grid) {
   using G = ChainGeom<ST, NST, TX, TY, PD>;
   static_assert(G::SMEM <= 232448, "chain tile exceeds 227 KB of shared memory");
   using KernFn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, ChainParams);
-  KernFn kern;
-  int fl = 0;   // x-pair kernel flavour: block-Jacobi cuts (1), periodic z (2)
+  using KernFn2 = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap,
+                           ChainParams);
+  KernFn kern = nullptr;
+  KernFn2 kern2 = nullptr;
+  int fl = 0;   // x-pair kernel flavour: block-Jacobi cuts (1), periodic z (2), ghost bands (4)
   if constexpr (X2 != 0) {
     bool cuts = false;
     for (int s = 0; s < NST; ++s) cuts = cuts || (cp.zb > 0 && cp.local[s]);
-    fl = (cuts ? 1 : 0) | (cp.pz ? 2 : 0);
+    fl = (cuts ? 1 : 0) | (cp.pz ? 2 : 0) | (cp.ghost ? 4 : 0);
     switch (fl) {
-      case 0: kern = chain_kernel_x2<ST, NST, TX, TY, PD, K0, K1, K2, 0>; break;
-      case 1: kern = chain_kernel_x2<ST, NST, TX, TY, PD, K0, K1, K2, 1>; break;
-      case 2: kern = chain_kernel_x2<ST, NST, TX, TY, PD, K0, K1, K2, 2>; break;
-      default: kern = chain_kernel_x2<ST, NST, TX, TY, PD, K0, K1, K2, 3>; break;
+      case 0: kern2 = chain_kernel_x2<ST, NST, TX, TY, PD, K0, K1, K2, 0>; break;
+      case 1: kern2 = chain_kernel_x2<ST, NST, TX, TY, PD, K0, K1, K2, 1>; break;
+      case 2: kern2 = chain_kernel_x2<ST, NST, TX, TY, PD, K0, K1, K2, 2>; break;
+      case 3: kern2 = chain_kernel_x2<ST, NST, TX, TY, PD, K0, K1, K2, 3>; break;
+      case 4: kern2 = chain_kernel_x2<ST, NST, TX, TY, PD, K0, K1, K2, 4>; break;
+      default: kern2 = chain_kernel_x2<ST, NST, TX, TY, PD, K0, K1, K2, 5>; break;
     }
   } else {
     kern = chain_kernel<ST, NST, TX, TY, PD, K0, K1, K2>;
   }
+  const void* kp = X2 ? (const void*)kern2 : (const void*)kern;
   const int nthr = X2 ? G::NTHR / 2 : G::NTHR;
   // resident CTAs per SM of this instantiation; the shared-memory attribute
   // is per device, so it is set (and the occupancy cached) per context
   int occ = 0;
   {
-    auto it = op->ctx->occ_cache.find((const void*)kern);
+    auto it = op->ctx->occ_cache.find(kp);
     if (it == op->ctx->occ_cache.end()) {
-      RK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
-      RK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nthr, G::SMEM));
+      RK_CUDA(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
+      RK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kp, nthr, G::SMEM));
       occ = std::max(1, occ);
-      op->ctx->occ_cache[(const void*)kern] = occ;
+      op->ctx->occ_cache[kp] = occ;
     } else {
       occ = it->second;
     }
@@ -482,24 +504,26 @@ void launch_one(rk_op* op, ChainParams cp, dim3 grid) {
   cp.zc = zc;
   grid.z = (unsigned)((nzl + zc - 1) / zc);
   const cuuint64_t nx = op->g.nx, ny = op->g.ny, nz = op->g.nz_local;
-  CUtensorMap mb, mr, mx;
+  CUtensorMap mb, mr, mx, mg;
   {
     cuuint64_t dims[4] = {nx, ny, nz, (cuuint64_t)G::NBAND};       // bands (then 1/D)
     cuuint64_t str[3] = {nx * 8, nx * ny * 8, (cuuint64_t)op->N * 8};
     cuuint32_t box[4] = {(cuuint32_t)G::SX, (cuuint32_t)G::EY, 1, (cuuint32_t)G::NBAND};
     encode(&mb, cp.bands, 4, dims, str, box);
+    if (cp.ghost) {   // the neighbours' band planes (op->gbands)
+      cuuint64_t gd[4] = {nx, ny, 2 * BGHOST, (cuuint64_t)G::NBAND};
+      cuuint64_t gs[3] = {nx * 8, nx * ny * 8, (cuuint64_t)(2 * BGHOST) * nx * ny * 8};
+      encode(&mg, op->gbands, 4, gd, gs, box);
+    } else {
+      mg = mb;
+    }
   }
+  encode_rhs(op, cp, &mr, (cuuint32_t)G::SX, (cuuint32_t)G::EY);
   {
-    cuuint64_t dims[3] = {nx, ny, nz};
-    cuuint64_t str[2] = {nx * 8, nx * ny * 8};
-    cuuint32_t box[3] = {(cuuint32_t)G::SX, (cuuint32_t)G::EY, 1};
-    encode(&mr, cp.r ? cp.r : cp.bands, 3, dims, str, box);
-  }
-  {
-    cuuint64_t dims[3] = {nx, ny, nz + 2};                 // padded: ghost planes at 0, nz + 1
+    cuuint64_t dims[3] = {nx, ny, nz + 2 * GHOST};         // padded: GHOST ghost planes each side
     cuuint64_t str[2] = {nx * 8, nx * ny * 8};
     cuuint32_t box[3] = {(cuuint32_t)G::XX, (cuuint32_t)G::XY, 1};
-    encode(&mx, cp.xin - op->P, 3, dims, str, box);
+    encode(&mx, cp.xin - GHOST * op->P, 3, dims, str, box);
   }
   dim3 blk(X2 ? G::EX / 2 : G::EX, G::EY);
   // PDL lets the next grid's CTAs become resident early; next to the chain
@@ -510,7 +534,8 @@ void launch_one(rk_op* op, ChainParams cp, dim3 grid) {
   // 3: the chain overlaps its predecessor, its successor does not
   const bool allow = ctx->pdl && (ctx->pdl_mode == 0 || ctx->pdl_mode == 3) && !ctx->pdl_skip_next;
   ctx->pdl_skip_next = ctx->pdl_mode >= 2;
-  launch_pdl_if(ctx, allow, kern, grid, blk, G::SMEM, mb, mr, mx, cp);
+  if constexpr (X2 != 0) launch_pdl_if(ctx, allow, kern2, grid, blk, G::SMEM, mb, mr, mx, mg, cp);
+  else launch_pdl_if(ctx, allow, kern, grid, blk, G::SMEM, mb, mr, mx, cp);
 }
 
 template <int NST, int TX, int TY, int PD, int X2 = 0>
@@ -599,16 +624,19 @@ void launch19(rk_op* op, ChainParams cp) {
   using G = C19Geom<NST, TX, TY, PD>;
   static_assert(G::SMEM <= 232448, "19-point chain tile exceeds 227 KB of shared memory");
   using KernFn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap,
-                          const CUtensorMap, const CUtensorMap, ChainParams);
+                          const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap,
+                          ChainParams);
   bool cuts = false;
   for (int s = 0; s < NST; ++s) cuts = cuts || (cp.zb > 0 && cp.local[s]);
-  const int fl = (cuts ? 1 : 0) | (cp.pz ? 2 : 0);
+  const int fl = (cuts ? 1 : 0) | (cp.pz ? 2 : 0) | (cp.ghost ? 4 : 0);
   KernFn kern;
   switch (fl) {
     case 0: kern = chain19_kernel<NST, TX, TY, PD, K0, K1, K2, 0>; break;
     case 1: kern = chain19_kernel<NST, TX, TY, PD, K0, K1, K2, 1>; break;
     case 2: kern = chain19_kernel<NST, TX, TY, PD, K0, K1, K2, 2>; break;
-    default: kern = chain19_kernel<NST, TX, TY, PD, K0, K1, K2, 3>; break;
+    case 3: kern = chain19_kernel<NST, TX, TY, PD, K0, K1, K2, 3>; break;
+    case 4: kern = chain19_kernel<NST, TX, TY, PD, K0, K1, K2, 4>; break;
+    default: kern = chain19_kernel<NST, TX, TY, PD, K0, K1, K2, 5>; break;
   }
   rk_ctx* ctx = op->ctx;
   int occ = 0;
@@ -630,7 +658,7 @@ void launch19(rk_op* op, ChainParams cp) {
   cp.zc = zc;
   grid.z = (unsigned)((nzl + zc - 1) / zc);
   const cuuint64_t nx = op->g.nx, ny = op->g.ny, nz = op->g.nz_local;
-  CUtensorMap mbM, mbH, mrM, mrH, mxM, mxH;
+  CUtensorMap mbM, mbH, mrM, mrH, mxM, mxH, mgM, mgH;
   {
     cuuint64_t dims[4] = {nx, ny, nz, (cuuint64_t)G::NBAND};
     cuuint64_t str[3] = {nx * 8, nx * ny * 8, (cuuint64_t)op->N * 8};
@@ -638,26 +666,30 @@ void launch19(rk_op* op, ChainParams cp) {
     cuuint32_t boxH[4] = {(cuuint32_t)G::HW, (cuuint32_t)G::EY, 1, (cuuint32_t)G::NBAND};
     encode(&mbM, cp.bands, 4, dims, str, boxM);
     encode(&mbH, cp.bands, 4, dims, str, boxH);
+    if (cp.ghost) {   // the neighbours' band planes (op->gbands)
+      cuuint64_t gd[4] = {nx, ny, 2 * BGHOST, (cuuint64_t)G::NBAND};
+      cuuint64_t gs[3] = {nx * 8, nx * ny * 8, (cuuint64_t)(2 * BGHOST) * nx * ny * 8};
+      encode(&mgM, op->gbands, 4, gd, gs, boxM);
+      encode(&mgH, op->gbands, 4, gd, gs, boxH);
+    } else {
+      mgM = mbM;
+      mgH = mbH;
+    }
   }
+  encode_rhs(op, cp, &mrM, (cuuint32_t)TX, (cuuint32_t)G::EY);
+  encode_rhs(op, cp, &mrH, (cuuint32_t)G::HW, (cuuint32_t)G::EY);
   {
-    cuuint64_t dims[3] = {nx, ny, nz};
-    cuuint64_t str[2] = {nx * 8, nx * ny * 8};
-    cuuint32_t boxM[3] = {(cuuint32_t)TX, (cuuint32_t)G::EY, 1};
-    cuuint32_t boxH[3] = {(cuuint32_t)G::HW, (cuuint32_t)G::EY, 1};
-    encode(&mrM, cp.r ? cp.r : cp.bands, 3, dims, str, boxM);
-    encode(&mrH, cp.r ? cp.r : cp.bands, 3, dims, str, boxH);
-  }
-  {
-    cuuint64_t dims[3] = {nx, ny, nz + 2};   // padded: ghost planes at 0, nz + 1
+    cuuint64_t dims[3] = {nx, ny, nz + 2 * GHOST};   // padded: GHOST ghost planes each side
     cuuint64_t str[2] = {nx * 8, nx * ny * 8};
     cuuint32_t boxM[3] = {(cuuint32_t)TX, (cuuint32_t)G::XROWS, 1};
     cuuint32_t boxH[3] = {(cuuint32_t)G::HW, (cuuint32_t)G::XROWS, 1};
-    encode(&mxM, cp.xin - op->P, 3, dims, str, boxM);
-    encode(&mxH, cp.xin - op->P, 3, dims, str, boxH);
+    encode(&mxM, cp.xin - GHOST * op->P, 3, dims, str, boxM);
+    encode(&mxH, cp.xin - GHOST * op->P, 3, dims, str, boxH);
   }
   const bool allow = ctx->pdl && (ctx->pdl_mode == 0 || ctx->pdl_mode == 3) && !ctx->pdl_skip_next;
   ctx->pdl_skip_next = ctx->pdl_mode >= 2;
-  launch_pdl_if(ctx, allow, kern, grid, dim3(G::NTHR), G::SMEM, mbM, mbH, mrM, mrH, mxM, mxH, cp);
+  launch_pdl_if(ctx, allow, kern, grid, dim3(G::NTHR), G::SMEM, mbM, mbH, mrM, mrH, mxM, mxH, mgM, mgH,
+                cp);
 }
 
 void chain19_dispatch(rk_op* op, int nst, const int* k, const ChainParams& cp) {
@@ -677,7 +709,10 @@ void chain19_dispatch(rk_op* op, int nst, const int* k, const ChainParams& cp) {
 }  // namespace
 
 int chain_max_stages(const rk_op* op) {
-  if (op->ctx->nranks != 1 || op->no_chain) return 0;      // deep halos not exchanged (yet)
+  if (op->no_chain) return 0;
+  // several ranks: the chain input's NST-deep halo comes from one exchange
+  // per launch (chain_run), the bands' from op->gbands
+  if (op->ctx->nranks != 1 && (op->gbands == nullptr || op->g.nz_local < 16)) return 0;
   if (op->S == 19) {
     // chain19.cuh: x-region boxes wrap a periodic x axis; y must not be periodic
     if (op->g.periodic_mask & 2) return 0;
@@ -688,6 +723,7 @@ int chain_max_stages(const rk_op* op) {
   }
   if (op->S != 7) return 0;
   if (op->g.periodic_mask & 3) return 0;                    // TMA boxes do not wrap in x/y
+  if (op->ctx->nranks != 1 && cfg_index() != DEFAULT_CFG) return 0;   // ghost bands: x-pair kernel only
   const TileCfg tc = CFGS[cfg_index()];
   if (op->g.nx % tc.tx != 0 || op->g.ny % tc.ty != 0 || op->g.nx % 2 != 0) return 0;
   if (op->g.nz_local < 16) return 0;
@@ -715,7 +751,9 @@ void chain_launch(rk_op* op, int nst, const int* kinds, const double* omegas, co
   cp.nz = (int)op->g.nz_local;
   cp.px = (op->S == 19 && (op->g.periodic_mask & 1)) ? 1 : 0;   // only the 19-point kernel wraps x
   cp.py = 0;
-  cp.pz = (op->g.periodic_mask & 4) ? 1 : 0;
+  cp.pz = op->wrapz;   // periodic z on one rank wraps in the kernel; on several, halos
+  cp.ghost = op->ctx->nranks > 1 ? 1 : 0;
+  cp.rz = op->ctx->nranks > 1 ? GHOST : 0;
   cp.xin = xin;
   cp.r = r;
   cp.out_t = out_t;
@@ -747,7 +785,7 @@ void chain_run(rk_op* op, const std::vector<int>& kinds, const std::vector<doubl
   // aligned outputs; a caller's misaligned vector (rk_precond_apply accepts
   // any pointer) takes the unfused path, which handles any alignment
   auto al16 = [](const void* p) { return p == nullptr || ((uintptr_t)p & 15u) == 0; };
-  const bool aligned = al16(xin - op->P) && al16(r) && al16(out_t) && al16(out_mid) && al16(out);
+  const bool aligned = al16(xin - GHOST * op->P) && al16(r) && al16(out_t) && al16(out_mid) && al16(out);
   const int nmax = aligned ? chain_max_stages(op) : 0;
   std::vector<int> loc(n, 0);
   for (int q = 0; q < n && q < (int)local.size(); ++q) loc[q] = local[q];
@@ -773,6 +811,11 @@ void chain_run(rk_op* op, const std::vector<int>& kinds, const std::vector<doubl
     const int len = n / g + (i < n % g ? 1 : 0);
     const bool last = (i == g - 1);
     double* dst = last ? out : bufs[i % 2];
+    // several ranks: the launch reads its input len planes and the sweeps'
+    // right-hand side len - 1 planes beyond the slab (stage 0 recomputes the
+    // halo planes the later stages need)
+    halo(op, cur, len);
+    if (kinds[a] != CK_SPMV1 && rhs && len > 1) halo(op, rhs, len - 1);
     chain_launch(op, len, kinds.data() + a, om.data() + a, cur, rhs,
                  (kinds[a] == CK_SPMV1) ? out_t : nullptr, last ? out_mid : nullptr, dst,
                  loc.data() + a, zbs);

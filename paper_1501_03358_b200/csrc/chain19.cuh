@@ -82,12 +82,15 @@ __device__ __forceinline__ int region_pitch(int c) {
   return (c < 0 || c >= TX) ? HW : TX;
 }
 
-// KIND of stage s; FL bit 0: block-Jacobi cuts possible, bit 1: periodic z.
+// KIND of stage s; FL bit 0: block-Jacobi cuts possible, bit 1: periodic z
+// (one rank, wrapped in the kernel), bit 2: several ranks -- the bands of
+// planes outside [0, nz) come from the ghost-band maps mgM / mgH.
 template <int NST, int TX, int TY, int PD, int K0, int K1, int K2, int FL>
 __global__ void __launch_bounds__(C19Geom<NST, TX, TY, PD>::NTHR, 1)
 chain19_kernel(const __grid_constant__ CUtensorMap mbM, const __grid_constant__ CUtensorMap mbH,
                const __grid_constant__ CUtensorMap mrM, const __grid_constant__ CUtensorMap mrH,
                const __grid_constant__ CUtensorMap mxM, const __grid_constant__ CUtensorMap mxH,
+               const __grid_constant__ CUtensorMap mgM, const __grid_constant__ CUtensorMap mgH,
                ChainParams cp) {
   RK_PDL_ENTRY();
   RK_GATE(cp.gate);
@@ -152,9 +155,9 @@ chain19_kernel(const __grid_constant__ CUtensorMap mbM, const __grid_constant__ 
     xl = xl < 0 ? xl + nx : xl;
     xr = xr >= nx ? xr - nx : xr;
   }
-  auto issue_x = [&](int q, int xs) {   // input tile of plane q (padded vector: z = pl + 1)
+  auto issue_x = [&](int q, int xs) {   // input tile of plane q (padded vector: z = pl + GHOST)
     unsigned char* xb = smem + G::XBASE + xs * G::XSLOT;
-    const int z = pl_of(q) + 1;
+    const int z = pl_of(q) + GHOST;
     tma_load_3d(xb, &mxH, &bars[xs], xl, gy0 - 1, z);
     tma_load_3d(xb + G::X_M, &mxM, &bars[xs], gx0, gy0 - 1, z);
     tma_load_3d(xb + G::X_R, &mxH, &bars[xs], xr, gy0 - 1, z);
@@ -167,13 +170,21 @@ chain19_kernel(const __grid_constant__ CUtensorMap mbM, const __grid_constant__ 
     const int pl = pl_of(q);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_expect_tx(&bars[xs], tx_bytes);
-    tma_load_4d(bb, &mbH, &bars[xs], xl, gy0, pl, 0);
-    tma_load_4d(bb + G::B_M, &mbM, &bars[xs], gx0, gy0, pl, 0);
-    tma_load_4d(bb + G::B_R, &mbH, &bars[xs], xr, gy0, pl, 0);
+    if ((FL & 4) && (pl < 0 || pl >= nz)) {
+      const int gz = pl < 0 ? pl + BGHOST : pl - nz + BGHOST;
+      tma_load_4d(bb, &mgH, &bars[xs], xl, gy0, gz, 0);
+      tma_load_4d(bb + G::B_M, &mgM, &bars[xs], gx0, gy0, gz, 0);
+      tma_load_4d(bb + G::B_R, &mgH, &bars[xs], xr, gy0, gz, 0);
+    } else {
+      tma_load_4d(bb, &mbH, &bars[xs], xl, gy0, pl, 0);
+      tma_load_4d(bb + G::B_M, &mbM, &bars[xs], gx0, gy0, pl, 0);
+      tma_load_4d(bb + G::B_R, &mbH, &bars[xs], xr, gy0, pl, 0);
+    }
     if (LOAD_R) {
-      tma_load_3d(rb, &mrH, &bars[xs], xl, gy0, pl);
-      tma_load_3d(rb + G::R_M, &mrM, &bars[xs], gx0, gy0, pl);
-      tma_load_3d(rb + G::R_R, &mrH, &bars[xs], xr, gy0, pl);
+      const int rzz = pl + cp.rz;
+      tma_load_3d(rb, &mrH, &bars[xs], xl, gy0, rzz);
+      tma_load_3d(rb + G::R_M, &mrM, &bars[xs], gx0, gy0, rzz);
+      tma_load_3d(rb + G::R_R, &mrH, &bars[xs], xr, gy0, rzz);
     }
     issue_x(q + 1, xs);
   };

@@ -170,10 +170,13 @@ struct ChainStepX2 {
   }
 };
 
+// FL bit 2: several ranks -- the bands of planes outside [0, nz) come from
+// the ghost-band map (the neighbours' planes, librk's op->gbands).
 template <int ST, int NST, int TX, int TY, int PD, int K0, int K1, int K2, int FL>
 __global__ void __launch_bounds__((TX + 2 * (NST - 1)) * (TY + 2 * (NST - 1)) / 2, 1)
 chain_kernel_x2(const __grid_constant__ CUtensorMap map_b, const __grid_constant__ CUtensorMap map_r,
-                const __grid_constant__ CUtensorMap map_x, ChainParams cp) {
+                const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_gb,
+                ChainParams cp) {
   RK_PDL_ENTRY();
   RK_GATE(cp.gate);
   using G = ChainGeom<ST, NST, TX, TY, PD>;
@@ -224,9 +227,13 @@ chain_kernel_x2(const __grid_constant__ CUtensorMap map_b, const __grid_constant
     const int pl = pl_of(q);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_expect_tx(&bars[xs], tx_bytes);
-    tma_load_4d(bbase, &map_b, &bars[xs], gx0 - PADB, gy0, pl, 0);
-    if (LOAD_R) tma_load_3d(bbase + G::R_OFF, &map_r, &bars[xs], gx0 - PADB, gy0, pl);
-    tma_load_3d(xbase, &map_x, &bars[xs], gx0 - 1 - PADX, gy0 - 1, (RK_CHAIN_XLEAD ? pl_of(q + 1) : pl) + 1);
+    if ((FL & 4) && (pl < 0 || pl >= nz))
+      tma_load_4d(bbase, &map_gb, &bars[xs], gx0 - PADB, gy0, pl < 0 ? pl + BGHOST : pl - nz + BGHOST, 0);
+    else
+      tma_load_4d(bbase, &map_b, &bars[xs], gx0 - PADB, gy0, pl, 0);
+    if (LOAD_R) tma_load_3d(bbase + G::R_OFF, &map_r, &bars[xs], gx0 - PADB, gy0, pl + cp.rz);
+    tma_load_3d(xbase, &map_x, &bars[xs], gx0 - 1 - PADX, gy0 - 1,
+                (RK_CHAIN_XLEAD ? pl_of(q + 1) : pl) + GHOST);
   };
 
   if (tid == 0) {
@@ -240,17 +247,17 @@ chain_kernel_x2(const __grid_constant__ CUtensorMap map_b, const __grid_constant
       // bands of qfirst are never used); batch tau0 + PD follows the barrier
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_expect_tx(&bars[0], G::X_BYTES);
-      tma_load_3d(smem + G::X_BASE, &map_x, &bars[0], gx0 - 1 - PADX, gy0 - 1, pl_of(qfirst) + 1);
+      tma_load_3d(smem + G::X_BASE, &map_x, &bars[0], gx0 - 1 - PADX, gy0 - 1, pl_of(qfirst) + GHOST);
       mbar_expect_tx(&bars[1], G::X_BYTES);
       tma_load_3d(smem + G::X_BASE + G::XSLOT, &map_x, &bars[1], gx0 - 1 - PADX, gy0 - 1,
-                  pl_of(qfirst + 1) + 1);
+                  pl_of(qfirst + 1) + GHOST);
       for (int q = qfirst + 1; q <= min(qfirst + PD, qiss); ++q)
         issue(q, (q + 1 - qfirst) % NXB, (q - qfirst - 1) % NB);
     } else if (RK_CHAIN_XLEAD) {
       // the first tile alone, then batches qfirst .. qfirst + PD
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_expect_tx(&bars[0], G::X_BYTES);
-      tma_load_3d(smem + G::X_BASE, &map_x, &bars[0], gx0 - 1 - PADX, gy0 - 1, pl_of(qfirst) + 1);
+      tma_load_3d(smem + G::X_BASE, &map_x, &bars[0], gx0 - 1 - PADX, gy0 - 1, pl_of(qfirst) + GHOST);
       for (int q = qfirst; q <= min(qfirst + PD, qiss); ++q)
         issue(q, (q + 1 - qfirst) % NXB, (q - qfirst) % NB);
     } else {

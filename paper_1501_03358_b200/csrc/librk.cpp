@@ -43,9 +43,9 @@ rk_status guarded(F&& f) {
   }
 }
 
-// Padded vector: one zero ghost plane below and above the owned planes.
+// Padded vector: GHOST zero ghost planes below and above the owned planes.
 double* alloc_padded(rk_op* op, double** base, int* nvec) {
-  const size_t n = (size_t)(op->N + 2 * op->P);
+  const size_t n = (size_t)(op->N + 2 * GHOST * op->P);
   cudaError_t e = cudaMalloc(base, n * sizeof(double));
   if (e != cudaSuccess) {
     cudaGetLastError();
@@ -53,7 +53,30 @@ double* alloc_padded(rk_op* op, double** base, int* nvec) {
   }
   RK_CUDA(cudaMemsetAsync(*base, 0, n * sizeof(double), op->ctx->stream));
   if (nvec) ++*nvec;
-  return *base + op->P;
+  return *base + GHOST * op->P;
+}
+
+// Several ranks: the BGHOST band planes (all S + 1 arrays, 1/D included)
+// next to this slab, from the z-neighbours, for the fused chains' halo
+// planes (zero at a non-periodic global boundary).  Once per matrix epoch.
+void exchange_ghost_bands(rk_op* op) {
+  if (op->ctx->nranks == 1) return;
+  const int64_t P = op->P, nzl = op->g.nz_local;
+  RK_REQUIRE(nzl >= BGHOST, RK_EINVAL, "slab thinner than the band halo");
+  const size_t per = (size_t)(2 * BGHOST) * P;
+  if (!op->gbands) {
+    cudaError_t e = cudaMalloc(&op->gbands, sizeof(double) * per * (op->S + 1));
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      throw Error(RK_ENOMEM, "cudaMalloc of the ghost bands failed");
+    }
+  }
+  RK_CUDA(cudaMemsetAsync(op->gbands, 0, sizeof(double) * per * (op->S + 1), op->ctx->stream));
+  for (int d = 0; d <= op->S; ++d) {
+    const double* b = op->bands + (int64_t)d * op->N;
+    double* g = op->gbands + per * d;
+    exchange(op, b, b + (nzl - BGHOST) * P, g, g + BGHOST * P, (size_t)(BGHOST * P));
+  }
 }
 
 int canonical_slot(int S, int dx, int dy, int dz) {
@@ -817,7 +840,7 @@ struct rk_solver {
       }
       bicg_setup(ctx, xi, eta(2), k, bi(0));
       RK_CUDA(cudaMemcpyAsync(rtl, r, sizeof(double) * N, cudaMemcpyDeviceToDevice, ctx->stream));
-      if (k > 0 && ctx->nranks == 1) bdot(ctx, C, rtl, N, eta(3));   // C^T r~ for bicg_proj_s [R20]
+      if (k > 0) bdot(ctx, C, rtl, N, eta(3));   // C^T r~ for bicg_proj_s [R20]
       fetch(o_bi, 8);
       sync();
       double rr = hbi(0)->rr;
@@ -849,8 +872,9 @@ struct rk_solver {
         }
         // line 7a: eta1 = C^T v ; v -= C eta1 ; sigma = r~^T v
         // line 8: alpha = rho / sigma ; s = r - alpha v (+ first sweep of s_hat)
-        const bool fused = k > 0 && ctx->nranks == 1 &&
-                           bicg_proj_s(op, C, v, rtl, eta(3), eta(0), r, s, jac() ? za : sh, wl, jac(), cur);
+        const bool fused = k > 0 &&
+                           bicg_proj_s(op, C, v, rtl, eta(3), eta(0), r, s, jac() ? za : sh, wl, jac(), cur,
+                                       eta(4));
         if (!fused) {
           if (k > 0) {
             bproject(ctx, C, v, N, eta(0), {rtl}, &cur->sigma);
@@ -866,7 +890,11 @@ struct rk_solver {
           stencil(op, SM_SPMV, sh, nullptr, tt, nullptr, 0.0, nullptr);
         }
         if (k > 0) {                                              // line 12a
-          bproject(ctx, C, tt, N, eta(1), {s, nullptr}, &cur->ts);
+          // several ranks: ||s||^2 (left rank-local by bicg_proj_s), t^T s and
+          // t^T t -- adjacent in the record -- in ONE all-reduce
+          const bool merge = fused && ctx->nranks > 1;
+          bproject(ctx, C, tt, N, eta(1), {s, nullptr}, &cur->ts, !merge);
+          if (merge) allreduce(ctx, &cur->ss, 3);
         } else {
           bdot(ctx, {s, tt}, tt, N, &cur->ts);
         }
@@ -1003,7 +1031,9 @@ rk_status rk_ctx_create(int device, int rank, int nranks, const uint8_t* uid, vo
         c->own_stream = true;
       }
       init_ctx_kernels(c);
-      if (nranks > 1) {
+      if (nranks > 1 && local_uid(uid)) {
+        local_join(c, uid);
+      } else if (nranks > 1) {
 #ifdef RK_WITH_NCCL
         ncclUniqueId id;
         std::memcpy(&id, uid, 128);
@@ -1036,6 +1066,7 @@ void rk_ctx_destroy(rk_ctx* c) {
 #ifdef RK_WITH_NCCL
   if (c->comm) ncclCommDestroy(c->comm);
 #endif
+  local_leave(c);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -1086,11 +1117,13 @@ rk_status rk_op_create(rk_ctx* ctx, const rk_grid* g, int nbands, const int8_t* 
                  "bands violate truncation (S:39) or have a zero diagonal: " +
                      std::to_string(bad) + " bad coefficients");
       compute_invdiag(op);
+      exchange_ghost_bands(op);
       op->user_offsets.assign(offsets, offsets + 3 * nbands);
       op->no_chain = std::getenv("RK_NO_CHAIN") != nullptr;
       op->force_chain = std::getenv("RK_FORCE_CHAIN") != nullptr;
     } catch (...) {
       cudaFree(op->bands);
+      cudaFree(op->gbands);
       delete op;
       throw;
     }
@@ -1105,6 +1138,7 @@ rk_status rk_op_update_bands(rk_op* op, const double* bands) {
     const int bad = validate_bands(op);
     RK_REQUIRE(bad == 0, RK_EINVAL, "bands violate truncation (S:39) or have a zero diagonal");
     compute_invdiag(op);
+    exchange_ghost_bands(op);
     ++op->epoch;
   });
 }
@@ -1114,6 +1148,8 @@ void rk_op_destroy(rk_op* op) {
   cudaSetDevice(op->ctx->device);
   cudaStreamSynchronize(op->ctx->stream);
   cudaFree(op->bands);
+  cudaFree(op->gbands);
+  cudaFree(op->rscratch_base);
   for (int i = 0; i < 2; ++i) cudaFree(op->scratch_base[i]);
   delete op;
 }
@@ -1159,7 +1195,16 @@ rk_status rk_precond_apply(rk_op* op, const rk_precond* pc, const double* r, dou
       w.back() = pc->omega_global;
       loc.back() = 0;
       const int zbl = pc->zblocks > 1 ? (int)(op->g.nz_global / pc->zblocks) : 0;
-      chain_run(op, k, w, za, r, nullptr, nullptr, z, za, zb, loc, zbl);
+      const double* rr = r;
+      if (op->ctx->nranks > 1 && chain_max_stages(op) > 0) {
+        // the fused chain reads the sweeps' right-hand side beyond the slab:
+        // a padded copy whose ghost planes chain_run fills
+        double* rp = op->rscratch_base ? op->rscratch_base + GHOST * op->P
+                                       : alloc_padded(op, &op->rscratch_base, nullptr);
+        RK_CUDA(cudaMemcpyAsync(rp, r, sizeof(double) * op->N, cudaMemcpyDeviceToDevice, op->ctx->stream));
+        rr = rp;
+      }
+      chain_run(op, k, w, za, rr, nullptr, nullptr, z, za, zb, loc, zbl);
     }
     RK_CUDA(cudaStreamSynchronize(op->ctx->stream));
   });
@@ -1228,7 +1273,7 @@ rk_status rk_solver_create(rk_op* op, const rk_config* cfg, rk_solver** out) {
       s->o_bi = o;
       o += 8 * (size_t)(s->max_it + 2);
       s->o_eta = o;
-      o += 4 * (size_t)MAXCOL;   // eta(0..2) + C^T r~ (rBiCGStab)
+      o += 5 * (size_t)MAXCOL;   // eta(0..2) + C^T r~ + all-reduce staging (rBiCGStab)
       s->nsc = o;
       RK_CUDA(cudaMalloc(&s->dsc, o * sizeof(double)));
       RK_CUDA(cudaMemsetAsync(s->dsc, 0, o * sizeof(double), s->ctx->stream));

@@ -21,6 +21,13 @@
 namespace rk {
 
 constexpr int MAXCOL = 80;      // columns of one block product ([C V_j w] <= k_max + m + 1)
+// Ghost planes below and above every padded vector: one per stencil stage
+// of a fused chain launch (at most 3), so a chain launch on a z-slab reads
+// its input NST planes beyond the slab after one NST-deep halo exchange.
+constexpr int GHOST = 3;
+// Ghost planes of the bands kept from each z-neighbour on several ranks
+// (the chains recompute NST - 1 <= 2 halo planes of stage 0).
+constexpr int BGHOST = 2;
 constexpr int MAXOUT = 5;       // outputs of one lincomb (dx, u1, c1, u2, c2)
 
 struct Error : std::runtime_error {
@@ -120,6 +127,8 @@ struct ChainParams {
   int zb, zg0;          // z-block size (0 = none) and global z of plane 0 (block-Jacobi)
   int local[3];         // stage s is a local sweep (no coupling across z-blocks)
   const double* gate;   // no-op when *gate != 0 (rBiCGStab lookahead)
+  int ghost;            // several ranks: bands of planes outside [0, nz) from the ghost-band map
+  int rz;               // z coordinate of plane 0 in the rhs tensor map (GHOST: padded rhs)
 };
 
 // Per-iteration device scalars of rBiCGStab (one 64-byte record per iteration).
@@ -175,6 +184,11 @@ struct rk_ctx {
 #ifdef RK_WITH_NCCL
   ncclComm_t comm = nullptr;
 #endif
+  // in-process rank group (comm.cpp, "RKLOCAL:" uids): ranks are contexts of
+  // one process driven by separate host threads; halos are device copies
+  // ordered by events, all-reduces sum the ranks' partials in rank order
+  struct LocalGroup* lgrp = nullptr;
+  cudaEvent_t lev[2] = {nullptr, nullptr};
   // resident CTAs per SM of each kernel instantiation (grid = SMs x occupancy)
   std::unordered_map<const void*, int> occ_cache;
 };
@@ -185,6 +199,10 @@ struct rk_op {
   int S = 7;                    // 7, 19 or 27 (canonical layout)
   int64_t N = 0, P = 0;
   double* bands = nullptr;      // [S][N] canonical bands, then [N] 1/D (invd())
+  double* gbands = nullptr;     // several ranks: [S + 1][2 BGHOST][P] neighbours' band planes
+                                //   (lower BGHOST planes from below, then upper from above; 0 at
+                                //   a non-periodic global boundary), for the fused chains
+  double* rscratch_base = nullptr;   // padded copy of a caller's rhs (rk_precond_apply, ranks > 1)
   const double* invd() const { return bands + (int64_t)S * N; }
   int64_t epoch = 0;
   // scratch (padded) for rk_op_apply / rk_precond_apply
@@ -301,15 +319,18 @@ void stencil(rk_op* op, int mode, const double* x, const double* r, double* out0
              double* out1, double omega, double* red_out, int zb = 0);
 void bdot(rk_ctx* ctx, const std::vector<const double*>& cols, const double* w, int64_t N,
           double* out);
+// reduce = false: the dots stay rank-local (the caller all-reduces them with
+// other values in one collective)
 void bupd(rk_ctx* ctx, const std::vector<const double*>& cols, const double* g, double gscale,
           double* w, int64_t N, const std::vector<const double*>& dots, double* red_out,
-          CoefIn cin = CoefIn{});
+          CoefIn cin = CoefIn{}, bool reduce = true);
 // Recycle projection w <- w - C (C^T w) (+ dots of the new w, as bupd);
 // eta <- C^T w.  One rank: the block dot leaves per-CTA partials and the
 // update kernel sums them (no last-CTA finalisation between the two);
 // otherwise bdot + allreduce + bupd.
 void bproject(rk_ctx* ctx, const std::vector<const double*>& cols, double* w, int64_t N,
-              double* eta, const std::vector<const double*>& dots, double* red_out);
+              double* eta, const std::vector<const double*>& dots, double* red_out,
+              bool reduce = true);
 // [Q^T w, Q^T v] in one read of Q (Gram-corrected CGS2, R19)
 void bdot2(rk_ctx* ctx, const std::vector<const double*>& cols, const double* w, const double* v,
            int64_t N, double* out_w, double* out_v);
@@ -331,13 +352,16 @@ void rotate(rk_ctx* ctx, const std::vector<double*>& cols, const double* T, int6
 // the rest of the iteration's kernels
 void bicg_p(rk_op* op, const double* r, double* p, const double* v, double* z, double wl,
             bool jacobi, BiIter* cur, const BiIter* prev, int first, double thr_conv, double thr_div);
-// rBiCGStab lines 7a + 8 in two launches (one rank; reading R20): the block
-// dot of [C, r~] with v, then one kernel for sigma, v -= C eta, alpha, s, the
-// first sweep of s_hat (z) and ||s||^2.  ctr = C^T r~ (k values, per solve).
-// Returns false (nothing launched) where it does not apply.
+// rBiCGStab lines 7a + 8 in two launches (reading R20): the block dot of
+// [C, r~] with v, then one kernel for sigma, v -= C eta, alpha, s, the first
+// sweep of s_hat (z) and ||s||^2.  ctr = C^T r~ (k values, per solve).  On
+// several ranks the block dot is finalised into `stage` (k + 1 values) and
+// all-reduced once between the two kernels; ||s||^2 stays rank-local (the
+// caller all-reduces it with t^T s, t^T t).  Returns false (nothing
+// launched) where it does not apply.
 bool bicg_proj_s(rk_op* op, const std::vector<const double*>& C, double* v, const double* rtl,
                  const double* ctr, double* eta, const double* r, double* s, double* z, double wl,
-                 bool jacobi, BiIter* cur);
+                 bool jacobi, BiIter* cur, double* stage);
 void bicg_s(rk_op* op, const double* r, const double* v, double* s, double* z, double wl,
             bool jacobi, BiIter* cur);
 void bicg_xr(rk_ctx* ctx, double* x, double* r, const double* s, const double* t, const double* ph,
@@ -353,7 +377,19 @@ void compute_invdiag(rk_op* op);
 void colour_sweep(rk_op* op, double* z, const double* r, double omega, int colour);
 
 // communication (comm.cpp): no-ops for one rank
-void halo(rk_op* op, const double* v);
+// Ghost planes of the padded vector v from the z-neighbours, `depth` planes
+// per side (<= GHOST).
+void halo(rk_op* op, const double* v, int depth = 1);
+// General neighbour exchange of `count` doubles: this rank's lo_src goes to
+// the lower neighbour's hi_dst, its hi_src to the upper neighbour's lo_dst.
+void exchange(rk_op* op, const double* lo_src, const double* hi_src, double* lo_dst, double* hi_dst,
+              size_t count);
 void allreduce(rk_ctx* ctx, double* buf, int n);
+// two reduction outputs (not adjacent in memory) in one collective launch
+void allreduce2(rk_ctx* ctx, double* a, int na, double* b, int nb);
+// in-process rank groups (tests of the multi-rank schedule on one device)
+bool local_uid(const uint8_t* uid);
+void local_join(rk_ctx* ctx, const uint8_t* uid);
+void local_leave(rk_ctx* ctx);
 
 }  // namespace rk
