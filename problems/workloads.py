@@ -84,6 +84,9 @@ WORKLOADS = {
     # 32^3: the smallest porous grid the fused TMA chain tiles (nx % 32, ny % 16)
     "c3m": Workload("c3m", lambda: porous7(32, 3), _hy(8, 8, 2), 6),
     "c4s": Workload("c4s", lambda: channel19(16), _rg(12, 10, 1), 9, epoch_every=3),
+    # 32^3 channel: the smallest 19-point grid the fused 19-point chain tiles
+    # (nx % 32, ny % 8, nz >= 16); hybrid with A epochs (tests, smoke)
+    "c2m": Workload("c2m", lambda: channel19(32), _hy(12, 8, 1, n_sw=2), 4, epoch_every=2),
     "c4hs": Workload("c4hs", lambda: channel19(16), _hy(12, 10, 1), 9, epoch_every=3),
     # 64^3 analogues of c4 with c4's solver parameters (the oracle runs whole
     # sequences in ~1 h; diagnosis of the c4 hybrid, profiles/r02_c4h_diag/)

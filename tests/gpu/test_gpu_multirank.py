@@ -31,7 +31,7 @@ import torch
 
 from oracle import run_sequence
 from problems import OFFSETS7, OFFSETS19, get_workload, slab_range
-from problems.stencils import StencilProblem, channel19
+from problems.stencils import StencilProblem
 
 from test_gpu_parity import compare_sequences, random_op_problem
 
@@ -138,17 +138,10 @@ def test_slab_operator_and_preconditioner_bitwise(rk, wname, R, force, monkeypat
         assert np.array_equal(np.concatenate([r[2] for r in res]), zb1)
 
 
-def _c2m():
-    from dataclasses import replace
-    from problems.workloads import Workload
-    w0 = get_workload("c2s")
-    return Workload("c2m", lambda: channel19(32), replace(w0.params, method="hybrid", n_sw=2), 4, 2, "")
-
-
 @pytest.mark.parametrize("wname,R,force", [("c3s", 2, False), ("c3s", 3, False), ("c2s", 2, False),
                                            ("c2s", 3, False), ("c4hs", 2, False), ("c2m", 2, True)])
 def test_slab_sequence_replicated_state(rk, wname, R, force, monkeypatch):
-    w = _c2m() if wname == "c2m" else get_workload(wname)
+    w = get_workload(wname)
     if force:
         monkeypatch.setenv("RK_FORCE_CHAIN", "1")
     prob = w.problem()

@@ -246,10 +246,7 @@ def test_chain19_solver_paths_bitwise(rk, ctx, monkeypatch):
     -- gives the same iterates, bit for bit, as the unfused path: one hybrid
     sequence on a 32^3 channel operator (periodic x/z) with and without
     RK_FORCE_CHAIN."""
-    from problems.workloads import Workload
-    from dataclasses import replace
-    w0 = get_workload("c2s")
-    w = Workload("c2m", lambda: channel19(32), replace(w0.params, method="hybrid", n_sw=2), 4, 2, "")
+    w = get_workload("c2m")
     monkeypatch.setenv("RK_FORCE_CHAIN", "1")
     g1, sp1 = gpu_sequence(rk, ctx, w)
     monkeypatch.delenv("RK_FORCE_CHAIN")
