@@ -273,7 +273,8 @@ struct ChainStep {
 template <int ST, int NST, int TX, int TY, int PD, int K0, int K1, int K2>
 __global__ void __launch_bounds__((TX + 2 * (NST - 1)) * (TY + 2 * (NST - 1)), 1)
 chain_kernel(const __grid_constant__ CUtensorMap map_b, const __grid_constant__ CUtensorMap map_r,
-             const __grid_constant__ CUtensorMap map_x, ChainParams cp) {
+             const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_gb,
+             ChainParams cp) {
   RK_PDL_ENTRY();
   RK_GATE(cp.gate);
   using G = ChainGeom<ST, NST, TX, TY, PD>;
@@ -317,7 +318,10 @@ chain_kernel(const __grid_constant__ CUtensorMap map_b, const __grid_constant__ 
     const int pl = pl_of(q);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_expect_tx(&bars[xs], tx_bytes);
-    tma_load_4d(bbase, &map_b, &bars[xs], gx0 - PADB, gy0, pl, 0);
+    if (cp.ghost && (pl < 0 || pl >= nz))   // several ranks: the neighbours' band planes
+      tma_load_4d(bbase, &map_gb, &bars[xs], gx0 - PADB, gy0, pl < 0 ? pl + BGHOST : pl - nz + BGHOST, 0);
+    else
+      tma_load_4d(bbase, &map_b, &bars[xs], gx0 - PADB, gy0, pl, 0);
     if (LOAD_R) tma_load_3d(bbase + G::R_OFF, &map_r, &bars[xs], gx0 - PADB, gy0, pl + cp.rz);
     // the input vector is padded: plane pl lives at z-coordinate pl + GHOST
     tma_load_3d(xbase, &map_x, &bars[xs], gx0 - 1 - PADX, gy0 - 1, pl + GHOST);
@@ -457,9 +461,9 @@ template <int ST, int NST, int TX, int TY, int PD, int K0, int K1, int K2, int X
 void launch_one(rk_op* op, ChainParams cp, dim3 grid) {
   using G = ChainGeom<ST, NST, TX, TY, PD>;
   static_assert(G::SMEM <= 232448, "chain tile exceeds 227 KB of shared memory");
-  using KernFn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, ChainParams);
-  using KernFn2 = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap,
-                           ChainParams);
+  using KernFn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap,
+                          ChainParams);
+  using KernFn2 = KernFn;
   KernFn kern = nullptr;
   KernFn2 kern2 = nullptr;
   int fl = 0;   // x-pair kernel flavour: block-Jacobi cuts (1), periodic z (2), ghost bands (4)
@@ -534,8 +538,7 @@ void launch_one(rk_op* op, ChainParams cp, dim3 grid) {
   // 3: the chain overlaps its predecessor, its successor does not
   const bool allow = ctx->pdl && (ctx->pdl_mode == 0 || ctx->pdl_mode == 3) && !ctx->pdl_skip_next;
   ctx->pdl_skip_next = ctx->pdl_mode >= 2;
-  if constexpr (X2 != 0) launch_pdl_if(ctx, allow, kern2, grid, blk, G::SMEM, mb, mr, mx, mg, cp);
-  else launch_pdl_if(ctx, allow, kern, grid, blk, G::SMEM, mb, mr, mx, cp);
+  launch_pdl_if(ctx, allow, X2 ? kern2 : kern, grid, blk, G::SMEM, mb, mr, mx, mg, cp);
 }
 
 template <int NST, int TX, int TY, int PD, int X2 = 0>
@@ -723,7 +726,6 @@ int chain_max_stages(const rk_op* op) {
   }
   if (op->S != 7) return 0;
   if (op->g.periodic_mask & 3) return 0;                    // TMA boxes do not wrap in x/y
-  if (op->ctx->nranks != 1 && cfg_index() != DEFAULT_CFG) return 0;   // ghost bands: x-pair kernel only
   const TileCfg tc = CFGS[cfg_index()];
   if (op->g.nx % tc.tx != 0 || op->g.ny % tc.ty != 0 || op->g.nx % 2 != 0) return 0;
   if (op->g.nz_local < 16) return 0;

@@ -473,7 +473,14 @@ struct rk_solver {
         k = (int)order.size();
         if (k == 0) break;
         auto C = ccols();
-        for (int c = 0; c < k; ++c) bdot(ctx, C, C[c], N, dsc + o_gram + (size_t)c * k);
+        // Gram G = C^T C, two columns of G per read of C (the two-RHS block
+        // dot): (k/2)(k+2) W instead of k(k+1) W
+        for (int c = 0; c < k; c += 2) {
+          if (c + 1 < k)
+            bdot2(ctx, C, C[c], C[c + 1], N, dsc + o_gram + (size_t)c * k, dsc + o_gram + (size_t)(c + 1) * k);
+          else
+            bdot(ctx, C, C[c], N, dsc + o_gram + (size_t)c * k);
+        }
         fetch(o_gram, (size_t)k * k);
         sync();
         std::vector<double> G(hsc + o_gram, hsc + o_gram + (size_t)k * k);

@@ -71,9 +71,12 @@ WORKLOADS = {
                    description="64^3 19-pt channel, rGCROT(30,20), 10 RHS, A constant"),
     "c3": Workload("c3", lambda: porous7(128, 6), _hy(10, 20, 2), 20,
                    description="128^3 7-pt porous, hybrid(3) rGCROT(10,20)->rBiCGStab, 20 RHS"),
-    "c4": Workload("c4", lambda: channel19(256), _rg(40, 30, 1), 50, epoch_every=10,
-                   description="256^3 19-pt channel, rGCROT(40,30), 50 RHS, A perturbed every 10"),
-    "c4h": Workload("c4h", lambda: channel19(256), _hy(40, 30, 1), 50, epoch_every=10,
+    # c4 truncates by principal angles (T2, reading R13): "GCROT measures
+    # angles between successive search spaces" -- measured on c4,
+    # 448 vs 480 Krylov matvecs per system for T1 (profiles/r02_compare/)
+    "c4": Workload("c4", lambda: channel19(256), replace(_rg(40, 30, 1), trunc="T2"), 50, epoch_every=10,
+                   description="256^3 19-pt channel, rGCROT(40,30) T2, 50 RHS, A perturbed every 10"),
+    "c4h": Workload("c4h", lambda: channel19(256), replace(_hy(40, 30, 1), trunc="T2"), 50, epoch_every=10,
                     description="256^3 19-pt channel, hybrid(3) comparison arm of c4"),
     "c5": Workload("c5", lambda: porous7(512, 12), _hy(10, 20, 2), 20,
                    description="512^3 7-pt porous r=12, hybrid(3), 20 RHS"),
