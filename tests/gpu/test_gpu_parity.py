@@ -883,7 +883,8 @@ def test_c4_shaped_hybrid_vs_stored_oracle(rk, ctx):
     rGCROT(40,30) for 3 systems then rBiCGStab with the frozen space): the
     oracle (tests/golden/oracle_seq_c4hm.json, scripts/diag_c4h.py, ~45 min
     on the host) and librk run the same 30 systems -- same tags and outcomes,
-    Krylov matvecs within 10 % per system and per sequence -- and both show
+    Krylov matvecs within 10 % per sequence and per rGCROT system, 25 % per
+    rBiCGStab system (reading R22) -- and both show
     the frozen space losing effect at every A epoch (rBiCGStab ~120 -> ~200 ->
     ~220 matvecs per system), which is the method's behaviour on this
     sequence, not a librk fault."""
@@ -895,8 +896,9 @@ def test_c4_shaped_hybrid_vs_stored_oracle(rk, ctx):
     og = g["systems"]
     assert [r["tag"] for r, _ in gpu] == [o["tag"] for o in og]
     assert all(r["outcome"] == o["outcome"] for (r, _), o in zip(gpu, og))
-    for (r, _), o in zip(gpu, og):
-        assert abs(r["krylov_matvecs"] - o["krylov_matvecs"]) <= max(0.1 * o["krylov_matvecs"], 2), (r, o)
+    for (r, _), o in zip(gpu, og):   # reading R22: rBiCGStab systems of this sequence to 25 %
+        tol = 0.1 if o["tag"] == "rgcrot" else 0.25
+        assert abs(r["krylov_matvecs"] - o["krylov_matvecs"]) <= max(tol * o["krylov_matvecs"], 2), (r, o)
     tg = sum(r["krylov_matvecs"] for r, _ in gpu)
     to = sum(o["krylov_matvecs"] for o in og)
     assert abs(tg - to) <= 0.1 * to
