@@ -600,7 +600,7 @@ void chain_dispatch_cfg(int ci, rk_op* op, const int* k, const ChainParams& cp, 
 // ------------------------------------------------------- 19-point chain
 // Tile of the 19-point chain (chain19.cuh): 32 x TY19 interior cells, TMA
 // prefetch distance PD19.
-constexpr int TY19 = 8, PD19 = 2, NST19 = 2;
+constexpr int TY19 = 8, PD19 = 1, NST19 = 2;
 
 // z chunks for a one-CTA-per-SM kernel with `tiles` x-y tiles: the chunk
 // count c (chunks of >= 16 planes) maximising the wave efficiency

@@ -206,14 +206,17 @@ chain19_kernel(const __grid_constant__ CUtensorMap mbM, const __grid_constant__ 
   }
   mbar_wait(&bars[0], 0);
   mbar_wait(&bars[1], 0);
-  // slot state: x slots of planes tau-1, tau, tau+1; parity of plane tau+1's
-  // barrier; band slot of plane tau
-  int xsm = 0, xs0 = 1, xsp = 2 % NXB;
-  uint32_t parp = 0;
-  int bs0 = 0;
-  auto adv = [](int& v, int n) { v = (v + 1 == n) ? 0 : v + 1; };
-  const double* xslot = reinterpret_cast<const double*>(smem + G::XBASE);
-  constexpr int XS = G::XSLOT / 8;
+  // Slots are compile-time: the step loop is unrolled 4 times and plane
+  // tau - tau0 = 4 it + U uses input-tile slot (U + 1) & 3 (NXB = 4: tiles
+  // of planes tau-1 .. tau+2), band / rhs slot U & 1 (NB = 2), ring slot
+  // U & 3 and register band set U % NST, so every shared-memory access is
+  // one per-thread offset register plus an immediate.
+  static_assert(NXB == 4 && NB == 2 && NST <= 2, "compile-time slots need PD = 1 and NST <= 2");
+  const double* xbase = reinterpret_cast<const double*>(smem + G::XBASE);
+  const double* bbase = reinterpret_cast<const double*>(smem);
+  const double* rbase = reinterpret_cast<const double*>(smem + G::RBASE);
+  constexpr int XS = G::XSLOT / 8, BSD = G::BSLOT / 8, RSD = G::RSLOT / 8, RP = EY * EX;
+  const bool mwarp = warp < G::NWM;   // interior-column warp: band stride EY * TX
 
   double bnd[NST][NBAND];
   double rr[NST];
@@ -223,12 +226,10 @@ chain19_kernel(const __grid_constant__ CUtensorMap mbM, const __grid_constant__ 
 #pragma unroll
     for (int d = 0; d < NBAND; ++d) bnd[s][d] = 0.0;
   }
-  // own z-columns: input at planes tau-1, tau (registers); stage s-1's
-  // outputs at the two planes below the one stage s-1 produced last
-  double xcm = xslot[xsm * XS + xo[1][1]], xcc = xslot[xs0 * XS + xo[1][1]];
-  double hm[NST > 1 ? NST - 1 : 1], hc[NST > 1 ? NST - 1 : 1];
-#pragma unroll
-  for (int s = 0; s < NST - 1; ++s) hm[s] = hc[s] = 0.0;
+  // own z-columns: input at planes tau-1, tau (registers); stage 0's outputs
+  // at the two planes below the one it produced last
+  double xcm = xbase[xo[1][1]], xcc = xbase[XS + xo[1][1]];
+  double hm = 0.0, hc = 0.0;
 
   // y = sum_d a_d v_d in stencil_kernel<19>'s order (even / odd FMA chains)
   auto apply19 = [](const double (&a)[NBAND], const double (&v)[19]) {
@@ -241,19 +242,25 @@ chain19_kernel(const __grid_constant__ CUtensorMap mbM, const __grid_constant__ 
     return ya + yb;
   };
 
-#define RK_C19_STEP(PH)                                                                           \
+#define RK_C19_STEP(U)                                                                            \
   {                                                                                               \
     if (tau >= tau_end) break;                                                                    \
-    if (tau + 1 <= qlast) mbar_wait(&bars[xsp], parp);                                            \
+    constexpr int PH = (U) % NST, XM = (U) & 3, X0 = ((U) + 1) & 3, XP = ((U) + 2) & 3;           \
+    constexpr int BS = (U) & 1;                                                                   \
+    mbar_wait(&bars[XP], (U) < 2 ? par : par ^ 1u);                                               \
     double v0 = 0.0;                                                                              \
     if (active) {                                                                                 \
       /* stage 0 at plane tau: bands / rhs to registers, input neighbours from the tiles */      \
-      const double* bsl = reinterpret_cast<const double*>(smem + bs0 * G::BSLOT) + boff;          \
-      _Pragma("unroll") for (int d = 0; d < NBAND; ++d) bnd[PH][d] = bsl[d * bstr];               \
-      if (LOAD_R) rr[PH] = reinterpret_cast<const double*>(smem + G::RBASE + bs0 * G::RSLOT)[roff]; \
-      const double* tm = xslot + xsm * XS;                                                        \
-      const double* t0 = xslot + xs0 * XS;                                                        \
-      const double* tp = xslot + xsp * XS;                                                        \
+      const double* bsl = bbase + BS * BSD + boff;                                                \
+      if (mwarp) {                                                                                \
+        _Pragma("unroll") for (int d = 0; d < NBAND; ++d) bnd[PH][d] = bsl[d * (EY * TX)];       \
+      } else {                                                                                    \
+        _Pragma("unroll") for (int d = 0; d < NBAND; ++d) bnd[PH][d] = bsl[d * bstr];            \
+      }                                                                                           \
+      if (LOAD_R) rr[PH] = rbase[BS * RSD + roff];                                                \
+      const double* tm = xbase + XM * XS;                                                         \
+      const double* t0 = xbase + X0 * XS;                                                         \
+      const double* tp = xbase + XP * XS;                                                         \
       bool cut_m = false, cut_p = false;                                                          \
       if ((FL & 1) && cp.zb > 0 && cp.local[0]) {                                                 \
         const int g = cp.zg0 + pl_of(tau);                                                        \
@@ -297,101 +304,66 @@ chain19_kernel(const __grid_constant__ CUtensorMap mbM, const __grid_constant__ 
         if (NST == 1) cp.out[nn] = v0;                                                            \
         if (NST == 2 && cp.out_mid) cp.out_mid[nn] = v0;                                          \
       }                                                                                           \
-      if (NST > 1) ring[(tau & 3) * EY * EX + gofs] = v0;                                         \
+      if (NST > 1) ring[XM * RP + gofs] = v0;   /* ring slot (tau - tau0) & 3 == U */            \
       xcm = xcc;                                                                                  \
       xcc = xn;                                                                                   \
     }                                                                                             \
     __syncthreads();                                                                              \
     /* the slots of plane tau-1's tile and plane tau's bands / rhs are free */                    \
-    if (tid == 0 && tau + PD + 1 <= tau_end - 1) issue(tau + PD + 1, xsm, bs0);                  \
-    double up = v0;   /* stage s-1's value at the plane above stage s's, own cell */              \
-    RK_C19_LATER(PH, 1)                                                                           \
-    RK_C19_LATER(PH, 2)                                                                           \
-    xsm = xs0;                                                                                    \
-    xs0 = xsp;                                                                                    \
-    adv(xsp, NXB);                                                                                \
-    if (xsp == 0) parp ^= 1u;                                                                     \
-    adv(bs0, NB);                                                                                 \
+    if (tid == 0 && tau + PD + 1 <= tau_end - 1) issue(tau + PD + 1, XM, BS);                    \
+    if constexpr (NST == 2) {                                                                     \
+      /* stage 1 at plane q = tau - 1: stage 0 at planes q-1, q, q+1 from ring slots           */ \
+      /* (U-2)&3, (U-1)&3, U&3 (own column from registers), bands / rhs of q from set PH ^ 1    */ \
+      constexpr int R = (PH + 1) % 2, RM = ((U) + 2) & 3, R0 = ((U) + 3) & 3, RQ = (U) & 3;       \
+      double vs = 0.0;                                                                            \
+      const int q = tau - 1;                                                                      \
+      if (tau >= tau0 + 2 && interior) {                                                          \
+        const double* rm = ring + RM * RP + gofs;                                                 \
+        const double* r0 = ring + R0 * RP + gofs;                                                 \
+        const double* rp = ring + RQ * RP + gofs;                                                 \
+        bool cut_m = false, cut_p = false;                                                        \
+        if ((FL & 1) && cp.zb > 0 && cp.local[1]) {                                               \
+          const int g = cp.zg0 + pl_of(q);                                                        \
+          cut_m = (g % cp.zb) == 0;                                                               \
+          cut_p = ((g + 1) % cp.zb) == 0;                                                         \
+        }                                                                                         \
+        double v[19];                                                                             \
+        v[0] = hc;                                                                                \
+        v[1] = r0[-1];                                                                            \
+        v[2] = r0[1];                                                                             \
+        v[3] = r0[-EX];                                                                           \
+        v[4] = r0[EX];                                                                            \
+        v[5] = cut_m ? 0.0 : hm;                                                                  \
+        v[6] = cut_p ? 0.0 : v0;                                                                  \
+        v[7] = r0[-EX - 1];                                                                       \
+        v[8] = r0[-EX + 1];                                                                       \
+        v[9] = r0[EX - 1];                                                                        \
+        v[10] = r0[EX + 1];                                                                       \
+        v[11] = cut_m ? 0.0 : rm[-EX];                                                            \
+        v[12] = cut_m ? 0.0 : rm[EX];                                                             \
+        v[13] = cut_p ? 0.0 : rp[-EX];                                                            \
+        v[14] = cut_p ? 0.0 : rp[EX];                                                             \
+        v[15] = cut_m ? 0.0 : rm[-1];                                                             \
+        v[16] = cut_m ? 0.0 : rm[1];                                                              \
+        v[17] = cut_p ? 0.0 : rp[-1];                                                             \
+        v[18] = cut_p ? 0.0 : rp[1];                                                              \
+        const double y = apply19(bnd[R], v);                                                      \
+        vs = (K1 == CK_SWEEP) ? fma(cp.omega[1] * (rr[R] - y), bnd[R][19], hc) : y;               \
+        if (q >= z0 && q < z1) cp.out[(int64_t)pl_of(q) * cp.P + cxy] = vs;                       \
+      }                                                                                           \
+      hm = hc;                                                                                    \
+      hc = v0;                                                                                    \
+    }                                                                                             \
     ++tau;                                                                                        \
   }
 
-  // stage S (1 <= S < NST) at plane q = tau - S: stage S-1's outputs at
-  // planes q-1, q, q+1 from ring S-1 (own column from registers hm / hc /
-  // up), the bands / rhs of plane q from register set (PH - S) mod NST
-#define RK_C19_LATER(PH, S)                                                                       \
-  if constexpr (NST > S) {                                                                        \
-    double vs = 0.0;                                                                              \
-    if constexpr (S > 1) __syncthreads();                                                         \
-    constexpr int R = ((PH) - (S) + 3 * NST) % NST;                                               \
-    const int q = tau - (S);                                                                      \
-    /* cells within NST-1-S of the interior (the next stage's stencil reach) */                 \
-    constexpr int RS = NST - 1 - (S);                                                             \
-    const bool act = (S == NST - 1) ? interior                                                    \
-                                    : (active && c >= -RS && c < TX + RS && ry >= H - RS &&       \
-                                       ry < H + TY + RS);                                         \
-    if (tau >= tau0 + 2 * (S) && act) {                                                           \
-      const double* rg = ring + ((S) - 1) * 4 * EY * EX + gofs;                                   \
-      const double* rm = rg + ((q - 1) & 3) * EY * EX;                                            \
-      const double* r0 = rg + (q & 3) * EY * EX;                                                  \
-      const double* rp = rg + ((q + 1) & 3) * EY * EX;                                            \
-      bool cut_m = false, cut_p = false;                                                          \
-      if ((FL & 1) && cp.zb > 0 && cp.local[S]) {                                                 \
-        const int g = cp.zg0 + pl_of(q);                                                          \
-        cut_m = (g % cp.zb) == 0;                                                                 \
-        cut_p = ((g + 1) % cp.zb) == 0;                                                           \
-      }                                                                                           \
-      const double cc = hc[(S) - 1];                                                              \
-      double v[19];                                                                               \
-      v[0] = cc;                                                                                  \
-      v[1] = r0[-1];                                                                              \
-      v[2] = r0[1];                                                                               \
-      v[3] = r0[-EX];                                                                             \
-      v[4] = r0[EX];                                                                              \
-      v[5] = cut_m ? 0.0 : hm[(S) - 1];                                                           \
-      v[6] = cut_p ? 0.0 : up;                                                                    \
-      v[7] = r0[-EX - 1];                                                                         \
-      v[8] = r0[-EX + 1];                                                                         \
-      v[9] = r0[EX - 1];                                                                          \
-      v[10] = r0[EX + 1];                                                                         \
-      v[11] = cut_m ? 0.0 : rm[-EX];                                                              \
-      v[12] = cut_m ? 0.0 : rm[EX];                                                               \
-      v[13] = cut_p ? 0.0 : rp[-EX];                                                              \
-      v[14] = cut_p ? 0.0 : rp[EX];                                                               \
-      v[15] = cut_m ? 0.0 : rm[-1];                                                               \
-      v[16] = cut_m ? 0.0 : rm[1];                                                                \
-      v[17] = cut_p ? 0.0 : rp[-1];                                                               \
-      v[18] = cut_p ? 0.0 : rp[1];                                                                \
-      const double y = apply19(bnd[R], v);                                                        \
-      vs = (KIND[S] == CK_SWEEP) ? fma(cp.omega[S] * (rr[R] - y), bnd[R][19], cc) : y;            \
-      if (interior && q >= z0 && q < z1) {                                                        \
-        const int64_t nq = (int64_t)pl_of(q) * cp.P + cxy;                                        \
-        if ((S) == NST - 1) cp.out[nq] = vs;                                                      \
-        else if ((S) == NST - 2 && cp.out_mid) cp.out_mid[nq] = vs;                               \
-      }                                                                                           \
-      if ((S) < NST - 1) ring[((S) * 4 + (q & 3)) * EY * EX + gofs] = vs;                         \
-    }                                                                                             \
-    hm[(S) - 1] = hc[(S) - 1];                                                                    \
-    hc[(S) - 1] = up;                                                                             \
-    up = vs;                                                                                      \
+  uint32_t par = 0;   // completion parity of the slots' current round
+  for (int tau = tau0; tau < tau_end; par ^= 1u) {
+    RK_C19_STEP(0)
+    RK_C19_STEP(1)
+    RK_C19_STEP(2)
+    RK_C19_STEP(3)
   }
-
-  if constexpr (NST == 3) {
-    for (int tau = tau0; tau < tau_end;) {
-      RK_C19_STEP(0)
-      RK_C19_STEP(1)
-      RK_C19_STEP(2)
-    }
-  } else if constexpr (NST == 2) {
-    for (int tau = tau0; tau < tau_end;) {
-      RK_C19_STEP(0)
-      RK_C19_STEP(1)
-    }
-  } else {
-    for (int tau = tau0; tau < tau_end;) {
-      RK_C19_STEP(0)
-    }
-  }
-#undef RK_C19_LATER
 #undef RK_C19_STEP
 }
 

@@ -1003,7 +1003,8 @@ def test_full_size_kernels_sampled(rk, ctx, name):
 
 
 @pytest.mark.parametrize("name,force,kw", [("c3m", True, {}), ("c2s", False, {}),
-                                          ("c3s", False, {"precond": "ssor"})])
+                                          ("c3s", False, {"precond": "ssor"}), ("c2m", True, {}),
+                                          ("c2m", True, {"trunc": "T2"})])
 def test_run_to_run_bitwise(rk, ctx, name, force, kw, monkeypatch):
     """Race detection without compute-sanitizer (closed on this pool): every
     reduction is a fixed-order two-stage tree and the chain's shared-memory
