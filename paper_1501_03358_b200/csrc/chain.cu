@@ -441,6 +441,26 @@ void encode(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims,
   RK_REQUIRE(r == CUDA_SUCCESS, RK_ECUDA, "cuTensorMapEncodeTiled failed");
 }
 
+// z chunks for a one-CTA-per-SM kernel with `tiles` x-y tiles: the chunk
+// count c (chunks of >= 16 planes) maximising the wave efficiency
+// tiles c / (slots ceil(tiles c / slots)) times the share of steps that are
+// not wavefront prologue, zc / (zc + 2 halo + 1).
+int pick_chunks(int tiles, int slots, int nzl, int halo) {
+  int best = 1;
+  double bv = -1.0;
+  for (int c = 1; c <= std::max(1, nzl / 16); ++c) {
+    const int zc = (nzl + c - 1) / c;
+    const int ctas = tiles * ((nzl + zc - 1) / zc);
+    const int waves = (ctas + slots - 1) / slots;
+    const double v = (double)ctas / ((double)slots * waves) * zc / (zc + 2.0 * halo + 1.0);
+    if (v > bv + 1e-9) {
+      bv = v;
+      best = c;
+    }
+  }
+  return best;
+}
+
 // The sweeps' right-hand side: the caller's unpadded vector on one rank;
 // on several ranks a padded vector whose ghost planes chain_run filled
 // (cp.rz = GHOST: plane pl at z-coordinate pl + GHOST).
@@ -498,12 +518,12 @@ void launch_one(rk_op* op, ChainParams cp, dim3 grid) {
       occ = it->second;
     }
   }
-  // z chunks: a single wave of SMs x occ CTAs -- chunks = resident slots /
-  // tiles (>= 1), long chunks (>= 16 planes) to amortise the 2 (NST-1)-plane
-  // wavefront prologue
+  // z chunks (>= 16 planes, to amortise the 2 (NST-1)-plane wavefront
+  // prologue) chosen for wave efficiency: 128^3 -> 32 tiles x 4 chunks (one
+  // wave of 128 CTAs), 512^3 -> 512 tiles x 2 chunks (6.9 waves of 148)
   const int nzl = (int)op->g.nz_local;
   const int tiles = (int)(grid.x * grid.y);
-  const int chunks = std::max(1, std::min(op->ctx->sms * occ / std::max(1, tiles), nzl / 16));
+  const int chunks = pick_chunks(tiles, op->ctx->sms * occ, nzl, NST - 1);
   const int zc = std::max(1, std::min((nzl + chunks - 1) / chunks, nzl));
   cp.zc = zc;
   grid.z = (unsigned)((nzl + zc - 1) / zc);
@@ -600,27 +620,7 @@ void chain_dispatch_cfg(int ci, rk_op* op, const int* k, const ChainParams& cp, 
 // ------------------------------------------------------- 19-point chain
 // Tile of the 19-point chain (chain19.cuh): 32 x TY19 interior cells, TMA
 // prefetch distance PD19.
-constexpr int TY19 = 8, PD19 = 1, NST19 = 2;
-
-// z chunks for a one-CTA-per-SM kernel with `tiles` x-y tiles: the chunk
-// count c (chunks of >= 16 planes) maximising the wave efficiency
-// tiles c / (slots ceil(tiles c / slots)) times the share of steps that are
-// not wavefront prologue, zc / (zc + 2 halo + 1).
-int pick_chunks(int tiles, int slots, int nzl, int halo) {
-  int best = 1;
-  double bv = -1.0;
-  for (int c = 1; c <= std::max(1, nzl / 16); ++c) {
-    const int zc = (nzl + c - 1) / c;
-    const int ctas = tiles * ((nzl + zc - 1) / zc);
-    const int waves = (ctas + slots - 1) / slots;
-    const double v = (double)ctas / ((double)slots * waves) * zc / (zc + 2.0 * halo + 1.0);
-    if (v > bv + 1e-9) {
-      bv = v;
-      best = c;
-    }
-  }
-  return best;
-}
+constexpr int TY19 = 8, PD19 = 2, NST19 = 2;
 
 template <int NST, int TX, int TY, int PD, int K0, int K1, int K2>
 void launch19(rk_op* op, ChainParams cp) {

@@ -44,8 +44,8 @@ struct C19Geom {
   static constexpr int NHALO = 2 * H * EY;             // halo-column cells
   static constexpr int NWH = (NHALO + 31) / 32;
   static constexpr int NTHR = 32 * (NWM + NWH);
-  static constexpr int NB = PD + 1;                    // band / rhs slots
-  static constexpr int NXB = PD + 3;                   // input-tile slots (planes tau-1 .. tau+PD+2)
+  static constexpr int NB = PD + 1;                    // band / rhs slots (planes tau .. tau+PD)
+  static constexpr int NXB = 8;                        // input-tile ring (planes tau-1 .. tau+6)
   __host__ __device__ static constexpr int al(int b) { return (b + 127) / 128 * 128; }
   // band slot: regions L, M, R, each [NBAND][EY][w]
   static constexpr int BL_BYTES = NBAND * EY * HW * 8, BM_BYTES = NBAND * EY * TX * 8;
@@ -66,7 +66,7 @@ struct C19Geom {
   static constexpr int RING_BASE = XBASE + NXB * XSLOT;         // stage rings [NST-1][4][EY][EX]
   static constexpr int RING = (NST > 1 ? NST - 1 : 1) * 4 * EY * EX * 8;
   static constexpr int BAR_BASE = RING_BASE + al(RING);
-  static constexpr int SMEM = BAR_BASE + 8 * NXB + 128;
+  static constexpr int SMEM = BAR_BASE + 8 * (NXB + NB) + 128;
 };
 
 // Offsets (in doubles, within one slot) of a cell in a region-split tile:
@@ -147,7 +147,8 @@ chain19_kernel(const __grid_constant__ CUtensorMap mbM, const __grid_constant__ 
   const int tau0 = z0 - H;
   const int tau_end = z1 + H;
   const int qfirst = tau0 - 1, qlast = tau_end;   // input planes read
-  const uint32_t tx_bytes = G::B_BYTES + (LOAD_R ? G::R_BYTES : 0) + G::X_BYTES;
+  const uint32_t b_bytes = G::B_BYTES + (LOAD_R ? G::R_BYTES : 0);
+  uint64_t* bbar = bars + NXB;   // band / rhs slots' barriers
   auto pl_of = [&](int q) { return pz ? (q < 0 ? q + nz : (q >= nz ? q - nz : q)) : q; };
   // x coordinates of the three region boxes (wrapped on a periodic x axis)
   int xl = gx0 - HW, xr = gx0 + TX;
@@ -158,60 +159,63 @@ chain19_kernel(const __grid_constant__ CUtensorMap mbM, const __grid_constant__ 
   auto issue_x = [&](int q, int xs) {   // input tile of plane q (padded vector: z = pl + GHOST)
     unsigned char* xb = smem + G::XBASE + xs * G::XSLOT;
     const int z = pl_of(q) + GHOST;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(&bars[xs], G::X_BYTES);
     tma_load_3d(xb, &mxH, &bars[xs], xl, gy0 - 1, z);
     tma_load_3d(xb + G::X_M, &mxM, &bars[xs], gx0, gy0 - 1, z);
     tma_load_3d(xb + G::X_R, &mxH, &bars[xs], xr, gy0 - 1, z);
   };
-  // batch q: bands / rhs of plane q and the input tile of plane q + 1, on
-  // the mbarrier of that tile's slot
-  auto issue = [&](int q, int xs, int bs) {
+  // band batch q: the bands (+ 1/D) and rhs of plane q, on band slot bs's barrier
+  auto issue_b = [&](int q, int bs) {
     unsigned char* bb = smem + bs * G::BSLOT;
     unsigned char* rb = smem + G::RBASE + bs * G::RSLOT;
     const int pl = pl_of(q);
+    uint64_t* bar = &bbar[bs];
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_expect_tx(&bars[xs], tx_bytes);
+    mbar_expect_tx(bar, b_bytes);
     if ((FL & 4) && (pl < 0 || pl >= nz)) {
       const int gz = pl < 0 ? pl + BGHOST : pl - nz + BGHOST;
-      tma_load_4d(bb, &mgH, &bars[xs], xl, gy0, gz, 0);
-      tma_load_4d(bb + G::B_M, &mgM, &bars[xs], gx0, gy0, gz, 0);
-      tma_load_4d(bb + G::B_R, &mgH, &bars[xs], xr, gy0, gz, 0);
+      tma_load_4d(bb, &mgH, bar, xl, gy0, gz, 0);
+      tma_load_4d(bb + G::B_M, &mgM, bar, gx0, gy0, gz, 0);
+      tma_load_4d(bb + G::B_R, &mgH, bar, xr, gy0, gz, 0);
     } else {
-      tma_load_4d(bb, &mbH, &bars[xs], xl, gy0, pl, 0);
-      tma_load_4d(bb + G::B_M, &mbM, &bars[xs], gx0, gy0, pl, 0);
-      tma_load_4d(bb + G::B_R, &mbH, &bars[xs], xr, gy0, pl, 0);
+      tma_load_4d(bb, &mbH, bar, xl, gy0, pl, 0);
+      tma_load_4d(bb + G::B_M, &mbM, bar, gx0, gy0, pl, 0);
+      tma_load_4d(bb + G::B_R, &mbH, bar, xr, gy0, pl, 0);
     }
     if (LOAD_R) {
       const int rzz = pl + cp.rz;
-      tma_load_3d(rb, &mrH, &bars[xs], xl, gy0, rzz);
-      tma_load_3d(rb + G::R_M, &mrM, &bars[xs], gx0, gy0, rzz);
-      tma_load_3d(rb + G::R_R, &mrH, &bars[xs], xr, gy0, rzz);
+      tma_load_3d(rb, &mrH, bar, xl, gy0, rzz);
+      tma_load_3d(rb + G::R_M, &mrM, bar, gx0, gy0, rzz);
+      tma_load_3d(rb + G::R_R, &mrH, bar, xr, gy0, rzz);
     }
-    issue_x(q + 1, xs);
   };
 
   if (tid == 0) {
-    for (int s = 0; s < NXB; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < NXB + NB; ++s) mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  // prologue: tiles qfirst (slot 0) and tau0 (slot 1) alone, then batches
-  // tau0 .. tau0 + PD (batch q's tile of plane q + 1 goes to slot q + 1 - qfirst)
+  // prologue: input tiles qfirst .. qfirst + 7 (plane p in slot p - qfirst),
+  // bands of planes tau0 .. tau0 + PD (plane q in slot q - tau0)
   if (tid == 0) {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_expect_tx(&bars[0], G::X_BYTES);
-    issue_x(qfirst, 0);
-    mbar_expect_tx(&bars[1], G::X_BYTES);
-    issue_x(qfirst + 1, 1);
-    for (int q = tau0; q <= min(tau0 + PD, tau_end - 1); ++q) issue(q, (q + 1 - qfirst) % NXB, (q - tau0) % NB);
+    for (int p = qfirst; p <= min(qfirst + NXB - 1, qlast); ++p) issue_x(p, p - qfirst);
+    for (int q = tau0; q <= min(tau0 + PD, tau_end - 1); ++q) issue_b(q, q - tau0);
   }
   mbar_wait(&bars[0], 0);
   mbar_wait(&bars[1], 0);
-  // Slots are compile-time: the step loop is unrolled 4 times and plane
-  // tau - tau0 = 4 it + U uses input-tile slot (U + 1) & 3 (NXB = 4: tiles
-  // of planes tau-1 .. tau+2), band / rhs slot U & 1 (NB = 2), ring slot
-  // U & 3 and register band set U % NST, so every shared-memory access is
-  // one per-thread offset register plus an immediate.
-  static_assert(NXB == 4 && NB == 2 && NST <= 2, "compile-time slots need PD = 1 and NST <= 2");
+  // Input-tile slots are compile-time: the step loop is unrolled 8 times and
+  // plane tau - tau0 = 8 it + U reads tiles of planes tau-1, tau, tau+1 from
+  // slots U, U+1, U+2 (mod 8; plane p lives in slot (p - qfirst) & 7), ring
+  // slot U & 3 and register band set U % NST, so every input / ring access is
+  // a per-thread offset register plus an immediate.  Tiles are issued 7
+  // planes ahead (after step tau's barrier, plane tau + 7 into the slot of
+  // plane tau - 1); the PD + 1 band slots rotate at run time (one pointer per
+  // step, then immediates), bands of plane tau + PD + 1 issued after step
+  // tau's barrier into plane tau's slot.
+  static_assert(NXB == 8 && NST <= 2, "compile-time input slots need an 8-slot ring and NST <= 2");
+  int bs0 = 0;             // band slot of plane tau
+  uint32_t bpar = 0;       // its barrier parity
   const double* xbase = reinterpret_cast<const double*>(smem + G::XBASE);
   const double* bbase = reinterpret_cast<const double*>(smem);
   const double* rbase = reinterpret_cast<const double*>(smem + G::RBASE);
@@ -228,7 +232,7 @@ chain19_kernel(const __grid_constant__ CUtensorMap mbM, const __grid_constant__ 
   }
   // own z-columns: input at planes tau-1, tau (registers); stage 0's outputs
   // at the two planes below the one it produced last
-  double xcm = xbase[xo[1][1]], xcc = xbase[XS + xo[1][1]];
+  double xcm = xbase[xo[1][1]], xcc = xbase[XS + xo[1][1]];   // planes qfirst, tau0: slots 0, 1
   double hm = 0.0, hc = 0.0;
 
   // y = sum_d a_d v_d in stencil_kernel<19>'s order (even / odd FMA chains)
@@ -245,19 +249,19 @@ chain19_kernel(const __grid_constant__ CUtensorMap mbM, const __grid_constant__ 
 #define RK_C19_STEP(U)                                                                            \
   {                                                                                               \
     if (tau >= tau_end) break;                                                                    \
-    constexpr int PH = (U) % NST, XM = (U) & 3, X0 = ((U) + 1) & 3, XP = ((U) + 2) & 3;           \
-    constexpr int BS = (U) & 1;                                                                   \
-    mbar_wait(&bars[XP], (U) < 2 ? par : par ^ 1u);                                               \
+    constexpr int PH = (U) % NST, XM = (U) & 7, X0 = ((U) + 1) & 7, XP = ((U) + 2) & 7;           \
+    mbar_wait(&bbar[bs0], bpar);                                                                  \
+    mbar_wait(&bars[XP], (U) < 6 ? par : par ^ 1u);                                               \
     double v0 = 0.0;                                                                              \
     if (active) {                                                                                 \
       /* stage 0 at plane tau: bands / rhs to registers, input neighbours from the tiles */      \
-      const double* bsl = bbase + BS * BSD + boff;                                                \
+      const double* bsl = bbase + bs0 * BSD + boff;                                               \
       if (mwarp) {                                                                                \
         _Pragma("unroll") for (int d = 0; d < NBAND; ++d) bnd[PH][d] = bsl[d * (EY * TX)];       \
       } else {                                                                                    \
         _Pragma("unroll") for (int d = 0; d < NBAND; ++d) bnd[PH][d] = bsl[d * bstr];            \
       }                                                                                           \
-      if (LOAD_R) rr[PH] = rbase[BS * RSD + roff];                                                \
+      if (LOAD_R) rr[PH] = rbase[bs0 * RSD + roff];                                               \
       const double* tm = xbase + XM * XS;                                                         \
       const double* t0 = xbase + X0 * XS;                                                         \
       const double* tp = xbase + XP * XS;                                                         \
@@ -304,13 +308,16 @@ chain19_kernel(const __grid_constant__ CUtensorMap mbM, const __grid_constant__ 
         if (NST == 1) cp.out[nn] = v0;                                                            \
         if (NST == 2 && cp.out_mid) cp.out_mid[nn] = v0;                                          \
       }                                                                                           \
-      if (NST > 1) ring[XM * RP + gofs] = v0;   /* ring slot (tau - tau0) & 3 == U */            \
+      if (NST > 1) ring[((U) & 3) * RP + gofs] = v0;   /* ring slot (tau - tau0) & 3 */          \
       xcm = xcc;                                                                                  \
       xcc = xn;                                                                                   \
     }                                                                                             \
     __syncthreads();                                                                              \
     /* the slots of plane tau-1's tile and plane tau's bands / rhs are free */                    \
-    if (tid == 0 && tau + PD + 1 <= tau_end - 1) issue(tau + PD + 1, XM, BS);                    \
+    if (tid == 0) {                                                                               \
+      if (tau + 7 <= qlast) issue_x(tau + 7, XM);                                                 \
+      if (tau + PD + 1 <= tau_end - 1) issue_b(tau + PD + 1, bs0);                                \
+    }                                                                                             \
     if constexpr (NST == 2) {                                                                     \
       /* stage 1 at plane q = tau - 1: stage 0 at planes q-1, q, q+1 from ring slots           */ \
       /* (U-2)&3, (U-1)&3, U&3 (own column from registers), bands / rhs of q from set PH ^ 1    */ \
@@ -354,6 +361,10 @@ chain19_kernel(const __grid_constant__ CUtensorMap mbM, const __grid_constant__ 
       hm = hc;                                                                                    \
       hc = v0;                                                                                    \
     }                                                                                             \
+    if (++bs0 == NB) {                                                                            \
+      bs0 = 0;                                                                                    \
+      bpar ^= 1u;                                                                                 \
+    }                                                                                             \
     ++tau;                                                                                        \
   }
 
@@ -363,6 +374,10 @@ chain19_kernel(const __grid_constant__ CUtensorMap mbM, const __grid_constant__ 
     RK_C19_STEP(1)
     RK_C19_STEP(2)
     RK_C19_STEP(3)
+    RK_C19_STEP(4)
+    RK_C19_STEP(5)
+    RK_C19_STEP(6)
+    RK_C19_STEP(7)
   }
 #undef RK_C19_STEP
 }
