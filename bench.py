@@ -120,16 +120,21 @@ class Clocks:
 
 
 # ------------------------------------------------------------------ oracle
-def oracle_matvec_sample(workload, planes=None, threads=None, host_bands=None):
+def oracle_matvec_sample(workload, planes=32, threads=None):
     """The oracle as it stands (oracle.krylov.rgcrot, untuned), timed on this
-    host: ONE rGCROT Krylov step (m = 1: one preconditioned operator
-    application M^-1 A v, the CGS2 orthogonalisation, the cycle end with its
-    true residual) against a recycle space of k + m/2 columns -- the average
-    width [C V_j] of a cycle of the workload's rGCROT(m, k) -- built from a
-    random orthonormal C (the cost of a step does not depend on the space's
-    quality).  `planes`: time the first `planes` z-planes of the grid as
-    their own grid and scale by nz / planes (every oracle operation is
-    linear in N).  Returns ms per Krylov matvec on the full grid."""
+    host on a bounded sample: the workload's operator on its first `planes`
+    z-planes (a grid of its own; every oracle operation is linear in N, so
+    times scale by nz / planes -- checked: 32 and 64 planes of c4 take 7.7 and
+    15.0 s per m = 1 cycle), a recycle space of k + m/2 columns (the average
+    [C V_j] width of an rGCROT(m, k) cycle; a random orthonormal C -- the cost
+    does not depend on the space's quality) and one rGCROT cycle with m = 1
+    and one with m = 4 Krylov steps.  A third of their difference is the
+    marginal cost of a Krylov matvec (the preconditioned operator application
+    and its CGS2 orthogonalisation); the rest of the m = 1 cycle is the
+    per-cycle cost (the
+    M^-1 b / re-projection at the start, the cycle end's update, true
+    residual and line-14a update).  Returns full-grid ms per Krylov matvec,
+    ms per cycle, and the space width."""
     from dataclasses import replace
     from oracle.krylov import rgcrot
     from oracle.stencil import Jacobi, Operator
@@ -137,9 +142,8 @@ def oracle_matvec_sample(workload, planes=None, threads=None, host_bands=None):
     w = get_workload(workload)
     prm = w.params
     prob = w.problem()
-    nz = prob.nz if planes is None else planes
-    bands = host_bands if (host_bands is not None and planes is None) else prob.bands(0, nz)
-    op = Operator(prob.nx, prob.ny, nz, prob.periodic, prob.offsets, bands, check=planes is None)
+    nz = min(planes, prob.nz)
+    op = Operator(prob.nx, prob.ny, nz, prob.periodic, prob.offsets, prob.bands(0, nz), check=False)
     pc = Jacobi(op, prm.sweeps, prm.omega_l, prm.omega_g)
     b = prob.rhs(0, 0, nz).reshape(-1)
     kk = prm.k_max + prm.m // 2
@@ -147,42 +151,49 @@ def oracle_matvec_sample(workload, planes=None, threads=None, host_bands=None):
     C, _ = np.linalg.qr(rng.standard_normal((op.N, kk)))
     U = rng.standard_normal((op.N, kk))
 
-    def run():
+    def cycle(m):
         t0 = time.perf_counter()
-        _, _, _, rep = rgcrot(op, pc, b, U, C, replace(prm, m=1, k_max=kk + 2, max_mv=1, tol=1e-30),
+        _, _, _, rep = rgcrot(op, pc, b, U, C, replace(prm, m=m, k_max=kk + 2, max_mv=m, tol=1e-30),
                               valid=True)
-        return time.perf_counter() - t0, rep
+        assert rep.krylov_mv == m and rep.cycles == 1
+        return time.perf_counter() - t0
+
+    def both():
+        return cycle(1), cycle(4)
 
     if threads is None:
-        dt, rep = run()
+        t1, t2 = both()
     else:
         from threadpoolctl import threadpool_limits
         with threadpool_limits(limits=threads):
-            dt, rep = run()
-    assert rep.krylov_mv == 1
-    return 1e3 * dt * (prob.nz / nz), kk
+            t1, t2 = both()
+    scale = 1e3 * prob.nz / nz
+    mv = max(t2 - t1, 0.0) / 3.0
+    return mv * scale, max(t1 - mv, 0.0) * scale, kk, nz
 
 
 # ------------------------------------------------------------------ reference arm
 def run_reference(args):
-    """--impl reference: the CPU oracle, one bounded sample per step: one
-    rGCROT Krylov step of the workload on its first 32 z-planes, scaled to
-    the full grid, times the matvecs per system of the workload (below)."""
+    """--impl reference: the CPU oracle, one bounded sample per step (the
+    two cycles of oracle_matvec_sample on the first 16 z-planes,
+    scaled to the full grid), composed into ms per system with the
+    workload's Krylov matvecs and cycles per system (below)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from problems import get_workload
     w = get_workload(args.workload)
-    planes = min(32, w.problem().nz)
-    ms = []
-    kk = None
-    for i in range(args.warmup + args.steps):
-        v, kk = oracle_matvec_sample(args.workload, planes=planes)
+    mvs, cys = [], []
+    kk = nz = None
+    for i in range(args.warmup + args.steps):   # 16 planes: ~12 s per step on the box's host
+        a, c, kk, nz = oracle_matvec_sample(args.workload, planes=16)
         if i >= args.warmup:
-            ms.append(v)
-    ms_mv = float(np.mean(ms))
+            mvs.append(a)
+            cys.append(c)
+    ms_mv, ms_cy = float(np.mean(mvs)), float(np.mean(cys))
     mv_sys = MV_PER_SYSTEM.get(args.workload, 100.0)
-    value = ms_mv * mv_sys
+    cy_sys = mv_sys / w.params.m
+    value = ms_mv * mv_sys + ms_cy * cy_sys
     cores = os.cpu_count()
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "ms/system",
@@ -192,12 +203,12 @@ def run_reference(args):
         "config": {"workload": f"{args.workload}: {w.description}", "l2": "inputs larger than L2"},
         "cpu_baseline": {"value": round(value, 3), "unit": "ms/system", "cores": cores,
                          "cpu_model": cpu_model(), "kind": "oracle",
-                         "sample": (f"per step: oracle rGCROT, one Krylov step (m=1) against a "
-                                    f"{kk}-column recycle space, on the first {planes} z-planes of "
-                                    f"the {args.workload} grid, scaled to the full grid: "
-                                    f"{ms_mv:.0f} ms per Krylov matvec x {mv_sys} matvecs per "
-                                    f"system ({MV_SOURCE}) (NumPy; stencil and elementwise work "
-                                    f"single-threaded, BLAS on all cores)")},
+                         "sample": (f"per step: oracle rGCROT cycles with m=1 and m=4 Krylov steps against "
+                                    f"a {kk}-column recycle space on the first {nz} z-planes of the "
+                                    f"{args.workload} grid, scaled to the full grid: {ms_mv:.0f} ms per "
+                                    f"Krylov matvec + {ms_cy:.0f} ms per cycle, x {mv_sys} matvecs and "
+                                    f"{cy_sys:.1f} cycles per system ({MV_SOURCE}) (NumPy; stencil and "
+                                    f"elementwise work single-threaded, BLAS on all cores)")},
         "e2e": {"value": round(value, 3), "unit": "ms/system", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -206,12 +217,12 @@ def run_reference(args):
 
 # Krylov matvecs per system used to turn the oracle's ms per matvec into ms
 # per system in the reference arm (a separate process that cannot see the
-# GPU arm's counts): the mean over systems 5-24 of the c4 rGCROT(40,30) run
-# (profiles/r02_bench_c4.json); GPU and oracle counts agree per system within
-# one cycle (tests/gpu/test_gpu_parity.py).  The GPU arm's own cpu_baseline
-# uses the counts of its own timed systems.
-MV_PER_SYSTEM = {"c4": 480.0, "c3": 178.8}
-MV_SOURCE = "mean Krylov matvecs per timed system of the GPU run, profiles/r02_bench_c4.json"
+# GPU arm's counts): the mean over systems 5-24 of the c4 rGCROT(40,30) T2
+# run (profiles/r02_bench_c4_T2.json); GPU and oracle counts agree per system
+# within one cycle (tests/gpu/test_gpu_parity.py).  The GPU arm's own
+# cpu_baseline uses the counts of its own timed systems.
+MV_PER_SYSTEM = {"c4": 430.0, "c3": 178.8}
+MV_SOURCE = "mean Krylov matvecs per timed system of the GPU run, profiles/r02_bench_c4_T2.json"
 
 
 # ------------------------------------------------------------------ GPU arm
@@ -243,8 +254,7 @@ def run_rk(args):
     ctx = rk.Context(local, rank, world, uid)
     stream = torch.cuda.current_stream()
     epoch_of = lambda s: w.epoch(s % T)          # cyclic sequence
-    host_bands0 = prob.bands(z0, z1, epoch=epoch_of(0))
-    epoch_bands = {epoch_of(0): torch.from_numpy(host_bands0).cuda()}
+    epoch_bands = {epoch_of(0): torch.from_numpy(prob.bands(z0, z1, epoch=epoch_of(0))).cuda()}
 
     def bands_for(e):
         if e not in epoch_bands:
@@ -312,6 +322,7 @@ def run_rk(args):
         ms = float(t.item())
     value = ms / K
     mv = [r["krylov_matvecs"] for r in reps]
+    cycles = [r["cycles_or_iters"] for r in reps]
     outcomes = [r["outcome"] for r in reps]
     # e2e: the same K systems from the same recycle-space state, host buffers
     e2e = None
@@ -394,18 +405,20 @@ def run_rk(args):
     B.clear()
     torch.cuda.empty_cache()
     if world == 1 and not args.no_cpu_baseline:
-        ms_all, kk = oracle_matvec_sample(args.workload, host_bands=host_bands0)
-        ms_one, _ = oracle_matvec_sample(args.workload, threads=1, host_bands=host_bands0)
+        a_all, c_all, kk, nzs = oracle_matvec_sample(args.workload)
+        a_one, c_one, _, _ = oracle_matvec_sample(args.workload, threads=1)
         mvs = float(np.mean(mv))
+        cys = float(np.mean(cycles))
         line["cpu_baseline"] = {
-            "value": round(ms_all * mvs, 1), "unit": "ms/system", "cores": os.cpu_count(),
-            "value_1thread": round(ms_one * mvs, 1), "cpu_model": cpu_model(), "kind": "oracle",
-            "sample": (f"oracle rGCROT, one Krylov step (m=1) against a {kk}-column recycle space "
-                       f"(the average [C V_j] width of an rGCROT({prm.m},{prm.k_max}) cycle) on the "
-                       f"full {prob.nx}x{prob.ny}x{prob.nz} grid: {ms_all:.0f} ms per Krylov matvec "
-                       f"with BLAS on all {os.cpu_count()} cores, {ms_one:.0f} ms on 1 thread; times "
-                       f"the GPU run's {mvs:.1f} Krylov matvecs per timed system (NumPy stencil and "
-                       f"elementwise work is single-threaded in both settings)")}
+            "value": round(a_all * mvs + c_all * cys, 1), "unit": "ms/system", "cores": os.cpu_count(),
+            "value_1thread": round(a_one * mvs + c_one * cys, 1), "cpu_model": cpu_model(), "kind": "oracle",
+            "sample": (f"oracle rGCROT cycles with m=1 and m=4 Krylov steps against a {kk}-column recycle "
+                       f"space (the average [C V_j] width of an rGCROT({prm.m},{prm.k_max}) cycle) on the "
+                       f"first {nzs} z-planes of the {prob.nx}x{prob.ny}x{prob.nz} grid, scaled to the full "
+                       f"grid: {a_all:.0f} ms per Krylov matvec + {c_all:.0f} ms per cycle with BLAS on all "
+                       f"{os.cpu_count()} cores ({a_one:.0f} + {c_one:.0f} ms on 1 thread); times the GPU "
+                       f"run's {mvs:.1f} Krylov matvecs and {cys:.1f} cycles per timed system (NumPy "
+                       f"stencil and elementwise work is single-threaded in both settings)")}
     text = json.dumps(line)
     print(text, flush=True)
     if args.out:
