@@ -90,6 +90,8 @@ def _random_problem(nx, ny, nz, periodic, offsets, seed):
 
 
 PROBLEMS = {
+    "c4_full": lambda: get_workload("c4").problem(),
+    "c3_full": lambda: get_workload("c3").problem(),
     "c3s": lambda: get_workload("c3s").problem(),
     "c2s": lambda: get_workload("c2s").problem(),
     "rand7_64x32x48": lambda: _random_problem(64, 32, 48, 0, OFFSETS7, 31),
@@ -100,6 +102,7 @@ PROBLEMS = {
 
 
 @pytest.mark.parametrize("wname,R,force", [
+    ("c4_full", 2, False), ("c3_full", 4, False),      # full size: the chains by the L2 rule
     ("c3s", 2, False), ("c3s", 3, False), ("c2s", 2, False), ("c2s", 3, False),
     ("rand7_64x32x48", 2, True), ("rand7_64x32x48", 3, True), ("rand7_64x32x48_pz", 2, True),
     ("rand19_64x16x40_pxz", 2, True), ("rand19_32x24x48", 3, True)])
