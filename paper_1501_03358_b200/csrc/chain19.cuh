@@ -235,15 +235,14 @@ chain19_kernel(const __grid_constant__ CUtensorMap mbM, const __grid_constant__ 
   double xcm = xbase[xo[1][1]], xcc = xbase[XS + xo[1][1]];   // planes qfirst, tau0: slots 0, 1
   double hm = 0.0, hc = 0.0;
 
-  // y = sum_d a_d v_d in stencil_kernel<19>'s order (even / odd FMA chains)
+  // y = sum_d a_d v_d in stencil_kernel<19>'s order: four FMA chains (band
+  // d mod 4), summed as (c0 + c1) + (c2 + c3) -- half the dependent-FMA
+  // latency of two chains (the "wait" stall led the PC samples)
   auto apply19 = [](const double (&a)[NBAND], const double (&v)[19]) {
-    double ya = 0.0, yb = 0.0;
+    double c[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-    for (int d = 0; d < 19; ++d) {
-      if (d % 2 == 0) ya = fma(a[d], v[d], ya);
-      else yb = fma(a[d], v[d], yb);
-    }
-    return ya + yb;
+    for (int d = 0; d < 19; ++d) c[d % 4] = fma(a[d], v[d], c[d % 4]);
+    return (c[0] + c[1]) + (c[2] + c[3]);
   };
 
 #define RK_C19_STEP(U)                                                                            \

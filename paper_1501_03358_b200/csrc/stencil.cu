@@ -104,11 +104,16 @@ __global__ void __launch_bounds__(256) stencil_kernel(StencilParams sp) {
           if (cut_p) xl[dy][2] = xr[dy][2] = 0.0;
         }
       }
-      // two interleaved FMA chains (even / odd bands), summed at the end --
-      // the same order as the fused chain kernel (chain.cu)
-      double y[VEC], ya[VEC], yb[VEC], a0[VEC];
+      // interleaved FMA chains -- two (even / odd bands) for 7 points, four
+      // (band d mod 4) for 19 / 27 points, summed at the end as (c0 + c1) + (c2
+      // + c3) -- the same order as the fused chain kernels (chain.cu,
+      // chain_x2.cuh, chain19.cuh)
+      constexpr int NCH = ST >= 19 ? 4 : 2;
+      double y[VEC], acc[NCH][VEC], a0[VEC];
 #pragma unroll
-      for (int t = 0; t < VEC; ++t) ya[t] = yb[t] = 0.0;
+      for (int t = 0; t < VEC; ++t)
+#pragma unroll
+        for (int q = 0; q < NCH; ++q) acc[q][t] = 0.0;
 #pragma unroll
       for (int d = 0; d < ST; ++d) {
         int dx = 0, dy = 0, dz = 0;
@@ -122,12 +127,12 @@ __global__ void __launch_bounds__(256) stencil_kernel(StencilParams sp) {
           else if (dx < 0) xv = (t == 0) ? xl[dy + 1][dz + 1] : c.v[t - 1];
           else xv = (t == VEC - 1) ? xr[dy + 1][dz + 1] : c.v[t + 1];
           if (d == 0) a0[t] = a.v[t];
-          if (d % 2 == 0) ya[t] = fma(a.v[t], xv, ya[t]);
-          else yb[t] = fma(a.v[t], xv, yb[t]);
+          acc[d % NCH][t] = fma(a.v[t], xv, acc[d % NCH][t]);
         }
       }
 #pragma unroll
-      for (int t = 0; t < VEC; ++t) y[t] = ya[t] + yb[t];
+      for (int t = 0; t < VEC; ++t)
+        y[t] = NCH == 4 ? (acc[0][t] + acc[1][t]) + (acc[2 % NCH][t] + acc[3 % NCH][t]) : acc[0][t] + acc[1][t];
       const Vec<VEC>& x0 = xc[1][1];
       Vec<VEC> o0, o1, iD;
       if constexpr (MODE == SM_SPMV_SWEEP1 || MODE == SM_SWEEP || MODE == SM_SWEEP_NORM ||
