@@ -25,7 +25,7 @@
 //  * Threads: one per cell.  Warps 0 .. EY-1 own the interior columns of one
 //    tile row each (32 lanes = TX columns: conflict-free, row-aligned shared
 //    loads); the last warps own the 2 H halo columns of every row.
-// Per-cell arithmetic (band order, two FMA chains, 1/D band) is that of
+// Per-cell arithmetic (band order, four FMA chains, 1/D band) is that of
 // stencil_kernel<19>, so fused and unfused paths agree bit for bit.
 #pragma once
 
