@@ -187,3 +187,54 @@ def test_slab_sequence_replicated_state(rk, wname, R, force, monkeypatch):
     gpu = [(res[0][0][t], np.concatenate([res[r][1][t] for r in range(R)])) for t in range(T)]
     ora = run_sequence(w)
     compare_sequences(w, gpu, ora, prm.method)
+
+
+def test_full_size_c4_solve_two_slabs_vs_one_rank(rk):
+    """SURVEY §8(d) "GPU-vs-GPU parity: c4/c5 at P > 1 vs P = 1" at full size,
+    on one GPU through the in-process rank group: system 0 of c4 (256^3
+    19-point channel, rGCROT(40,30) T2 from an empty space) on 2 z-slabs of
+    128 planes -- fused 19-point chains with deep halos and ghost bands,
+    all-reduced reductions -- against the one-rank solve: both converge, the
+    Krylov matvec counts agree within one cycle, and both solutions are
+    certified solutions (true residual <= tol ||b||, recomputed here by the
+    oracle's operator); they agree to 1e-4 relative -- the channel operator is
+    ill-conditioned, so two tol-converged solutions may differ by more than the
+    north star's 1e-6 (reading R12), and the reductions differ in order."""
+    w = get_workload("c4")
+    prob = w.problem()
+    prm = w.params
+    b = prob.rhs(0).reshape(-1)
+    ctx1 = rk.Context(0)
+    op1 = rk.GridOperator(ctx1, prob.nx, prob.ny, prob.nz, prob.offsets, dev(prob.bands()), prob.periodic)
+    s1 = rk.Solver(op1, rk.config_from_params(prm))
+    x1, r1 = s1.solve(dev(b))
+    x1 = x1.cpu().numpy()
+    s1.close()
+    op1.close()
+    ctx1.close()
+    P = prob.nx * prob.ny
+
+    def rank(r):
+        st = torch.cuda.Stream()
+        with torch.cuda.stream(st):
+            ctx, op, z0, z1 = slab_op(rk, prob, r, 2, "c4_full_solve", st)
+            s = rk.Solver(op, rk.config_from_params(prm))
+            x, rep = s.solve(dev(b[z0 * P:z1 * P]))
+            st.synchronize()
+            out = (rep, x.cpu().numpy())
+            s.close()
+            op.close()
+            ctx.close()
+            return out
+
+    res = run_ranks(2, rank, timeout=1200)
+    assert r1["outcome"] == "CONVERGED" and all(rep["outcome"] == "CONVERGED" for rep, _ in res)
+    assert res[0][0]["krylov_matvecs"] == res[1][0]["krylov_matvecs"]
+    assert abs(res[0][0]["krylov_matvecs"] - r1["krylov_matvecs"]) <= prm.m
+    x2 = np.concatenate([x for _, x in res])
+    from oracle.stencil import Operator
+    A = Operator.from_problem(prob)
+    bn = np.linalg.norm(b)
+    for x in (x1, x2):
+        assert np.linalg.norm(b - A.apply(x)) <= prm.tol * bn * (1 + 1e-6)
+    assert np.linalg.norm(x2 - x1) <= 1e-4 * np.linalg.norm(x1)

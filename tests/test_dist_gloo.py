@@ -6,9 +6,11 @@ planes with the z-neighbours -- first every rank sends its TOP plane up and
 receives its lower ghost from below, then sends its BOTTOM plane down and
 receives its upper ghost from above (periodic z: a ring) -- and sums every
 batch of partial dot products with one all-reduce, so the tiny Krylov state
-(H, B, alpha, ...) is replicated bit-identically.  No GPU is available to
-run that NCCL code here; these tests run the SAME protocol with gloo over
-world_size 2 and 3 and check, against the single-domain oracle:
+(H, B, alpha, ...) is replicated bit-identically.  librk's OWN schedule of
+those calls runs at world 2/3 in tests/gpu/test_gpu_multirank.py (an
+in-process rank group on one GPU); here, without a GPU, the same protocol
+runs with gloo over world_size 2 and 3 and is checked against the
+single-domain oracle:
   * halo exchange + local stencil == global SpMV (periodic and Dirichlet z),
   * the Jacobi(5+1) preconditioner with a halo per sweep == global M^-1,
   * block Jacobi with one z-block per rank and NO halo in the local sweeps
