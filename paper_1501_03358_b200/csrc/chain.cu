@@ -413,7 +413,6 @@ chain_kernel(const __grid_constant__ CUtensorMap map_b, const __grid_constant__ 
 
 #include "chain_x2.cuh"
 #include "chain19.cuh"
-#include "chain19g.cuh"
 
 namespace rk {
 
@@ -696,89 +695,8 @@ void launch19(rk_op* op, ChainParams cp) {
                 cp);
 }
 
-// variant G (chain19g.cuh): bands straight from global memory into registers
-template <int K0, int K1>
-void launch19g(rk_op* op, ChainParams cp) {
-  constexpr int TX = 32, TY = TY19;
-  using G = C19GGeom<TX, TY>;
-  static_assert(G::SMEM <= 232448, "19-point chain (G) tile exceeds 227 KB of shared memory");
-  using KernFn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap,
-                          const CUtensorMap, const CUtensorMap, ChainParams);
-  bool cuts = false;
-  for (int s = 0; s < 2; ++s) cuts = cuts || (cp.zb > 0 && cp.local[s]);
-  const int fl = (cuts ? 1 : 0) | (cp.pz ? 2 : 0) | (cp.ghost ? 4 : 0);
-  KernFn kern;
-  switch (fl) {
-    case 0: kern = chain19g_kernel<TX, TY, K0, K1, 0>; break;
-    case 1: kern = chain19g_kernel<TX, TY, K0, K1, 1>; break;
-    case 2: kern = chain19g_kernel<TX, TY, K0, K1, 2>; break;
-    case 3: kern = chain19g_kernel<TX, TY, K0, K1, 3>; break;
-    case 4: kern = chain19g_kernel<TX, TY, K0, K1, 4>; break;
-    default: kern = chain19g_kernel<TX, TY, K0, K1, 5>; break;
-  }
-  rk_ctx* ctx = op->ctx;
-  int occ = 0;
-  {
-    auto it = ctx->occ_cache.find((const void*)kern);
-    if (it == ctx->occ_cache.end()) {
-      RK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
-      RK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, G::NTHR, G::SMEM));
-      occ = std::max(1, occ);
-      ctx->occ_cache[(const void*)kern] = occ;
-    } else {
-      occ = it->second;
-    }
-  }
-  const int nzl = (int)op->g.nz_local;
-  dim3 grid((unsigned)(op->g.nx / TX), (unsigned)(op->g.ny / TY), 1);
-  const int chunks = pick_chunks((int)(grid.x * grid.y), ctx->sms * occ, nzl, G::H);
-  const int zc = (nzl + chunks - 1) / chunks;
-  cp.zc = zc;
-  grid.z = (unsigned)((nzl + zc - 1) / zc);
-  const cuuint64_t nx = op->g.nx, ny = op->g.ny, nz = op->g.nz_local;
-  CUtensorMap mbM, mbH, mxM, mxH, mgM, mgH;
-  {
-    cuuint64_t dims[4] = {nx, ny, nz, (cuuint64_t)G::NBAND};
-    cuuint64_t str[3] = {nx * 8, nx * ny * 8, (cuuint64_t)op->N * 8};
-    cuuint32_t boxM[4] = {(cuuint32_t)TX, (cuuint32_t)G::EY, 1, (cuuint32_t)G::NBAND};
-    cuuint32_t boxH[4] = {(cuuint32_t)G::HW, (cuuint32_t)G::EY, 1, (cuuint32_t)G::NBAND};
-    encode(&mbM, cp.bands, 4, dims, str, boxM);
-    encode(&mbH, cp.bands, 4, dims, str, boxH);
-    if (cp.ghost) {
-      cuuint64_t gd[4] = {nx, ny, 2 * BGHOST, (cuuint64_t)G::NBAND};
-      cuuint64_t gs[3] = {nx * 8, nx * ny * 8, (cuuint64_t)(2 * BGHOST) * nx * ny * 8};
-      encode(&mgM, op->gbands, 4, gd, gs, boxM);
-      encode(&mgH, op->gbands, 4, gd, gs, boxH);
-    } else {
-      mgM = mbM;
-      mgH = mbH;
-    }
-  }
-  {
-    cuuint64_t dims[3] = {nx, ny, nz + 2 * GHOST};
-    cuuint64_t str[2] = {nx * 8, nx * ny * 8};
-    cuuint32_t boxM[3] = {(cuuint32_t)TX, (cuuint32_t)G::XROWS, 1};
-    cuuint32_t boxH[3] = {(cuuint32_t)G::HW, (cuuint32_t)G::XROWS, 1};
-    encode(&mxM, cp.xin - GHOST * op->P, 3, dims, str, boxM);
-    encode(&mxH, cp.xin - GHOST * op->P, 3, dims, str, boxH);
-  }
-  const bool allow = ctx->pdl && (ctx->pdl_mode == 0 || ctx->pdl_mode == 3) && !ctx->pdl_skip_next;
-  ctx->pdl_skip_next = ctx->pdl_mode >= 2;
-  launch_pdl_if(ctx, allow, kern, grid, dim3(G::NTHR), G::SMEM, mbM, mbH, mxM, mxH, mgM, mgH, cp);
-}
-
-bool chain19g_on() {
-  const char* e = std::getenv("RK_CHAIN19");
-  return e && e[0] == 'g';
-}
-
 void chain19_dispatch(rk_op* op, int nst, const int* k, const ChainParams& cp) {
   constexpr int TX = 32, TY = TY19, PD = PD19;
-  if (nst == 2 && chain19g_on()) {
-    if (k[0] == CK_SPMV1 && k[1] == CK_SWEEP) return launch19g<CK_SPMV1, CK_SWEEP>(op, cp);
-    if (k[0] == CK_SWEEP && k[1] == CK_SWEEP) return launch19g<CK_SWEEP, CK_SWEEP>(op, cp);
-    if (k[0] == CK_SWEEP && k[1] == CK_SPMV) return launch19g<CK_SWEEP, CK_SPMV>(op, cp);
-  }
   if (nst == 2) {
     if (k[0] == CK_SPMV1 && k[1] == CK_SWEEP) return launch19<2, TX, TY, PD, CK_SPMV1, CK_SWEEP, 0>(op, cp);
     if (k[0] == CK_SWEEP && k[1] == CK_SWEEP) return launch19<2, TX, TY, PD, CK_SWEEP, CK_SWEEP, 0>(op, cp);
@@ -838,7 +756,6 @@ void chain_launch(rk_op* op, int nst, const int* kinds, const double* omegas, co
   cp.pz = op->wrapz;   // periodic z on one rank wraps in the kernel; on several, halos
   cp.ghost = op->ctx->nranks > 1 ? 1 : 0;
   cp.rz = op->ctx->nranks > 1 ? GHOST : 0;
-  cp.gbands = op->gbands;
   cp.xin = xin;
   cp.r = r;
   cp.out_t = out_t;

@@ -129,7 +129,6 @@ struct ChainParams {
   const double* gate;   // no-op when *gate != 0 (rBiCGStab lookahead)
   int ghost;            // several ranks: bands of planes outside [0, nz) from the ghost-band map
   int rz;               // z coordinate of plane 0 in the rhs tensor map (GHOST: padded rhs)
-  const double* gbands; // several ranks: op->gbands (chain19g reads it directly)
 };
 
 // Per-iteration device scalars of rBiCGStab (one 64-byte record per iteration).

@@ -208,10 +208,9 @@ def test_chain_bitwise_equals_unfused(rk, ctx, shape, periodic, cfg, monkeypatch
 
 # 19-point chain (chain19.cuh): 2 stages per launch, x staged as three TMA
 # regions so that a periodic x axis wraps; nx % 32 == 0, ny % 8 == 0, nz >= 16.
-@pytest.mark.parametrize("variant", ["smem", "g"])   # RK_CHAIN19=g: bands straight to registers
 @pytest.mark.parametrize("shape,periodic", [((64, 16, 40), 5), ((32, 24, 17), 1), ((96, 16, 33), 4),
                                             ((64, 32, 20), 0), ((32, 8, 16), 1)])
-def test_chain19_bitwise_equals_unfused(rk, ctx, shape, periodic, variant, monkeypatch):
+def test_chain19_bitwise_equals_unfused(rk, ctx, shape, periodic, monkeypatch):
     """The 19-point fused chain against the one-stage-per-launch stencil path
     on random 19-band operators: M^-1 r (the 5 sweeps after the first run
     as launches of 2, 2 and 1 stages) and block-Jacobi local sweeps agree bit
@@ -228,14 +227,11 @@ def test_chain19_bitwise_equals_unfused(rk, ctx, shape, periodic, variant, monke
     monkeypatch.delenv("RK_NO_CHAIN")
     rh = np.random.default_rng(4).uniform(-1, 1, nx * ny * nz)
     r = dev(rh)
-    if variant == "g":
-        monkeypatch.setenv("RK_CHAIN19", "g")   # read per launch
     a, b = fused.precond(r), plain.precond(r)
     assert torch.equal(a, b)
     zb = 4 if nz % 4 == 0 else 1
     if zb > 1:
         assert torch.equal(fused.precond(r, zblocks=zb), plain.precond(r, zblocks=zb))
-    monkeypatch.delenv("RK_CHAIN19", raising=False)
     ref = Operator(nx, ny, nz, periodic, OFFSETS19, hb)
     zr = Jacobi(ref)(rh)
     assert np.max(np.abs(a.cpu().numpy() - zr)) <= 1e-12 * np.max(np.abs(zr))
@@ -243,8 +239,7 @@ def test_chain19_bitwise_equals_unfused(rk, ctx, shape, periodic, variant, monke
     plain.close()
 
 
-@pytest.mark.parametrize("variant", ["smem", "g"])
-def test_chain19_solver_paths_bitwise(rk, ctx, variant, monkeypatch):
+def test_chain19_solver_paths_bitwise(rk, ctx, monkeypatch):
     """Every solver use of the 19-point chain -- rGCROT's A_hat v (stages
     [SPMV1, SWEEP] [SWEEP, SWEEP] [SWEEP, SWEEP]), rBiCGStab's p_hat / v
     ([SWEEP, SWEEP] x 2, [SWEEP, SPMV]), the refresh and the cycle-end M^-1
@@ -253,11 +248,8 @@ def test_chain19_solver_paths_bitwise(rk, ctx, variant, monkeypatch):
     RK_FORCE_CHAIN."""
     w = get_workload("c2m")
     monkeypatch.setenv("RK_FORCE_CHAIN", "1")
-    if variant == "g":
-        monkeypatch.setenv("RK_CHAIN19", "g")
     g1, sp1 = gpu_sequence(rk, ctx, w)
     monkeypatch.delenv("RK_FORCE_CHAIN")
-    monkeypatch.delenv("RK_CHAIN19", raising=False)
     g2, sp2 = gpu_sequence(rk, ctx, w)
     for (r1, x1), (r2, x2) in zip(g1, g2):
         assert r1["krylov_matvecs"] == r2["krylov_matvecs"] and r1["outcome"] == r2["outcome"]
