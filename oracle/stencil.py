@@ -132,6 +132,30 @@ def to_dense(op, cap=8192):
     return Ad
 
 
+def to_sparse(op):
+    """A as a scipy CSR matrix, assembled band by band with to_dense's
+    per-cell rule (wrap on periodic axes, drop out-of-grid neighbours),
+    vectorised: the direct-solve reference for grids too large for
+    to_dense (sparse LU up to 32^3)."""
+    import scipy.sparse as sp
+    k, j, i = np.meshgrid(np.arange(op.nz), np.arange(op.ny), np.arange(op.nx), indexing="ij")
+    rows, cols, vals = [], [], []
+    n = (i + op.nx * (j + op.ny * k)).ravel()
+    for d, (dx, dy, dz) in enumerate(op.offsets):
+        ii, jj, kk = i + dx, j + dy, k + dz
+        ok = np.ones(ii.shape, dtype=bool)
+        for v, nn, bit in ((ii, op.nx, 1), (jj, op.ny, 2), (kk, op.nz, 4)):
+            if not (op.periodic & bit):
+                ok &= (v >= 0) & (v < nn)
+        m = ok.ravel()
+        col = ((ii % op.nx) + op.nx * ((jj % op.ny) + op.ny * (kk % op.nz))).ravel()
+        rows.append(n[m])
+        cols.append(col[m])
+        vals.append(op.bands[d].ravel()[m])
+    return sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                         shape=(op.N, op.N))
+
+
 def local_operator(op, zblocks):
     """A_loc: A with every coupling between different z-blocks removed.  The
     z axis is cut into `zblocks` equal slabs (planes [b nz/P, (b+1) nz/P),

@@ -809,6 +809,8 @@ void chain_run(rk_op* op, const std::vector<int>& kinds, const std::vector<doubl
   const int g = (n + nmax - 1) / nmax;
   const double* cur = xin;
   int a = 0;
+  int rhs_depth = 0;   // ghost planes of rhs already exchanged in this call (it does not change
+                       // after the launch that produces it)
   for (int i = 0; i < g; ++i) {
     const int len = n / g + (i < n % g ? 1 : 0);
     const bool last = (i == g - 1);
@@ -817,7 +819,10 @@ void chain_run(rk_op* op, const std::vector<int>& kinds, const std::vector<doubl
     // right-hand side len - 1 planes beyond the slab (stage 0 recomputes the
     // halo planes the later stages need)
     halo(op, cur, len);
-    if (kinds[a] != CK_SPMV1 && rhs && len > 1) halo(op, rhs, len - 1);
+    if (kinds[a] != CK_SPMV1 && rhs && len - 1 > rhs_depth) {
+      halo(op, rhs, len - 1);
+      rhs_depth = len - 1;
+    }
     chain_launch(op, len, kinds.data() + a, om.data() + a, cur, rhs,
                  (kinds[a] == CK_SPMV1) ? out_t : nullptr, last ? out_mid : nullptr, dst,
                  loc.data() + a, zbs);

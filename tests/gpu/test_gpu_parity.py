@@ -369,31 +369,9 @@ def solution_tolerance(op, b, xo):
         xs = np.linalg.solve(to_dense(op), b)
     else:   # up to 32^3: sparse LU ("sparse LU on <= 32^3")
         import scipy.sparse.linalg as spla
-        xs = spla.splu(sparse_of(op).tocsc()).solve(b)
+        from oracle.stencil import to_sparse
+        xs = spla.splu(to_sparse(op).tocsc()).solve(b)
     return max(1e-6 * np.linalg.norm(xo), 10.0 * np.linalg.norm(xo - xs))
-
-
-def sparse_of(op):
-    """A as a scipy CSR matrix, assembled band by band (wrap on periodic
-    axes, drop out-of-grid neighbours) -- the per-cell rule of to_dense,
-    vectorised."""
-    import scipy.sparse as sp
-    k, j, i = np.meshgrid(np.arange(op.nz), np.arange(op.ny), np.arange(op.nx), indexing="ij")
-    rows, cols, vals = [], [], []
-    n = (i + op.nx * (j + op.ny * k)).ravel()
-    for d, (dx, dy, dz) in enumerate(op.offsets):
-        ii, jj, kk = i + dx, j + dy, k + dz
-        ok = np.ones(ii.shape, dtype=bool)
-        for v, nn, bit in ((ii, op.nx, 1), (jj, op.ny, 2), (kk, op.nz, 4)):
-            if not (op.periodic & bit):
-                ok &= (v >= 0) & (v < nn)
-        m = ok.ravel()
-        col = ((ii % op.nx) + op.nx * ((jj % op.ny) + op.ny * (kk % op.nz))).ravel()
-        rows.append(n[m])
-        cols.append(col[m])
-        vals.append(op.bands[d].ravel()[m])
-    return sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
-                         shape=(op.N, op.N))
 
 
 def compare_sequences(w, gpu, ora, method):

@@ -351,3 +351,13 @@ def test_ssor_matches_block_triangular_formula(mk):
     out[perm] = z
     ref = ssor(op, r, sweeps=3, omega=w)
     assert np.allclose(ref, out, rtol=0, atol=1e-12 * np.abs(out).max())
+
+
+@pytest.mark.parametrize("mk", [lambda: channel19(8), lambda: porous7(10, 2),
+                                lambda: convection_diffusion_c1(6)])
+def test_to_sparse_equals_dense_expansion(mk):
+    """oracle.stencil.to_sparse (the sparse-LU reference of reading R12) is
+    the per-cell dense expansion to_dense, entry for entry."""
+    from oracle.stencil import to_sparse
+    op = Operator.from_problem(mk())
+    assert np.array_equal(to_sparse(op).toarray(), to_dense(op))
