@@ -115,7 +115,7 @@ __device__ __forceinline__ double apply19c(const double (&a)[20], const double (
 
 // FL bit 0: block-Jacobi cuts, bit 1: periodic z (one rank), bit 2: ghost bands (ranks > 1)
 template <int TY, int K0, int K1, int K2, int FL>
-__global__ void __maxnreg__(144)   // 14 warps x 144 registers fill the register file
+__global__ void __launch_bounds__(C19CGeom<TY>::NTHR, 1)   // 14 warps: <= 128 registers (4 warps per SM sub-partition)
 chain19c_kernel(const __grid_constant__ CUtensorMap b0M, const __grid_constant__ CUtensorMap b0H,
                 const __grid_constant__ CUtensorMap r0M, const __grid_constant__ CUtensorMap r0H,
                 const __grid_constant__ CUtensorMap xM, const __grid_constant__ CUtensorMap xH,
