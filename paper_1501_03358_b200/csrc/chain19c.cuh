@@ -6,8 +6,9 @@
 //   * the PRODUCER (cluster rank 0) runs stage 0 over the tile + 2-cell halo
 //     (TMA-fed input ring, bands / rhs of plane tau) and stores its outputs
 //     (and t = A x when stage 0 is CK_SPMV1) straight into the CONSUMER's
-//     shared memory (DSMEM st.shared::cluster), one 4-plane ring, signalling
-//     each plane with a release-arrive on the consumer's "full" mbarrier;
+//     shared memory (DSMEM st.shared::cluster), one 4-plane ring; after the
+//     step's barrier one thread publishes the plane (cluster-scope fence,
+//     release-arrive on the consumer's "full" mbarrier);
 //   * the CONSUMER (rank 1) runs stages 1 (tile + 1-cell halo) and 2 (tile)
 //     with its own TMA-fed bands / rhs, as chain19.cuh's stages 0 and 1, and
 //     hands each ring plane back with a release-arrive on the producer's
@@ -145,9 +146,7 @@ chain19c_kernel(const __grid_constant__ CUtensorMap b0M, const __grid_constant__
 
   if (tid == 0) {
     for (int s = 0; s < G::NBAR; ++s) {
-      // full barriers count every producer thread's arrive; the rest one arrive (or TMA)
-      const bool full = s >= G::BAR_CF;
-      mbar_init(&bars[s], full ? (uint32_t)(32 * G::NW0) : 1u);
+      mbar_init(&bars[s], 1u);   // one arrive per phase: a TMA batch or one signalling thread
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -307,9 +306,12 @@ chain19c_kernel(const __grid_constant__ CUtensorMap b0M, const __grid_constant__
       st_cluster_f64(ring0r + 8u * RS_ * RP, v0);                                                 \
       if (K0 == CK_SPMV1) st_cluster_f64(ringtr + 8u * RS_ * RP, y);                              \
     }                                                                                             \
-    mbar_arrive_remote(fullr + 8u * RS_);                                                         \
     __syncthreads();                                                                              \
     if (tid == 0) {                                                                               \
+      /* every thread's DSMEM stores precede the barrier; one cluster-scope   */                  \
+      /* fence + release-arrive publishes them (one fence per plane, not 448) */                  \
+      asm volatile("fence.acq_rel.cluster;" ::: "memory");                                        \
+      mbar_arrive_remote(fullr + 8u * RS_);                                                       \
       if (tau + G::NXB - 1 <= qlast) issue_x(tau + G::NXB - 1, XM_);                              \
       if (tau + G::NB0 <= tau_end - 1) issue_b(tau + G::NB0, BS_);                                \
     }                                                                                             \
