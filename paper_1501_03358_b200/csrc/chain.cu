@@ -413,7 +413,6 @@ chain_kernel(const __grid_constant__ CUtensorMap map_b, const __grid_constant__ 
 
 #include "chain_x2.cuh"
 #include "chain19.cuh"
-#include "chain19c.cuh"
 
 namespace rk {
 
@@ -697,118 +696,8 @@ void launch19(rk_op* op, ChainParams cp) {
                 cp);
 }
 
-// three stages on a CTA pair (chain19c.cuh)
-template <int K0, int K1, int K2>
-void launch19c(rk_op* op, ChainParams cp) {
-  constexpr int TY = 8;
-  using G = C19CGeom<TY>;
-  constexpr int TX = G::TX;
-  static_assert(G::SMEM <= 232448, "19-point pair chain exceeds 227 KB of shared memory");
-  using KernFn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap,
-                          const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap,
-                          const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap,
-                          const CUtensorMap, const CUtensorMap, ChainParams);
-  bool cuts = false;
-  for (int s = 0; s < 3; ++s) cuts = cuts || (cp.zb > 0 && cp.local[s]);
-  const int fl = (cuts ? 1 : 0) | (cp.pz ? 2 : 0) | (cp.ghost ? 4 : 0);
-  KernFn kern;
-  switch (fl) {
-    case 0: kern = chain19c_kernel<TY, K0, K1, K2, 0>; break;
-    case 1: kern = chain19c_kernel<TY, K0, K1, K2, 1>; break;
-    case 2: kern = chain19c_kernel<TY, K0, K1, K2, 2>; break;
-    case 3: kern = chain19c_kernel<TY, K0, K1, K2, 3>; break;
-    case 4: kern = chain19c_kernel<TY, K0, K1, K2, 4>; break;
-    default: kern = chain19c_kernel<TY, K0, K1, K2, 5>; break;
-  }
-  rk_ctx* ctx = op->ctx;
-  const int nzl = (int)op->g.nz_local;
-  dim3 grid((unsigned)(2 * (op->g.nx / TX)), (unsigned)(op->g.ny / TY), 1);
-  cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed =
-      (ctx->pdl && (ctx->pdl_mode == 0 || ctx->pdl_mode == 3) && !ctx->pdl_skip_next) ? 1 : 0;
-  ctx->pdl_skip_next = ctx->pdl_mode >= 2;
-  cfg.blockDim = dim3(G::NTHR);
-  cfg.dynamicSmemBytes = G::SMEM;
-  cfg.stream = ctx->stream;
-  cfg.attrs = attr;
-  cfg.numAttrs = 2;
-  int clusters = 0;
-  {
-    auto it = ctx->occ_cache.find((const void*)kern);
-    if (it == ctx->occ_cache.end()) {
-      RK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
-      cfg.gridDim = grid;
-      cfg.numAttrs = 1;
-      RK_CUDA(cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg));
-      cfg.numAttrs = 2;
-      clusters = std::max(1, clusters);
-      ctx->occ_cache[(const void*)kern] = clusters;
-    } else {
-      clusters = it->second;
-    }
-  }
-  const int tiles = (int)(op->g.nx / TX) * (int)(op->g.ny / TY);
-  const int chunks = pick_chunks(tiles, clusters, nzl, 2);
-  const int zc = (nzl + chunks - 1) / chunks;
-  cp.zc = zc;
-  grid.z = (unsigned)((nzl + zc - 1) / zc);
-  cfg.gridDim = grid;
-  const cuuint64_t nx = op->g.nx, ny = op->g.ny, nz = op->g.nz_local;
-  CUtensorMap b0M, b0H, r0M, r0H, xM, xH, g0M, g0H, b1M, b1H, r1M, r1H, g1M, g1H;
-  auto bands = [&](CUtensorMap* mM, CUtensorMap* mH, CUtensorMap* gM, CUtensorMap* gH, int rows, int hw) {
-    cuuint64_t dims[4] = {nx, ny, nz, (cuuint64_t)G::NBAND};
-    cuuint64_t str[3] = {nx * 8, nx * ny * 8, (cuuint64_t)op->N * 8};
-    cuuint32_t boxM[4] = {(cuuint32_t)TX, (cuuint32_t)rows, 1, (cuuint32_t)G::NBAND};
-    cuuint32_t boxH[4] = {(cuuint32_t)hw, (cuuint32_t)rows, 1, (cuuint32_t)G::NBAND};
-    encode(mM, cp.bands, 4, dims, str, boxM);
-    encode(mH, cp.bands, 4, dims, str, boxH);
-    if (cp.ghost) {
-      cuuint64_t gd[4] = {nx, ny, 2 * BGHOST, (cuuint64_t)G::NBAND};
-      cuuint64_t gs[3] = {nx * 8, nx * ny * 8, (cuuint64_t)(2 * BGHOST) * nx * ny * 8};
-      encode(gM, op->gbands, 4, gd, gs, boxM);
-      encode(gH, op->gbands, 4, gd, gs, boxH);
-    } else {
-      *gM = *mM;
-      *gH = *mH;
-    }
-  };
-  bands(&b0M, &b0H, &g0M, &g0H, G::EY0, G::HW0);
-  bands(&b1M, &b1H, &g1M, &g1H, G::EY1, G::HW1);
-  encode_rhs(op, cp, &r0M, (cuuint32_t)TX, (cuuint32_t)G::EY0);
-  encode_rhs(op, cp, &r0H, (cuuint32_t)G::HW0, (cuuint32_t)G::EY0);
-  encode_rhs(op, cp, &r1M, (cuuint32_t)TX, (cuuint32_t)G::EY1);
-  encode_rhs(op, cp, &r1H, (cuuint32_t)G::HW1, (cuuint32_t)G::EY1);
-  {
-    cuuint64_t dims[3] = {nx, ny, nz + 2 * GHOST};
-    cuuint64_t str[2] = {nx * 8, nx * ny * 8};
-    cuuint32_t boxM[3] = {(cuuint32_t)TX, (cuuint32_t)G::XROWS, 1};
-    cuuint32_t boxH[3] = {(cuuint32_t)G::HW0, (cuuint32_t)G::XROWS, 1};
-    encode(&xM, cp.xin - GHOST * op->P, 3, dims, str, boxM);
-    encode(&xH, cp.xin - GHOST * op->P, 3, dims, str, boxH);
-  }
-  RK_CUDA(cudaLaunchKernelEx(&cfg, kern, b0M, b0H, r0M, r0H, xM, xH, g0M, g0H, b1M, b1H, r1M, r1H, g1M,
-                             g1H, cp));
-}
-
-// RK_CHAIN19=3 (read at rk_op_create): three 19-point stages per launch on CTA pairs
-bool chain19_pairs(const rk_op* op) { return op->chain19_pairs; }
-
 void chain19_dispatch(rk_op* op, int nst, const int* k, const ChainParams& cp) {
   constexpr int TX = 32, TY = TY19, PD = PD19;
-  if (nst == 3) {
-    if (k[0] == CK_SPMV1 && k[1] == CK_SWEEP && k[2] == CK_SWEEP)
-      return launch19c<CK_SPMV1, CK_SWEEP, CK_SWEEP>(op, cp);
-    if (k[0] == CK_SWEEP && k[1] == CK_SWEEP && k[2] == CK_SWEEP)
-      return launch19c<CK_SWEEP, CK_SWEEP, CK_SWEEP>(op, cp);
-    if (k[0] == CK_SWEEP && k[1] == CK_SWEEP && k[2] == CK_SPMV)
-      return launch19c<CK_SWEEP, CK_SWEEP, CK_SPMV>(op, cp);
-  }
   if (nst == 2) {
     if (k[0] == CK_SPMV1 && k[1] == CK_SWEEP) return launch19<2, TX, TY, PD, CK_SPMV1, CK_SWEEP, 0>(op, cp);
     if (k[0] == CK_SWEEP && k[1] == CK_SWEEP) return launch19<2, TX, TY, PD, CK_SWEEP, CK_SWEEP, 0>(op, cp);
@@ -834,7 +723,7 @@ int chain_max_stages(const rk_op* op) {
     if (op->g.nx % 32 != 0 || op->g.ny % TY19 != 0 || op->g.nz_local < 16) return 0;
     if (!op->force_chain && (double)(op->S + 3) * 8.0 * (double)op->N <= (double)op->ctx->l2_bytes)
       return 0;
-    return chain19_pairs(op) ? 3 : NST19;
+    return NST19;
   }
   if (op->S != 7) return 0;
   if (op->g.periodic_mask & 3) return 0;                    // TMA boxes do not wrap in x/y

@@ -1128,7 +1128,6 @@ rk_status rk_op_create(rk_ctx* ctx, const rk_grid* g, int nbands, const int8_t* 
       op->user_offsets.assign(offsets, offsets + 3 * nbands);
       op->no_chain = std::getenv("RK_NO_CHAIN") != nullptr;
       op->force_chain = std::getenv("RK_FORCE_CHAIN") != nullptr;
-      if (const char* e = std::getenv("RK_CHAIN19")) op->chain19_pairs = e[0] == '3';
     } catch (...) {
       cudaFree(op->bands);
       cudaFree(op->gbands);

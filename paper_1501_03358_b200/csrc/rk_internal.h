@@ -212,7 +212,6 @@ struct rk_op {
   std::vector<int8_t> user_offsets;   // caller's band order (for rk_op_update_bands)
   bool no_chain = false;              // env RK_NO_CHAIN: disable the fused TMA chain
   bool force_chain = false;           // env RK_FORCE_CHAIN: use it below the L2 threshold (tests)
-  bool chain19_pairs = false;         // 19-point chains of 3 stages on CTA pairs (chain19c.cuh)
 };
 
 namespace rk {

@@ -105,12 +105,9 @@ PROBLEMS = {
     ("c4_full", 2, False), ("c3_full", 4, False),      # full size: the chains by the L2 rule
     ("c3s", 2, False), ("c3s", 3, False), ("c2s", 2, False), ("c2s", 3, False),
     ("rand7_64x32x48", 2, True), ("rand7_64x32x48", 3, True), ("rand7_64x32x48_pz", 2, True),
-    ("rand19_64x16x40_pxz", 2, True), ("rand19_32x24x48", 3, True), ("rand19_32x24x48", 2, "pairs"),
-    ("c4_full", 2, "pairs")])
+    ("rand19_64x16x40_pxz", 2, True), ("rand19_32x24x48", 3, True)])
 def test_slab_operator_and_preconditioner_bitwise(rk, wname, R, force, monkeypatch):
     prob = PROBLEMS[wname]()
-    if force == "pairs":
-        monkeypatch.setenv("RK_CHAIN19", "3")      # 19-point chains of 3 stages on CTA pairs
     if force:
         monkeypatch.setenv("RK_FORCE_CHAIN", "1")     # read at rk_op_create
     x = np.random.default_rng(5).uniform(-1, 1, prob.N)
@@ -138,7 +135,6 @@ def test_slab_operator_and_preconditioner_bitwise(rk, wname, R, force, monkeypat
 
     res = run_ranks(R, rank)
     monkeypatch.delenv("RK_FORCE_CHAIN", raising=False)
-    monkeypatch.delenv("RK_CHAIN19", raising=False)
     assert np.array_equal(np.concatenate([r[0] for r in res]), y1)
     assert np.array_equal(np.concatenate([r[1] for r in res]), z1)
     if zb1 is not None:

@@ -208,10 +208,9 @@ def test_chain_bitwise_equals_unfused(rk, ctx, shape, periodic, cfg, monkeypatch
 
 # 19-point chain (chain19.cuh): 2 stages per launch, x staged as three TMA
 # regions so that a periodic x axis wraps; nx % 32 == 0, ny % 8 == 0, nz >= 16.
-@pytest.mark.parametrize("pairs", [False, True], ids=["cta", "pair"])   # RK_CHAIN19=3: chain19c.cuh
 @pytest.mark.parametrize("shape,periodic", [((64, 16, 40), 5), ((32, 24, 17), 1), ((96, 16, 33), 4),
                                             ((64, 32, 20), 0), ((32, 8, 16), 1)])
-def test_chain19_bitwise_equals_unfused(rk, ctx, shape, periodic, pairs, monkeypatch):
+def test_chain19_bitwise_equals_unfused(rk, ctx, shape, periodic, monkeypatch):
     """The 19-point fused chain against the one-stage-per-launch stencil path
     on random 19-band operators: M^-1 r (the 5 sweeps after the first run
     as launches of 2, 2 and 1 stages) and block-Jacobi local sweeps agree bit
@@ -221,11 +220,8 @@ def test_chain19_bitwise_equals_unfused(rk, ctx, shape, periodic, pairs, monkeyp
     bands = dev(hb)
     mk = lambda: rk.GridOperator(ctx, nx, ny, nz, OFFSETS19, bands, periodic)
     monkeypatch.setenv("RK_FORCE_CHAIN", "1")
-    if pairs:
-        monkeypatch.setenv("RK_CHAIN19", "3")
     fused = mk()
     monkeypatch.delenv("RK_FORCE_CHAIN")
-    monkeypatch.delenv("RK_CHAIN19", raising=False)
     monkeypatch.setenv("RK_NO_CHAIN", "1")
     plain = mk()
     monkeypatch.delenv("RK_NO_CHAIN")
@@ -243,8 +239,7 @@ def test_chain19_bitwise_equals_unfused(rk, ctx, shape, periodic, pairs, monkeyp
     plain.close()
 
 
-@pytest.mark.parametrize("pairs", [False, True], ids=["cta", "pair"])
-def test_chain19_solver_paths_bitwise(rk, ctx, pairs, monkeypatch):
+def test_chain19_solver_paths_bitwise(rk, ctx, monkeypatch):
     """Every solver use of the 19-point chain -- rGCROT's A_hat v (stages
     [SPMV1, SWEEP] [SWEEP, SWEEP] [SWEEP, SWEEP]), rBiCGStab's p_hat / v
     ([SWEEP, SWEEP] x 2, [SWEEP, SPMV]), the refresh and the cycle-end M^-1
@@ -253,11 +248,8 @@ def test_chain19_solver_paths_bitwise(rk, ctx, pairs, monkeypatch):
     RK_FORCE_CHAIN."""
     w = get_workload("c2m")
     monkeypatch.setenv("RK_FORCE_CHAIN", "1")
-    if pairs:
-        monkeypatch.setenv("RK_CHAIN19", "3")
     g1, sp1 = gpu_sequence(rk, ctx, w)
     monkeypatch.delenv("RK_FORCE_CHAIN")
-    monkeypatch.delenv("RK_CHAIN19", raising=False)
     g2, sp2 = gpu_sequence(rk, ctx, w)
     for (r1, x1), (r2, x2) in zip(g1, g2):
         assert r1["krylov_matvecs"] == r2["krylov_matvecs"] and r1["outcome"] == r2["outcome"]
