@@ -52,6 +52,9 @@
 #ifndef RK_CHAIN_TMA_INVD
 #define RK_CHAIN_TMA_INVD 1
 #endif
+#ifndef RK_C19_INVD
+#define RK_C19_INVD 0   // 19-point chain: 1/D recomputed (0) or streamed as a 20th band (1)
+#endif
 #ifndef RK_CHAIN_COMPUTEONLY
 #define RK_CHAIN_COMPUTEONLY 0  // experiments: 1 = no TMA after the prologue (stale data)
 #endif
@@ -664,14 +667,14 @@ void launch19(rk_op* op, ChainParams cp) {
   const cuuint64_t nx = op->g.nx, ny = op->g.ny, nz = op->g.nz_local;
   CUtensorMap mbM, mbH, mrM, mrH, mxM, mxH, mgM, mgH;
   {
-    cuuint64_t dims[4] = {nx, ny, nz, (cuuint64_t)G::NBAND};
+    cuuint64_t dims[4] = {nx, ny, nz, (cuuint64_t)G::NBT};
     cuuint64_t str[3] = {nx * 8, nx * ny * 8, (cuuint64_t)op->N * 8};
-    cuuint32_t boxM[4] = {(cuuint32_t)TX, (cuuint32_t)G::EY, 1, (cuuint32_t)G::NBAND};
-    cuuint32_t boxH[4] = {(cuuint32_t)G::HW, (cuuint32_t)G::EY, 1, (cuuint32_t)G::NBAND};
+    cuuint32_t boxM[4] = {(cuuint32_t)TX, (cuuint32_t)G::EY, 1, (cuuint32_t)G::NBT};
+    cuuint32_t boxH[4] = {(cuuint32_t)G::HW, (cuuint32_t)G::EY, 1, (cuuint32_t)G::NBT};
     encode(&mbM, cp.bands, 4, dims, str, boxM);
     encode(&mbH, cp.bands, 4, dims, str, boxH);
     if (cp.ghost) {   // the neighbours' band planes (op->gbands)
-      cuuint64_t gd[4] = {nx, ny, 2 * BGHOST, (cuuint64_t)G::NBAND};
+      cuuint64_t gd[4] = {nx, ny, 2 * BGHOST, (cuuint64_t)G::NBT};
       cuuint64_t gs[3] = {nx * 8, nx * ny * 8, (cuuint64_t)(2 * BGHOST) * nx * ny * 8};
       encode(&mgM, op->gbands, 4, gd, gs, boxM);
       encode(&mgH, op->gbands, 4, gd, gs, boxH);

@@ -33,7 +33,11 @@ namespace rk {
 
 template <int NST, int TX, int TY, int PD>
 struct C19Geom {
-  static constexpr int ST = 19, NBAND = 20;           // bands + 1/D
+  static constexpr int ST = 19, NBAND = 20;           // register set: bands + 1/D
+  // arrays streamed per plane: the 19 bands (+ the 1/D band unless
+  // RK_C19_INVD = 0, where 1/D = 1.0 / D is recomputed at stage 0 -- the
+  // same correctly rounded value invdiag_kernel stores)
+  static constexpr int NBT = RK_C19_INVD ? 20 : 19;
   static constexpr int H = NST - 1;                    // recomputed halo of stage 0
   static constexpr int EY = TY + 2 * H;                // stage-0 rows
   static constexpr int EX = TX + 2 * H;                // stage-0 columns (ring pitch)
@@ -48,7 +52,7 @@ struct C19Geom {
   static constexpr int NXB = 8;                        // input-tile ring (planes tau-1 .. tau+6)
   __host__ __device__ static constexpr int al(int b) { return (b + 127) / 128 * 128; }
   // band slot: regions L, M, R, each [NBAND][EY][w]
-  static constexpr int BL_BYTES = NBAND * EY * HW * 8, BM_BYTES = NBAND * EY * TX * 8;
+  static constexpr int BL_BYTES = NBT * EY * HW * 8, BM_BYTES = NBT * EY * TX * 8;
   static constexpr int B_BYTES = 2 * BL_BYTES + BM_BYTES;
   static constexpr int RL_BYTES = EY * HW * 8, RM_BYTES = EY * TX * 8;
   static constexpr int R_BYTES = 2 * RL_BYTES + RM_BYTES;
@@ -256,10 +260,11 @@ chain19_kernel(const __grid_constant__ CUtensorMap mbM, const __grid_constant__ 
       /* stage 0 at plane tau: bands / rhs to registers, input neighbours from the tiles */      \
       const double* bsl = bbase + bs0 * BSD + boff;                                               \
       if (mwarp) {                                                                                \
-        _Pragma("unroll") for (int d = 0; d < NBAND; ++d) bnd[PH][d] = bsl[d * (EY * TX)];       \
+        _Pragma("unroll") for (int d = 0; d < G::NBT; ++d) bnd[PH][d] = bsl[d * (EY * TX)];      \
       } else {                                                                                    \
-        _Pragma("unroll") for (int d = 0; d < NBAND; ++d) bnd[PH][d] = bsl[d * bstr];            \
+        _Pragma("unroll") for (int d = 0; d < G::NBT; ++d) bnd[PH][d] = bsl[d * bstr];           \
       }                                                                                           \
+      if (!RK_C19_INVD) bnd[PH][19] = bnd[PH][0] != 0.0 ? 1.0 / bnd[PH][0] : 0.0;                 \
       if (LOAD_R) rr[PH] = rbase[bs0 * RSD + roff];                                               \
       const double* tm = xbase + XM * XS;                                                         \
       const double* t0 = xbase + X0 * XS;                                                         \
