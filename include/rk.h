@@ -233,6 +233,111 @@ rk_status rk_trace(rk_solver* s, int what, double* out, int64_t cap, int64_t* le
 /* Workspace audit: number of N_local-length vectors allocated. */
 rk_status rk_solver_workspace(rk_solver* s, int64_t* nvec);
 
+/* ---------------------------------------------------------------------
+ * Per-kernel entry points (operations "exported for
+ * per-kernel parity", as rk_op_apply / rk_precond_apply are).  Each runs one
+ * family of the solvers' block or rBiCGStab kernels -- through the same
+ * host launch path, size thresholds and kernel variants the solvers use --
+ * on the context stream, and synchronises before returning.
+ *   Q: HOST array of ncol DEVICE pointers, each to n fp64 values (one
+ *      column of [C V_j], U or C); 1 <= ncol <= 80 (RK_EINVAL otherwise).
+ *   Every other vector or coefficient pointer is DEVICE, fp64.
+ *   Single-rank contexts only (RK_EUNSUPPORTED otherwise): the multi-rank
+ *   all-reduces of the same kernels are exercised through rk_solve.
+ *   Ownership: nothing is retained after the call.
+ * --------------------------------------------------------------------- */
+/* Block dot (kernel K3; Alg. 3 lines 6a and 6b-9 "[C V_j]^T w", Alg. 4
+ * lines 7a / 12a "C^T v"): out_w[c] = Q_c^T w;
+ * with v != NULL also out_v[c] = Q_c^T v in the same read of Q (the
+ * two-right-hand-side form of DESIGN.md reading R19). */
+rk_status rk_block_dot(rk_ctx* ctx, int ncol, const double* const* Q, const double* w,
+                       const double* v, int64_t n, double* out_w, double* out_v);
+/* Block update (kernel K4; Alg. 3 lines 6c / 9, Alg. 4 line 7a):
+ * w <- w - sum_c Q_c g[c]; then red[q] = w_new^T dots[q] for q < ndots
+ * (ndots <= 3; dots: HOST array of DEVICE pointers, a NULL entry means
+ * w_new itself; red may be NULL iff ndots == 0). */
+rk_status rk_block_update(rk_ctx* ctx, int ncol, const double* const* Q, const double* g,
+                          double* w, int64_t n, int ndots, const double* const* dots,
+                          double* red);
+/* Recycle projection (K3 + K4; Alg. 3 lines 1b, 6a-6c, Alg. 4 lines 1c,
+ * 7a, 12a): eta = Q^T w; w <- w - Q eta; nrm2 (nullable) =
+ * ||w_new||^2.  The update kernel sums the block dot's per-CTA partials
+ * itself (deferred finalisation). ncol <= 40. */
+rk_status rk_block_project(rk_ctx* ctx, int ncol, const double* const* Q, double* w, int64_t n,
+                           double* eta, double* nrm2);
+/* Gram-corrected CGS2 update (reading R19, replacing Alg. 3
+ * lines 6a-9): h = 2 g - G g with G the Gram matrix of Q = [C, v_0 ..]
+ * whose leading k x k block (C^T C) is taken as I and whose other entries
+ * are G[i][l] = G[l][i] = grow[i * 80 + l] for rows i >= k, l <= i (row
+ * stride 80); then w <- w - Q h, h_out[c] = h[c], nrm2 = ||w_new||^2.
+ * 0 <= k <= ncol; n even and every pointer 16-byte aligned. */
+rk_status rk_gram_update(rk_ctx* ctx, int ncol, int k, const double* const* Q, const double* g,
+                         const double* grow, double* h_out, double* w, int64_t n, double* nrm2);
+/* Arnoldi normalisation (Alg. 3 line 10, reading D18): h = sqrt(nrm2[0]);
+ * if nin2 != NULL and !(h > 1e-14 sqrt(nin2[0])) (happy breakdown) then
+ * w <- 0 and flag[0] = 1, else w <- w / h and flag[0] = 0 (flag nullable). */
+rk_status rk_normalize(rk_ctx* ctx, double* w, int64_t n, const double* nrm2, const double* nin2,
+                       double* flag);
+/* Linear combinations (kernel K5; Alg. 3 lines 13-13a (eq. (6)) and the
+ * line-14a extension): for o < nout (<= 5): out[o] = scale[o] *
+ * sum_c Q_c coef[o * ncol + c], plus the old out[o] when acc[o] != 0.
+ * out: HOST array of nout DEVICE pointers; scale, acc: HOST arrays. */
+rk_status rk_lincomb(rk_ctx* ctx, int ncol, const double* const* Q, const double* coef, int nout,
+                     double* const* out, const double* scale, const int* acc, int64_t n);
+/* Recycle-space rotation (kernel K8; line 1a U <- U R^-1, C <- C~ R^-1 and
+ * the line-14a truncation): in place [q_0 .. q_{k-1}] <- [q_0 .. q_{k-1}] T
+ * (T: DEVICE k x k column-major); only the first kout (1 <= kout <= k)
+ * columns are written.  Q: HOST array of k (1 <= k <= 48) DEVICE pointers. */
+rk_status rk_rotate(rk_ctx* ctx, int k, double* const* Q, const double* T, int kout, int64_t n);
+
+/* rBiCGStab per-iteration device scalars (one record per iteration). */
+typedef struct {
+  double rho;    /* r~^T r_i                                              */
+  double rr;     /* ||r_i||^2                                             */
+  double sigma;  /* r~^T v_i (v projected, line 7a)                       */
+  double ss;     /* ||s_i||^2                                             */
+  double ts;     /* t_i^T s_i (t projected, line 12a)                     */
+  double tt;     /* ||t_i||^2                                             */
+  double flag;   /* 0 normal, 1 exact exit (s = 0), 2 breakdown           */
+  double stop;   /* 1: iteration not run (set by its rk_bicg_p)           */
+} rk_bicg_iter;
+/* Alg. 4 line 6 fused with the first Jacobi sweep of p_hat = M^-1 p
+ * (right preconditioning, reading D2): first != 0: p = r;
+ * else, unless the stop test below holds, p = r + beta (p - omega v) with
+ * alpha = prev->rho / prev->sigma, omega = prev->ts / prev->tt,
+ * beta = (cur->rho / prev->rho)(alpha / omega).  z = omega_l p / D
+ * (jacobi != 0; D the operator's diagonal band) or z = p.  Stop test (the
+ * lookahead decision): prev->flag != 0, prev->sigma == 0,
+ * !(sqrt(cur->rr) > thr_conv), cur->rho == 0 or !(sqrt(cur->rr) <= thr_div);
+ * cur->stop receives it (p, z untouched when it holds).  cur, prev: DEVICE
+ * records (prev ignored when first != 0). */
+rk_status rk_bicg_p(rk_op* op, int first, const double* r, double* p, const double* v, double* z,
+                    double omega_l, int jacobi, rk_bicg_iter* cur, const rk_bicg_iter* prev,
+                    double thr_conv, double thr_div);
+/* Alg. 4 line 8 fused with the first sweep of s_hat = M^-1 s: alpha =
+ * cur->rho / cur->sigma; s = r - alpha v; z = omega_l s / D (or s);
+ * cur->ss = ||s||^2. */
+rk_status rk_bicg_s(rk_op* op, const double* r, const double* v, double* s, double* z,
+                    double omega_l, int jacobi, rk_bicg_iter* cur);
+/* Alg. 4 lines 7a + 8 fused (reading R20): eta = C^T v, sigma = r~^T v -
+ * ctr^T eta (ctr = C^T r~), v <- v - C eta, alpha = cur->rho / sigma, then
+ * s = r - alpha v, z = omega_l s / D (or s), cur->sigma = sigma,
+ * cur->ss = ||s||^2.  C: HOST array of k (1 <= k <= 39) DEVICE pointers;
+ * n even and every pointer 16-byte aligned (RK_EUNSUPPORTED otherwise). */
+rk_status rk_bicg_project_s(rk_op* op, int k, const double* const* C, double* v, const double* rt,
+                            const double* ctr, double* eta, const double* r, double* s, double* z,
+                            double omega_l, int jacobi, rk_bicg_iter* cur);
+/* Alg. 4 lines 13-15 (+ 10-10a exact exit, breakdown guards of reading
+ * D17): alpha = rho / sigma, omega = ts / tt from *cur; mode 2 (no update)
+ * if sigma == 0, or tt == 0 or omega == 0 with ss != 0; mode 1 (exact
+ * exit) if ss == 0: x += alpha p_hat, r = s; mode 0: x += alpha p_hat +
+ * omega s_hat, r = s - omega t.  xi[c] += alpha eta1[c] (+ omega eta2[c])
+ * for c < k; cur->flag = mode; next->rho = r~^T r, next->rr = ||r||^2. */
+rk_status rk_bicg_xr(rk_op* op, double* x, double* r, const double* s, const double* t,
+                     const double* p_hat, const double* s_hat, const double* rt,
+                     rk_bicg_iter* cur, rk_bicg_iter* next, double* xi, const double* eta1,
+                     const double* eta2, int k);
+
 /* Instrumentation.  Every kernel launch increments a per-context counter.
  * With profiling on, launches of the kernel classes whose names contain
  * `filter` (NULL = all) are bracketed by CUDA events on the context stream;

@@ -90,6 +90,18 @@ def lib():
         "rk_profile_enable": ([vp, i32, C.c_char_p], i32),
         "rk_profile_every": ([vp, i32], i32),
         "rk_profile_read": ([vp, i32, vp, vp, vp, vp, P(i32)], i32),
+        # per-kernel entry points (pointer arrays are passed as c_void_p)
+        "rk_block_dot": ([vp, i32, vp, vp, vp, i64, vp, vp], i32),
+        "rk_block_update": ([vp, i32, vp, vp, vp, i64, i32, vp, vp], i32),
+        "rk_block_project": ([vp, i32, vp, vp, i64, vp, vp], i32),
+        "rk_gram_update": ([vp, i32, i32, vp, vp, vp, vp, vp, i64, vp], i32),
+        "rk_normalize": ([vp, vp, i64, vp, vp, vp], i32),
+        "rk_lincomb": ([vp, i32, vp, vp, i32, vp, vp, vp, i64], i32),
+        "rk_rotate": ([vp, i32, vp, vp, i32, i64], i32),
+        "rk_bicg_p": ([vp, i32, vp, vp, vp, vp, dbl, i32, vp, vp, dbl, dbl], i32),
+        "rk_bicg_s": ([vp, vp, vp, vp, vp, dbl, i32, vp], i32),
+        "rk_bicg_project_s": ([vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, dbl, i32, vp], i32),
+        "rk_bicg_xr": ([vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i32], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -112,4 +124,7 @@ EXPORTED = ["rk_last_error", "rk_version", "rk_nccl_unique_id", "rk_ctx_create",
             "rk_solver_set_method", "rk_recycle_set", "rk_recycle_dim", "rk_recycle_export",
             "rk_solve", "rk_solve_host", "rk_solve_host_ex", "rk_stage_rhs", "rk_solve_staged",
             "rk_host_sync", "rk_history", "rk_trace", "rk_solver_workspace", "rk_launch_count",
-            "rk_profile_enable", "rk_profile_every", "rk_profile_read"]
+            "rk_profile_enable", "rk_profile_every", "rk_profile_read",
+            "rk_block_dot", "rk_block_update", "rk_block_project", "rk_gram_update",
+            "rk_normalize", "rk_lincomb", "rk_rotate", "rk_bicg_p", "rk_bicg_s",
+            "rk_bicg_project_s", "rk_bicg_xr"]

@@ -12,6 +12,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
+#include <cstddef>
 #include <cstring>
 #include <limits>
 #include <numeric>
@@ -1596,6 +1597,183 @@ rk_status rk_profile_read(rk_ctx* ctx, int cap, char* names, int64_t* launches, 
     }
     *n = i;
     if (cap < 0) ctx->agg.clear();  // cap < 0: reset
+  });
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------- per-kernel entry points
+// (include/rk.h "Per-kernel entry points"): one kernel family each, through
+// the solvers' own host launch functions, on one rank, synchronised.
+namespace {
+static_assert(sizeof(rk_bicg_iter) == sizeof(rk::BiIter) &&
+                  offsetof(rk_bicg_iter, stop) == offsetof(rk::BiIter, stop) &&
+                  offsetof(rk_bicg_iter, ts) == offsetof(rk::BiIter, ts),
+              "rk_bicg_iter must mirror rk::BiIter");
+
+void kernel_entry(rk_ctx* ctx) {
+  RK_REQUIRE(ctx, RK_EINVAL, "NULL ctx");
+  RK_REQUIRE(ctx->nranks == 1, RK_EUNSUPPORTED, "per-kernel entry points need a one-rank context");
+  RK_CUDA(cudaSetDevice(ctx->device));
+  ctx->gate = nullptr;
+}
+
+std::vector<const double*> col_list(int ncol, const double* const* Q, int maxcol) {
+  RK_REQUIRE(Q && ncol >= 1 && ncol <= maxcol, RK_EINVAL, "need 1 <= ncol <= " + std::to_string(maxcol));
+  std::vector<const double*> v(Q, Q + ncol);
+  for (auto p : v) RK_REQUIRE(p, RK_EINVAL, "NULL column pointer");
+  return v;
+}
+
+void kernel_done(rk_ctx* ctx) { RK_CUDA(cudaStreamSynchronize(ctx->stream)); }
+}  // namespace
+
+extern "C" {
+
+rk_status rk_block_dot(rk_ctx* ctx, int ncol, const double* const* Q, const double* w,
+                       const double* v, int64_t n, double* out_w, double* out_v) {
+  return guarded([&] {
+    kernel_entry(ctx);
+    auto cols = col_list(ncol, Q, MAXCOL);
+    RK_REQUIRE(w && out_w && n >= 1 && (!v || out_v), RK_EINVAL, "NULL argument or n < 1");
+    if (v) bdot2(ctx, cols, w, v, n, out_w, out_v);
+    else bdot(ctx, cols, w, n, out_w);
+    kernel_done(ctx);
+  });
+}
+
+rk_status rk_block_update(rk_ctx* ctx, int ncol, const double* const* Q, const double* g,
+                          double* w, int64_t n, int ndots, const double* const* dots,
+                          double* red) {
+  return guarded([&] {
+    kernel_entry(ctx);
+    auto cols = col_list(ncol, Q, MAXCOL);
+    RK_REQUIRE(g && w && n >= 1, RK_EINVAL, "NULL argument or n < 1");
+    RK_REQUIRE(ndots >= 0 && ndots <= 3 && (ndots == 0 || (dots && red)), RK_EINVAL,
+               "0 <= ndots <= 3, dots and red given when ndots > 0");
+    std::vector<const double*> d(dots, dots + ndots);
+    bupd(ctx, cols, g, 1.0, w, n, d, ndots ? red : nullptr);
+    kernel_done(ctx);
+  });
+}
+
+rk_status rk_block_project(rk_ctx* ctx, int ncol, const double* const* Q, double* w, int64_t n,
+                           double* eta, double* nrm2) {
+  return guarded([&] {
+    kernel_entry(ctx);
+    auto cols = col_list(ncol, Q, 40);
+    RK_REQUIRE(w && eta && n >= 1, RK_EINVAL, "NULL argument or n < 1");
+    if (nrm2) bproject(ctx, cols, w, n, eta, {nullptr}, nrm2);
+    else bproject(ctx, cols, w, n, eta, {}, nullptr);
+    kernel_done(ctx);
+  });
+}
+
+rk_status rk_gram_update(rk_ctx* ctx, int ncol, int k, const double* const* Q, const double* g,
+                         const double* grow, double* h_out, double* w, int64_t n, double* nrm2) {
+  return guarded([&] {
+    kernel_entry(ctx);
+    auto cols = col_list(ncol, Q, MAXCOL);
+    RK_REQUIRE(k >= 0 && k <= ncol, RK_EINVAL, "need 0 <= k <= ncol");
+    RK_REQUIRE(g && grow && h_out && w && nrm2 && n >= 1, RK_EINVAL, "NULL argument or n < 1");
+    bupd_gram(ctx, cols, k, g, grow, h_out, w, n, nrm2);
+    kernel_done(ctx);
+  });
+}
+
+rk_status rk_normalize(rk_ctx* ctx, double* w, int64_t n, const double* nrm2, const double* nin2,
+                       double* flag) {
+  return guarded([&] {
+    kernel_entry(ctx);
+    RK_REQUIRE(w && nrm2 && n >= 1, RK_EINVAL, "NULL argument or n < 1");
+    normalize(ctx, w, n, nrm2, nin2, flag);
+    kernel_done(ctx);
+  });
+}
+
+rk_status rk_lincomb(rk_ctx* ctx, int ncol, const double* const* Q, const double* coef, int nout,
+                     double* const* out, const double* scale, const int* acc, int64_t n) {
+  return guarded([&] {
+    kernel_entry(ctx);
+    auto cols = col_list(ncol, Q, MAXCOL);
+    RK_REQUIRE(coef && out && scale && acc && n >= 1, RK_EINVAL, "NULL argument or n < 1");
+    RK_REQUIRE(nout >= 1 && nout <= MAXOUT, RK_EINVAL, "need 1 <= nout <= 5");
+    LcOut lo;
+    memset(&lo, 0, sizeof(lo));
+    for (int o = 0; o < nout; ++o) {
+      RK_REQUIRE(out[o], RK_EINVAL, "NULL output pointer");
+      lo.out[o] = out[o];
+      lo.scale[o] = scale[o];
+      lo.acc[o] = acc[o] != 0;
+    }
+    lincomb(ctx, cols, coef, nout, lo, n);
+    kernel_done(ctx);
+  });
+}
+
+rk_status rk_rotate(rk_ctx* ctx, int k, double* const* Q, const double* T, int kout, int64_t n) {
+  return guarded([&] {
+    kernel_entry(ctx);
+    RK_REQUIRE(Q && T && n >= 1 && k >= 1 && k <= MAXCOL, RK_EINVAL, "NULL argument, n < 1 or bad k");
+    std::vector<double*> cols(Q, Q + k);
+    for (auto p : cols) RK_REQUIRE(p, RK_EINVAL, "NULL column pointer");
+    rotate(ctx, cols, T, n, kout);
+    kernel_done(ctx);
+  });
+}
+
+rk_status rk_bicg_p(rk_op* op, int first, const double* r, double* p, const double* v, double* z,
+                    double omega_l, int jacobi, rk_bicg_iter* cur, const rk_bicg_iter* prev,
+                    double thr_conv, double thr_div) {
+  return guarded([&] {
+    RK_REQUIRE(op, RK_EINVAL, "NULL op");
+    kernel_entry(op->ctx);
+    RK_REQUIRE(r && p && z && cur && (first || (v && prev)), RK_EINVAL, "NULL argument");
+    bicg_p(op, r, p, v, z, omega_l, jacobi != 0, reinterpret_cast<BiIter*>(cur),
+           reinterpret_cast<const BiIter*>(prev), first ? 1 : 0, thr_conv, thr_div);
+    kernel_done(op->ctx);
+  });
+}
+
+rk_status rk_bicg_s(rk_op* op, const double* r, const double* v, double* s, double* z,
+                    double omega_l, int jacobi, rk_bicg_iter* cur) {
+  return guarded([&] {
+    RK_REQUIRE(op, RK_EINVAL, "NULL op");
+    kernel_entry(op->ctx);
+    RK_REQUIRE(r && v && s && z && cur, RK_EINVAL, "NULL argument");
+    bicg_s(op, r, v, s, z, omega_l, jacobi != 0, reinterpret_cast<BiIter*>(cur));
+    kernel_done(op->ctx);
+  });
+}
+
+rk_status rk_bicg_project_s(rk_op* op, int k, const double* const* C, double* v, const double* rt,
+                            const double* ctr, double* eta, const double* r, double* s, double* z,
+                            double omega_l, int jacobi, rk_bicg_iter* cur) {
+  return guarded([&] {
+    RK_REQUIRE(op, RK_EINVAL, "NULL op");
+    kernel_entry(op->ctx);
+    auto cols = col_list(k, C, 39);
+    RK_REQUIRE(v && rt && ctr && eta && r && s && z && cur, RK_EINVAL, "NULL argument");
+    const bool ok = bicg_proj_s(op, cols, v, rt, ctr, eta, r, s, z, omega_l, jacobi != 0,
+                                reinterpret_cast<BiIter*>(cur), nullptr);
+    RK_REQUIRE(ok, RK_EUNSUPPORTED,
+               "fused projection needs even n, 16-byte aligned pointers and deferred coefficients");
+    kernel_done(op->ctx);
+  });
+}
+
+rk_status rk_bicg_xr(rk_op* op, double* x, double* r, const double* s, const double* t,
+                     const double* p_hat, const double* s_hat, const double* rt,
+                     rk_bicg_iter* cur, rk_bicg_iter* next, double* xi, const double* eta1,
+                     const double* eta2, int k) {
+  return guarded([&] {
+    RK_REQUIRE(op, RK_EINVAL, "NULL op");
+    kernel_entry(op->ctx);
+    RK_REQUIRE(x && r && s && t && p_hat && s_hat && rt && cur && next, RK_EINVAL, "NULL argument");
+    RK_REQUIRE(k >= 0 && (k == 0 || (xi && eta1 && eta2)), RK_EINVAL, "xi, eta1, eta2 needed for k > 0");
+    bicg_xr(op->ctx, x, r, s, t, p_hat, s_hat, rt, op->N, reinterpret_cast<BiIter*>(cur),
+            reinterpret_cast<BiIter*>(next), xi, eta1, eta2, k);
+    kernel_done(op->ctx);
   });
 }
 

@@ -1,0 +1,395 @@
+"""Per-kernel GPU parity (BASELINE north_star: "GPU results must match the
+oracle per kernel to 1e-12 relative in fp64"): each block / rBiCGStab
+kernel family of the solvers, called through librk's per-kernel C-ABI
+entry points (include/rk.h), against oracle/kernels.py on the same seeded
+inputs.
+
+Tolerance (R25 for reductions): a computed inner product may
+differ from the extended-precision one by 1e-12 of the sum of the absolute
+products, componentwise: |g_gpu - g_ref|_c <= 1e-12 (|Q|^T |w|)_c; an
+updated vector by 1e-12 of the absolute terms it sums:
+|w_gpu - w_ref|_i <= 1e-12 (|w| + sum_c |g_c| |Q_c|)_i.
+
+Sizes span the kernel variants the solvers pick: odd n (one element per
+thread, VEC = 1), an even n below the bulk threshold (register-tiled
+kernels, 1024-row tiles plus a ragged tail), and n above 2048 x #SMs
+(bulk-copy block dots, 2048-row ring items, ragged tail); column counts
+from 1 to 80 (one launch, balanced multi-launch, padded column groups).
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import kernels as K
+from oracle.stencil import Operator
+from problems.stencils import porous7
+
+pytestmark = pytest.mark.gpu
+
+SIZES = [4099, 65538, 2048 * 148 + 2048 * 3 + 6]
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def rk():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_1501_03358_b200 as rk
+    rk.lib()
+    return rk
+
+
+@pytest.fixture(scope="module")
+def kern(rk):
+    from paper_1501_03358_b200 import kernels
+    return kernels
+
+
+@pytest.fixture(scope="module")
+def ctx(rk):
+    c = rk.Context(0)
+    yield c
+    c.close()
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
+def host(t):
+    return t.detach().cpu().numpy().astype(np.float64)
+
+
+def cols(n, ncol, seed):
+    rng = np.random.default_rng(seed)
+    Qh = [rng.uniform(-1, 1, n) for _ in range(ncol)]
+    return Qh, [dev(q) for q in Qh]
+
+
+def check_dots(got, ref, Qh, w):
+    scale = np.array([np.abs(q) @ np.abs(w) for q in Qh])
+    err = np.abs(np.asarray(got) - np.asarray(ref))
+    assert np.all(err <= TOL * scale), float(np.max(err / scale))
+
+
+def check_vec(got, ref, absterms):
+    err = np.abs(got - ref)
+    assert np.all(err <= TOL * absterms + 1e-300), float(np.max(err / (absterms + 1e-300)))
+
+
+def abs_update_terms(Qh, g, w):
+    s = np.abs(w).copy()
+    for c, q in enumerate(Qh):
+        s += abs(g[c]) * np.abs(q)
+    return s
+
+
+# ------------------------------------------------------------ K3 block dot
+@pytest.mark.parametrize("n", SIZES)
+@pytest.mark.parametrize("ncol", [1, 7, 24, 33, 72, 80])
+@pytest.mark.parametrize("two", [False, True])
+def test_block_dot(kern, ctx, n, ncol, two):
+    Qh, Q = cols(n, ncol, 100 + ncol)
+    rng = np.random.default_rng(n + ncol)
+    w = rng.uniform(-1, 1, n)
+    v = rng.uniform(-1, 1, n) if two else None
+    gw, gv = kern.block_dot(ctx, Q, dev(w), dev(v) if two else None)
+    check_dots(host(gw), K.block_dot(Qh, w), Qh, w)
+    if two:
+        check_dots(host(gv), K.block_dot(Qh, v), Qh, v)
+
+
+@pytest.mark.parametrize("bulk", ["0", "2"])
+def test_block_dot_forced_variants(rk, kern, bulk, monkeypatch):
+    """RK_BDOT_BULK=0 (register-tiled only) and =2 (bulk copies always)
+    at a size where the default would pick the other one."""
+    monkeypatch.setenv("RK_BDOT_BULK", bulk)
+    c = rk.Context(0)
+    try:
+        n = SIZES[2] if bulk == "0" else SIZES[1]
+        Qh, Q = cols(n, 20, 7)
+        w = np.random.default_rng(8).uniform(-1, 1, n)
+        v = np.random.default_rng(9).uniform(-1, 1, n)
+        gw, gv = kern.block_dot(c, Q, dev(w), dev(v))
+        check_dots(host(gw), K.block_dot(Qh, w), Qh, w)
+        check_dots(host(gv), K.block_dot(Qh, v), Qh, v)
+    finally:
+        c.close()
+
+
+def test_block_dot_misaligned(kern, ctx):
+    """A vector starting 8 bytes past a 16-byte boundary takes the
+    one-element-per-thread kernel (same values)."""
+    n = 70000
+    Qh, Q = cols(n, 9, 3)
+    w = np.random.default_rng(4).uniform(-1, 1, n)
+    buf = torch.zeros(n + 1, dtype=torch.float64, device="cuda")
+    buf[1:] = dev(w)
+    gw, _ = kern.block_dot(ctx, Q, buf[1:])
+    check_dots(host(gw), K.block_dot(Qh, w), Qh, w)
+
+
+# ------------------------------------------------------------ K4 block update
+@pytest.mark.parametrize("n", SIZES)
+@pytest.mark.parametrize("ncol", [1, 9, 40, 80])
+@pytest.mark.parametrize("nd", [0, 1, 3])
+def test_block_update(kern, ctx, n, ncol, nd):
+    Qh, Q = cols(n, ncol, 200 + ncol)
+    rng = np.random.default_rng(300 + n % 97 + nd)
+    w = rng.uniform(-1, 1, n)
+    g = rng.uniform(-1, 1, ncol)
+    dvh = [None, rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)][:nd]
+    wd = dev(w)
+    red = kern.block_update(ctx, Q, dev(g), wd, [None if d is None else dev(d) for d in dvh])
+    ref, rdots = K.block_update(Qh, g, w, dvh)
+    got = host(wd)
+    check_vec(got, ref, abs_update_terms(Qh, g, w))
+    for q, d in enumerate(dvh):
+        dd = ref if d is None else d
+        assert abs(host(red)[q] - rdots[q]) <= TOL * float(np.abs(ref) @ np.abs(dd))
+
+
+@pytest.mark.parametrize("n", SIZES)
+@pytest.mark.parametrize("ncol", [1, 5, 20, 40])
+def test_block_project(kern, ctx, n, ncol):
+    """eta = Q^T w, w <- w - Q eta (deferred finalisation on one rank)."""
+    rng = np.random.default_rng(400 + ncol)
+    Cq, _ = np.linalg.qr(rng.uniform(-1, 1, (n, ncol)))
+    Qh = [Cq[:, c].copy() for c in range(ncol)]
+    Q = [dev(q) for q in Qh]
+    w = rng.uniform(-1, 1, n)
+    wd = dev(w)
+    eta, nrm2 = kern.block_project(ctx, Q, wd)
+    reta, rw, rnn = K.block_project(Qh, w)
+    check_dots(host(eta), reta, Qh, w)
+    # w_new is computed from the GPU's eta: compare against the update with
+    # the same coefficients, and eta's own error bound propagated
+    ref, _ = K.block_update(Qh, host(eta), w)
+    check_vec(host(wd), ref, abs_update_terms(Qh, host(eta), w))
+    assert np.max(np.abs(host(wd) - rw)) <= TOL * np.linalg.norm(w)
+    assert abs(host(nrm2)[0] - rnn) <= TOL * rnn
+
+
+# ---------------------------------------------- R19 Gram-corrected update
+@pytest.mark.parametrize("n", SIZES[1:])
+@pytest.mark.parametrize("ncol,k", [(8, 0), (21, 20), (31, 30), (70, 30), (80, 40)])
+def test_gram_update(kern, ctx, n, ncol, k):
+    rng = np.random.default_rng(500 + ncol)
+    Cq, _ = np.linalg.qr(rng.uniform(-1, 1, (n, ncol)))
+    Qh = [Cq[:, c].copy() for c in range(ncol)]
+    Q = [dev(q) for q in Qh]
+    w = rng.uniform(-1, 1, n)
+    g = np.array(K.block_dot(Qh, w))
+    grow = np.zeros((80, 80))
+    for i in range(k, ncol):
+        for l in range(i + 1):
+            grow[i, l] = float(Qh[i] @ Qh[l]) + rng.uniform(-1e-10, 1e-10)   # lagged, not exact
+    wd = dev(w)
+    h, nrm2 = kern.gram_update(ctx, Q, k, dev(g), dev(grow.reshape(-1)), wd)
+    rh, rw, rnn = K.gram_update(Qh, k, g, grow, w)
+    G = K.gram_matrix(ncol, k, grow)
+    hscale = 2 * np.abs(g) + np.abs(G) @ np.abs(g)
+    assert np.all(np.abs(host(h) - rh) <= TOL * hscale)
+    check_vec(host(wd), rw, abs_update_terms(Qh, rh, w))
+    assert abs(host(nrm2)[0] - rnn) <= TOL * rnn
+
+
+# ------------------------------------------------------------ normalise, K5, K8
+@pytest.mark.parametrize("n", SIZES)
+def test_normalize(kern, ctx, n):
+    w = np.random.default_rng(600).uniform(-1, 1, n)
+    nn = float(w @ w)
+    wd = dev(w)
+    flag = kern.normalize(ctx, wd, dev([nn]), dev([1.0]))
+    ref, f = K.normalize(w, nn, 1.0)
+    assert host(flag)[0] == f == 0.0
+    assert np.max(np.abs(host(wd) - ref)) <= TOL * np.max(np.abs(ref))
+    wd = dev(1e-20 * w)
+    flag = kern.normalize(ctx, wd, dev([1e-40 * nn]), dev([1.0]))
+    assert host(flag)[0] == 1.0 and not host(wd).any()
+
+
+@pytest.mark.parametrize("n", SIZES)
+@pytest.mark.parametrize("ncol,nout", [(1, 1), (12, 3), (45, 5), (80, 2)])
+def test_lincomb(kern, ctx, n, ncol, nout):
+    Qh, Q = cols(n, ncol, 700 + ncol)
+    rng = np.random.default_rng(701 + nout)
+    coef = rng.uniform(-1, 1, (nout, ncol))
+    olds = [rng.uniform(-1, 1, n) for _ in range(nout)]
+    scale = list(rng.uniform(-2, 2, nout))
+    acc = [o % 2 == 1 for o in range(nout)]
+    outs = [dev(o) for o in olds]
+    kern.lincomb(ctx, Q, dev(coef), outs, scale, acc)
+    refs = K.lincomb(Qh, coef, olds, scale, acc)
+    for o in range(nout):
+        terms = abs(scale[o]) * sum(abs(coef[o][c]) * np.abs(Qh[c]) for c in range(ncol))
+        if acc[o]:
+            terms = terms + np.abs(olds[o])
+        check_vec(host(outs[o]), refs[o], terms)
+
+
+@pytest.mark.parametrize("n", SIZES)
+@pytest.mark.parametrize("k,kout", [(1, 1), (10, 10), (30, 20), (48, 30)])
+def test_rotate(kern, ctx, n, k, kout):
+    Qh, Q = cols(n, k, 800 + k)
+    T = np.random.default_rng(801).uniform(-1, 1, (k, k))
+    kern.rotate(ctx, Q, dev(T), kout)
+    refs = K.rotate(Qh, T, kout)
+    for c in range(kout):
+        terms = sum(abs(T[l][c]) * np.abs(Qh[l]) for l in range(k))
+        check_vec(host(Q[c]), refs[c], terms)
+    for c in range(kout, k):
+        assert np.array_equal(host(Q[c]), Qh[c])     # columns past kout untouched
+
+
+def test_entry_point_argument_errors(rk, kern, ctx):
+    """Bad sizes are RK_EINVAL, not faults: 81 columns, a rotation past 48."""
+    Qh, Q = cols(1000, 81, 1)
+    w = dev(np.ones(1000))
+    with pytest.raises(rk.RkError, match="RK_EINVAL"):
+        kern.block_dot(ctx, Q, w)
+    with pytest.raises(rk.RkError, match="RK_EINVAL"):
+        kern.rotate(ctx, Q[:49], dev(np.eye(49)))
+
+
+# ------------------------------------------------------------ K6 rBiCGStab
+@pytest.fixture(scope="module")
+def bop(rk, ctx):
+    """porous 40^3 operator (N = 64000: 62 whole 1024-row tiles + a ragged tail)."""
+    prob = porous7(40, 4)
+    op = rk.GridOperator(ctx, prob.nx, prob.ny, prob.nz, prob.offsets, dev(prob.bands()), prob.periodic)
+    ora = Operator.from_problem(prob)
+    yield op, 1.0 / ora.diag()
+    op.close()
+
+
+def rec(**kw):
+    vals = [kw.get(f, 0.0) for f in ("rho", "rr", "sigma", "ss", "ts", "tt", "flag", "stop")]
+    return dev(vals)
+
+
+def recd(t):
+    return dict(zip(("rho", "rr", "sigma", "ss", "ts", "tt", "flag", "stop"), host(t)))
+
+
+@pytest.mark.parametrize("first", [True, False])
+@pytest.mark.parametrize("jacobi", [True, False])
+def test_bicg_p(kern, bop, first, jacobi):
+    op, invD = bop
+    n = op.N
+    rng = np.random.default_rng(900)
+    r, p, v = (rng.uniform(-1, 1, n) for _ in range(3))
+    cur = dict(rho=0.7, rr=float(r @ r))
+    prev = dict(rho=1.3, sigma=0.9, ts=0.4, tt=1.1, flag=0.0)
+    pd, zd = dev(p), torch.zeros(n, dtype=torch.float64, device="cuda")
+    cd = rec(**cur)
+    kern.bicg_p(op, first, dev(r), pd, dev(v), zd, 0.8, jacobi, cd, rec(**prev), 1e-30, 1e30)
+    stop, rp, rz = K.bicg_p(first, r, p, v, invD if jacobi else None, 0.8, cur, prev, 1e-30, 1e30)
+    assert recd(cd)["stop"] == 0.0 and not stop
+    beta = 0.0 if first else (0.7 / 1.3) * ((1.3 / 0.9) / (0.4 / 1.1))
+    pterms = np.abs(r) + abs(beta) * (np.abs(p) + (0.4 / 1.1) * np.abs(v))
+    check_vec(host(pd), rp, pterms)
+    check_vec(host(zd), rz, pterms * (0.8 * np.abs(invD) if jacobi else 1.0))
+
+
+@pytest.mark.parametrize("why", ["converged", "rho0", "flag", "sigma0", "diverged"])
+def test_bicg_p_stop_decision(kern, bop, why):
+    """The lookahead's stop test: p and z untouched, cur->stop = 1."""
+    op, invD = bop
+    n = op.N
+    rng = np.random.default_rng(901)
+    r, p, v = (rng.uniform(-1, 1, n) for _ in range(3))
+    cur = dict(rho=0.7, rr=float(r @ r))
+    prev = dict(rho=1.3, sigma=0.9, ts=0.4, tt=1.1, flag=0.0)
+    thr_conv, thr_div = 1e-30, 1e30
+    if why == "converged":
+        thr_conv = 2 * np.sqrt(cur["rr"])
+    elif why == "rho0":
+        cur["rho"] = 0.0
+    elif why == "flag":
+        prev["flag"] = 1.0
+    elif why == "sigma0":
+        prev["sigma"] = 0.0
+    else:
+        thr_div = 0.5 * np.sqrt(cur["rr"])
+    pd, zd = dev(p), dev(np.full(n, 7.0))
+    cd = rec(**cur)
+    kern.bicg_p(op, False, dev(r), pd, dev(v), zd, 0.8, True, cd, rec(**prev), thr_conv, thr_div)
+    stop, _, _ = K.bicg_p(False, r, p, v, invD, 0.8, cur, prev, thr_conv, thr_div)
+    assert stop and recd(cd)["stop"] == 1.0
+    assert np.array_equal(host(pd), p) and np.all(host(zd) == 7.0)
+
+
+@pytest.mark.parametrize("jacobi", [True, False])
+def test_bicg_s(kern, bop, jacobi):
+    op, invD = bop
+    n = op.N
+    rng = np.random.default_rng(902)
+    r, v = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+    cd = rec(rho=0.6, sigma=1.7)
+    sd, zd = (torch.zeros(n, dtype=torch.float64, device="cuda") for _ in range(2))
+    kern.bicg_s(op, dev(r), dev(v), sd, zd, 0.8, jacobi, cd)
+    rs, rz, rss = K.bicg_s(r, v, invD if jacobi else None, 0.8, 0.6, 1.7)
+    terms = np.abs(r) + (0.6 / 1.7) * np.abs(v)
+    check_vec(host(sd), rs, terms)
+    check_vec(host(zd), rz, terms * (0.8 * np.abs(invD) if jacobi else 1.0))
+    assert abs(recd(cd)["ss"] - rss) <= TOL * rss
+
+
+@pytest.mark.parametrize("k", [1, 10, 20, 39])
+def test_bicg_project_s(kern, bop, k):
+    """Lines 7a + 8 fused (R20): eta, projected v, sigma, s, z, ||s||^2."""
+    op, invD = bop
+    n = op.N
+    rng = np.random.default_rng(903 + k)
+    Cq, _ = np.linalg.qr(rng.uniform(-1, 1, (n, k)))
+    Ch = [Cq[:, c].copy() for c in range(k)]
+    Cd = [dev(c) for c in Ch]
+    v, rt, r = (rng.uniform(-1, 1, n) for _ in range(3))
+    ctr = np.array(K.block_dot(Ch, rt))
+    vd = dev(v)
+    sd, zd = (torch.zeros(n, dtype=torch.float64, device="cuda") for _ in range(2))
+    cd = rec(rho=0.45)
+    eta = kern.bicg_project_s(op, Cd, vd, dev(rt), dev(ctr), dev(r), sd, zd, 0.8, True, cd)
+    reta, rv, rsig, rs, rz, rss = K.bicg_project_s(Ch, v, rt, r, invD, 0.8, 0.45)
+    check_dots(host(eta), reta, Ch, v)
+    check_vec(host(vd), rv, abs_update_terms(Ch, reta, v))
+    got = recd(cd)
+    # sigma = r~^T v - ctr^T eta: bounded by the absolute terms of both forms
+    sig_terms = float(np.abs(rt) @ np.abs(v) + np.abs(ctr) @ np.abs(reta))
+    assert abs(got["sigma"] - rsig) <= TOL * sig_terms
+    alpha = 0.45 / rsig
+    terms = np.abs(r) + abs(alpha) * abs_update_terms(Ch, reta, v)
+    check_vec(host(sd), rs, terms)
+    check_vec(host(zd), rz, terms * 0.8 * np.abs(invD))
+    assert abs(got["ss"] - rss) <= 1e-11 * float(np.abs(rs) @ terms)
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("k", [0, 5])
+def test_bicg_xr(kern, bop, mode, k):
+    op, _ = bop
+    n = op.N
+    rng = np.random.default_rng(904 + mode)
+    x, r, s, t, ph, sh, rt = (rng.uniform(-1, 1, n) for _ in range(7))
+    cur = dict(rho=0.3, sigma=0.5, ss=1.0, ts=0.2, tt=0.4)
+    if mode == 1:
+        cur["ss"] = 0.0
+    elif mode == 2:
+        cur["tt"] = 0.0
+    xi, e1, e2 = (rng.uniform(-1, 1, k) for _ in range(3))
+    xd, rd = dev(x), dev(r)
+    cd, nd = rec(**cur), rec()
+    xid = dev(xi) if k else None
+    kern.bicg_xr(op, xd, rd, dev(s), dev(t), dev(ph), dev(sh), dev(rt), cd, nd, xid,
+                 dev(e1) if k else None, dev(e2) if k else None)
+    m, rx, rr_, rxi, rho_n, rr_n = K.bicg_xr(x, r, s, t, ph, sh, rt, cur, xi if k else None,
+                                            e1 if k else None, e2 if k else None)
+    assert m == mode and recd(cd)["flag"] == float(mode)
+    xterms = np.abs(x) + 0.6 * np.abs(ph) + 0.5 * np.abs(sh)
+    check_vec(host(xd), rx, xterms)
+    check_vec(host(rd), rr_, np.abs(s) + 0.5 * np.abs(t) + np.abs(r))
+    if k:
+        check_vec(host(xid), rxi, np.abs(xi) + 0.6 * np.abs(e1) + 0.5 * np.abs(e2))
+    got = recd(nd)
+    assert abs(got["rho"] - rho_n) <= TOL * float(np.abs(rt) @ np.abs(rr_))
+    assert abs(got["rr"] - rr_n) <= TOL * rr_n
