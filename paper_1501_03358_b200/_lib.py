@@ -5,7 +5,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIBPATH = os.path.join(HERE, "librk.so")
+# RK_LIBPATH: an A/B variant built by scripts/build_variant.py (measurement only)
+LIBPATH = os.environ.get("RK_LIBPATH") or os.path.join(HERE, "librk.so")
 
 RK_OK, RK_EINVAL, RK_ECUDA, RK_ENCCL, RK_ENOMEM, RK_ESTATE, RK_EUNSUPPORTED = range(7)
 STATUS_NAMES = ["RK_OK", "RK_EINVAL", "RK_ECUDA", "RK_ENCCL", "RK_ENOMEM", "RK_ESTATE",

@@ -439,6 +439,130 @@ __global__ void __launch_bounds__(256) bupd_gram_kernel(ColPtrs Q, int ncol, int
   block_reduce_store<1>(acc, 1, ra);
 }
 
+// Bulk-copy-fed form of bupd_gram_kernel for large N (one CTA per SM): the
+// w rows and the column chunks of the CTA's 2048-row tiles stream through
+// the bdot_bulk ring (8 x 16 KB, cp.async.bulk + mbarrier), the h prologue
+// runs while the first items are in flight, and the new w rows are stored
+// from registers.  Every element's update w - h_0 q_0 - h_1 q_1 - ... is
+// the tile kernel's FMA chain in the same column order (bit-identical w and
+// h); only ||w||^2 is summed in another order.
+__global__ void __launch_bounds__(256, 1) bupd_gram_bulk_kernel(ColPtrs Q, int ncol, int k,
+                                                                const double* __restrict__ g,
+                                                                const double* __restrict__ grow,
+                                                                double* __restrict__ hout, double* w,
+                                                                int64_t N, RedArgs ra) {
+  RK_PDL_ENTRY();
+  extern __shared__ __align__(128) unsigned char bk_sm[];
+  double2* ring = reinterpret_cast<double2*>(bk_sm);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(bk_sm + (size_t)BK_SLOTS * BK_BYTES);
+  __shared__ double gs[MAXCOL], hs[MAXCOL];
+  constexpr int RV = BK_ROWS / 512;
+  const int64_t ntile = N / BK_ROWS;
+  const int64_t mytiles = ntile > blockIdx.x ? (ntile - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int per = ncol + 1;   // items per tile: w, Q_0 .. Q_{ncol-1}
+  const int64_t nitem = mytiles * per;
+  int ic = -1;
+  int64_t irow = (int64_t)blockIdx.x * BK_ROWS;
+  auto issue = [&](int slot) {
+    const double* src = (ic < 0 ? w : Q.p[ic]) + irow;
+    if (++ic == ncol) {
+      ic = -1;
+      irow += (int64_t)gridDim.x * BK_ROWS;
+    }
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bk_smem(bar + slot)),
+                 "r"(BK_BYTES)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            bk_smem(ring + (size_t)slot * (BK_ROWS / 2))),
+        "l"(src), "r"(BK_BYTES), "r"(bk_smem(bar + slot))
+        : "memory");
+  };
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < BK_SLOTS; ++q)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bk_smem(bar + q)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int q = 0; q < BK_SLOTS && q < nitem; ++q) issue(q);
+  }
+  // h = 2 g - G g (bupd_gram_kernel's prologue, same FMA order)
+  for (int c = threadIdx.x; c < MAXCOL; c += blockDim.x) gs[c] = c < ncol ? g[c] : 0.0;
+  __syncthreads();
+  for (int c = threadIdx.x; c < ncol; c += blockDim.x) {
+    double gg = 0.0;
+    for (int l = 0; l < ncol; ++l) {
+      double Gcl;
+      if (c < k && l < k) Gcl = (c == l) ? 1.0 : 0.0;
+      else if (c >= l) Gcl = grow[(int64_t)c * MAXCOL + l];
+      else Gcl = grow[(int64_t)l * MAXCOL + c];
+      gg = fma(Gcl, gs[l], gg);
+    }
+    const double h = 2.0 * gs[c] - gg;
+    hs[c] = h;
+    if (blockIdx.x == 0) hout[c] = h;
+  }
+  __syncthreads();
+  int slot = 0;
+  uint32_t phase = 0;
+  int64_t it = 0;
+  auto next = [&]() {
+    __syncthreads();   // every thread is done with the slot
+    if (threadIdx.x == 0 && it + BK_SLOTS < nitem) issue(slot);
+    ++it;
+    if (++slot == BK_SLOTS) {
+      slot = 0;
+      phase ^= 1;
+    }
+  };
+  double acc[1] = {0.0};
+  int64_t row0 = (int64_t)blockIdx.x * BK_ROWS;
+#pragma unroll 1
+  for (int64_t lt = 0; lt < mytiles; ++lt, row0 += (int64_t)gridDim.x * BK_ROWS) {
+    double2 wv[RV];
+    while (!bk_try(bar + slot, phase)) {
+    }
+    {
+      const double2* sl = ring + (size_t)slot * (BK_ROWS / 2);
+#pragma unroll
+      for (int u = 0; u < RV; ++u) wv[u] = sl[threadIdx.x + 256 * u];
+    }
+    next();
+#pragma unroll 1
+    for (int c = 0; c < ncol; ++c) {
+      const double hc = hs[c];
+      while (!bk_try(bar + slot, phase)) {
+      }
+      const double2* qs = ring + (size_t)slot * (BK_ROWS / 2);
+#pragma unroll
+      for (int u = 0; u < RV; ++u) {
+        const double2 q = qs[threadIdx.x + 256 * u];
+        wv[u].x = fma(-hc, q.x, wv[u].x);
+        wv[u].y = fma(-hc, q.y, wv[u].y);
+      }
+      next();
+    }
+#pragma unroll
+    for (int u = 0; u < RV; ++u) {
+      *reinterpret_cast<double2*>(w + row0 + 2 * (threadIdx.x + 256 * u)) = wv[u];
+      acc[0] = fma(wv[u].x, wv[u].x, acc[0]);
+      acc[0] = fma(wv[u].y, wv[u].y, acc[0]);
+    }
+  }
+  for (int64_t r = ntile * BK_ROWS + 2 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x); r < N;
+       r += 2 * (int64_t)gridDim.x * blockDim.x) {
+    double2 wn = *reinterpret_cast<const double2*>(w + r);
+#pragma unroll 1
+    for (int c = 0; c < ncol; ++c) {
+      const Vec<2> a = ldv_stream<2>(Q.p[c] + r);
+      wn.x = fma(-hs[c], a.v[0], wn.x);
+      wn.y = fma(-hs[c], a.v[1], wn.y);
+    }
+    *reinterpret_cast<double2*>(w + r) = wn;
+    acc[0] = fma(wn.x, wn.x, acc[0]);
+    acc[0] = fma(wn.y, wn.y, acc[0]);
+  }
+  block_reduce_store<1>(acc, 1, ra);
+}
+
 // gsh[c] = gs g_c with g_c the deferred block-dot sums; CTA 0 stores g_c
 template <int NC>
 __device__ __forceinline__ void coef_from_partials(const CoefIn& cin, int ncol, double gs, double* gsh) {
@@ -1058,6 +1182,14 @@ void bupd_gram(rk_ctx* ctx, const std::vector<const double*>& cols, int k, const
   ColPtrs Q = make_cols_padded(cols, nc);
   RedArgs ra = red_args(ctx, red_out);
   Launch L(ctx, "bupd", 8.0 * N * (ncol + 2));
+  // bulk-copy form at large N (>= 16 ring tiles per SM: the ring's fill and
+  // drain are amortised); RK_BUPD_BULK: 0 never, 2 always
+  if (ctx->bupd_bulk == 2 || (ctx->bupd_bulk == 1 && N >= (int64_t)BK_ROWS * ctx->sms * 16)) {
+    launch_bulk(ctx, bupd_gram_bulk_kernel, Q, ncol, k, g, grow, hout, w, N, ra);
+    L.done();
+    allreduce(ctx, red_out, 1);
+    return;
+  }
 #define RK_BG(NCV) launch_k(ctx, bupd_gram_kernel<NCV>, N / (2 * TRV), dim3(256), Q, ncol, k, g, grow, hout, w, N, ra)
   switch (nc) {
     case 8: RK_BG(8); break;

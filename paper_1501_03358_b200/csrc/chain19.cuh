@@ -238,6 +238,27 @@ chain19_kernel(const __grid_constant__ CUtensorMap mbM, const __grid_constant__ 
   // at the two planes below the one it produced last
   double xcm = xbase[xo[1][1]], xcc = xbase[XS + xo[1][1]];   // planes qfirst, tau0: slots 0, 1
   double hm = 0.0, hc = 0.0;
+  // In-plane neighbourhoods carried in registers from step to step (each
+  // tile / ring value is read from shared memory once per thread instead of
+  // up to three times): order W, E, S, N, SW, SE, NW, NE (xo[1][0], xo[1][2],
+  // xo[0][1], xo[2][1], xo[0][0], xo[0][2], xo[2][0], xo[2][2]).
+  //   stage 0: a0 = input plane tau's 8 neighbours, p0 = plane tau-1's 4 edges;
+  //   stage 1: a1 = stage-0 plane tau-1's 8 neighbours, p1 = plane tau-2's 4 edges.
+  // RK_C19_ROT bit 0: stage 0 carries, bit 1: stage 1 carries.
+  constexpr bool ROT0 = (RK_C19_ROT & 1) != 0, ROT1 = (RK_C19_ROT & 2) != 0;
+  const int xn8[8] = {xo[1][0], xo[1][2], xo[0][1], xo[2][1], xo[0][0], xo[0][2], xo[2][0], xo[2][2]};
+  constexpr int rn8[8] = {-1, 1, -EX, EX, -EX - 1, -EX + 1, EX - 1, EX + 1};
+  double a0[8], p0[4], a1[8], p1[4];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    a0[e] = ROT0 ? xbase[XS + xn8[e]] : 0.0;
+    a1[e] = 0.0;
+  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    p0[e] = ROT0 ? xbase[xn8[e]] : 0.0;
+    p1[e] = 0.0;
+  }
 
   // y = sum_d a_d v_d in stencil_kernel<19>'s order: four FMA chains (band
   // d mod 4), summed as (c0 + c1) + (c2 + c3) -- half the dependent-FMA
@@ -276,26 +297,32 @@ chain19_kernel(const __grid_constant__ CUtensorMap mbM, const __grid_constant__ 
         cut_p = ((g + 1) % cp.zb) == 0;                                                           \
       }                                                                                           \
       const double xn = tp[xo[1][1]];                                                             \
+      double nb[8];   /* plane tau+1's neighbours (all 8 when carried, else the 4 edges) */      \
+      _Pragma("unroll") for (int e = 0; e < (ROT0 ? 8 : 4); ++e) nb[e] = tp[xn8[e]];            \
       double v[19];                                                                               \
       v[0] = xcc;                                                                                 \
-      v[1] = t0[xo[1][0]];                                                                        \
-      v[2] = t0[xo[1][2]];                                                                        \
-      v[3] = t0[xo[0][1]];                                                                        \
-      v[4] = t0[xo[2][1]];                                                                        \
+      v[1] = ROT0 ? a0[0] : t0[xo[1][0]];                                                         \
+      v[2] = ROT0 ? a0[1] : t0[xo[1][2]];                                                         \
+      v[3] = ROT0 ? a0[2] : t0[xo[0][1]];                                                         \
+      v[4] = ROT0 ? a0[3] : t0[xo[2][1]];                                                         \
       v[5] = cut_m ? 0.0 : xcm;                                                                   \
       v[6] = cut_p ? 0.0 : xn;                                                                    \
-      v[7] = t0[xo[0][0]];                                                                        \
-      v[8] = t0[xo[0][2]];                                                                        \
-      v[9] = t0[xo[2][0]];                                                                        \
-      v[10] = t0[xo[2][2]];                                                                       \
-      v[11] = cut_m ? 0.0 : tm[xo[0][1]];                                                         \
-      v[12] = cut_m ? 0.0 : tm[xo[2][1]];                                                         \
-      v[13] = cut_p ? 0.0 : tp[xo[0][1]];                                                         \
-      v[14] = cut_p ? 0.0 : tp[xo[2][1]];                                                         \
-      v[15] = cut_m ? 0.0 : tm[xo[1][0]];                                                         \
-      v[16] = cut_m ? 0.0 : tm[xo[1][2]];                                                         \
-      v[17] = cut_p ? 0.0 : tp[xo[1][0]];                                                         \
-      v[18] = cut_p ? 0.0 : tp[xo[1][2]];                                                         \
+      v[7] = ROT0 ? a0[4] : t0[xo[0][0]];                                                         \
+      v[8] = ROT0 ? a0[5] : t0[xo[0][2]];                                                         \
+      v[9] = ROT0 ? a0[6] : t0[xo[2][0]];                                                         \
+      v[10] = ROT0 ? a0[7] : t0[xo[2][2]];                                                        \
+      v[11] = cut_m ? 0.0 : (ROT0 ? p0[2] : tm[xo[0][1]]);                                        \
+      v[12] = cut_m ? 0.0 : (ROT0 ? p0[3] : tm[xo[2][1]]);                                        \
+      v[13] = cut_p ? 0.0 : nb[2];                                                                \
+      v[14] = cut_p ? 0.0 : nb[3];                                                                \
+      v[15] = cut_m ? 0.0 : (ROT0 ? p0[0] : tm[xo[1][0]]);                                        \
+      v[16] = cut_m ? 0.0 : (ROT0 ? p0[1] : tm[xo[1][2]]);                                        \
+      v[17] = cut_p ? 0.0 : nb[0];                                                                \
+      v[18] = cut_p ? 0.0 : nb[1];                                                                \
+      if (ROT0) {                                                                                 \
+        _Pragma("unroll") for (int e = 0; e < 4; ++e) p0[e] = a0[e];                              \
+        _Pragma("unroll") for (int e = 0; e < 8; ++e) a0[e] = nb[e];                              \
+      }                                                                                           \
       const double y = apply19(bnd[PH], v);                                                       \
       const double inv = bnd[PH][19];                                                             \
       if (K0 == CK_SPMV1) {                                                                       \
@@ -328,6 +355,11 @@ chain19_kernel(const __grid_constant__ CUtensorMap mbM, const __grid_constant__ 
       constexpr int R = (PH + 1) % 2, RM = ((U) + 2) & 3, R0 = ((U) + 3) & 3, RQ = (U) & 3;       \
       double vs = 0.0;                                                                            \
       const int q = tau - 1;                                                                      \
+      double nr[8];   /* stage-0 plane tau's neighbours (carried: read once, every step) */      \
+      if (ROT1 && interior) {                                                                     \
+        const double* rp = ring + RQ * RP + gofs;                                                 \
+        _Pragma("unroll") for (int e = 0; e < 8; ++e) nr[e] = rp[rn8[e]];                         \
+      }                                                                                           \
       if (tau >= tau0 + 2 && interior) {                                                          \
         const double* rm = ring + RM * RP + gofs;                                                 \
         const double* r0 = ring + R0 * RP + gofs;                                                 \
@@ -340,27 +372,31 @@ chain19_kernel(const __grid_constant__ CUtensorMap mbM, const __grid_constant__ 
         }                                                                                         \
         double v[19];                                                                             \
         v[0] = hc;                                                                                \
-        v[1] = r0[-1];                                                                            \
-        v[2] = r0[1];                                                                             \
-        v[3] = r0[-EX];                                                                           \
-        v[4] = r0[EX];                                                                            \
+        v[1] = ROT1 ? a1[0] : r0[-1];                                                             \
+        v[2] = ROT1 ? a1[1] : r0[1];                                                              \
+        v[3] = ROT1 ? a1[2] : r0[-EX];                                                            \
+        v[4] = ROT1 ? a1[3] : r0[EX];                                                             \
         v[5] = cut_m ? 0.0 : hm;                                                                  \
         v[6] = cut_p ? 0.0 : v0;                                                                  \
-        v[7] = r0[-EX - 1];                                                                       \
-        v[8] = r0[-EX + 1];                                                                       \
-        v[9] = r0[EX - 1];                                                                        \
-        v[10] = r0[EX + 1];                                                                       \
-        v[11] = cut_m ? 0.0 : rm[-EX];                                                            \
-        v[12] = cut_m ? 0.0 : rm[EX];                                                             \
-        v[13] = cut_p ? 0.0 : rp[-EX];                                                            \
-        v[14] = cut_p ? 0.0 : rp[EX];                                                             \
-        v[15] = cut_m ? 0.0 : rm[-1];                                                             \
-        v[16] = cut_m ? 0.0 : rm[1];                                                              \
-        v[17] = cut_p ? 0.0 : rp[-1];                                                             \
-        v[18] = cut_p ? 0.0 : rp[1];                                                              \
+        v[7] = ROT1 ? a1[4] : r0[-EX - 1];                                                        \
+        v[8] = ROT1 ? a1[5] : r0[-EX + 1];                                                        \
+        v[9] = ROT1 ? a1[6] : r0[EX - 1];                                                         \
+        v[10] = ROT1 ? a1[7] : r0[EX + 1];                                                        \
+        v[11] = cut_m ? 0.0 : (ROT1 ? p1[2] : rm[-EX]);                                           \
+        v[12] = cut_m ? 0.0 : (ROT1 ? p1[3] : rm[EX]);                                            \
+        v[13] = cut_p ? 0.0 : (ROT1 ? nr[2] : rp[-EX]);                                           \
+        v[14] = cut_p ? 0.0 : (ROT1 ? nr[3] : rp[EX]);                                            \
+        v[15] = cut_m ? 0.0 : (ROT1 ? p1[0] : rm[-1]);                                            \
+        v[16] = cut_m ? 0.0 : (ROT1 ? p1[1] : rm[1]);                                             \
+        v[17] = cut_p ? 0.0 : (ROT1 ? nr[0] : rp[-1]);                                            \
+        v[18] = cut_p ? 0.0 : (ROT1 ? nr[1] : rp[1]);                                             \
         const double y = apply19(bnd[R], v);                                                      \
         vs = (K1 == CK_SWEEP) ? fma(cp.omega[1] * (rr[R] - y), bnd[R][19], hc) : y;               \
         if (q >= z0 && q < z1) cp.out[(int64_t)pl_of(q) * cp.P + cxy] = vs;                       \
+      }                                                                                           \
+      if (ROT1 && interior) {                                                                     \
+        _Pragma("unroll") for (int e = 0; e < 4; ++e) p1[e] = a1[e];                              \
+        _Pragma("unroll") for (int e = 0; e < 8; ++e) a1[e] = nr[e];                              \
       }                                                                                           \
       hm = hc;                                                                                    \
       hc = v0;                                                                                    \

@@ -160,6 +160,7 @@ struct rk_ctx {
   bool pdl_skip_next = false;   // set by a chain launch (mode 2)
   const double* gate = nullptr; // copied into the kernels launched while set (rBiCGStab lookahead)
   bool defer_coef = true;        // bproject: deferred block-dot finalisation (RK_DEFER_COEF=0: off)
+  int bupd_bulk = 1;             // bulk-copy-fed Gram-corrected update: 0 off, 1 large N, 2 always (RK_BUPD_BULK)
   int bdot_bulk = 1;             // bulk-copy-fed bdot: 0 off, 1 large N, 2 always (RK_BDOT_BULK)
   cudaStream_t stream = nullptr;
   bool own_stream = false;

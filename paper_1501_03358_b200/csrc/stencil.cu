@@ -261,6 +261,7 @@ void init_ctx_kernels(rk_ctx* ctx) {
   ctx->pdl = std::getenv("RK_NO_PDL") == nullptr;
   if (const char* m = std::getenv("RK_PDL_MODE")) ctx->pdl_mode = std::atoi(m);
   if (const char* m = std::getenv("RK_BDOT_BULK")) ctx->bdot_bulk = std::atoi(m);
+  if (const char* m = std::getenv("RK_BUPD_BULK")) ctx->bupd_bulk = std::atoi(m);
   if (const char* m = std::getenv("RK_DEFER_COEF")) ctx->defer_coef = std::atoi(m) != 0;
   // per-CTA partials for up to MAXCOL + 4 values, up to 8 resident 256-thread CTAs per SM
   ctx->partials_cap = (size_t)(MAXCOL + 4) * sms * 8;

@@ -393,3 +393,35 @@ def test_bicg_xr(kern, bop, mode, k):
     got = recd(nd)
     assert abs(got["rho"] - rho_n) <= TOL * float(np.abs(rt) @ np.abs(rr_))
     assert abs(got["rr"] - rr_n) <= TOL * rr_n
+
+
+@pytest.mark.parametrize("n", SIZES[1:])
+@pytest.mark.parametrize("ncol,k", [(8, 0), (31, 30), (71, 30)])
+def test_gram_update_bulk_bitwise(rk, kern, n, ncol, k, monkeypatch):
+    """The bulk-copy-fed Gram-corrected update (RK_BUPD_BULK=2) gives the
+    register-tiled kernel's w and h bit for bit (same FMA chain per
+    element), ||w||^2 to rounding, and the oracle's values to 1e-12."""
+    rng = np.random.default_rng(550 + ncol)
+    Qh, Q = cols(n, ncol, 551 + ncol)
+    w = rng.uniform(-1, 1, n)
+    g = rng.uniform(-1, 1, ncol)
+    grow = np.zeros((80, 80))
+    grow[k:ncol, :ncol] = rng.uniform(-1e-3, 1e-3, (ncol - k, ncol))
+    for i in range(k, ncol):
+        grow[i, i] = 1.0
+    out = {}
+    for mode in ("0", "2"):
+        monkeypatch.setenv("RK_BUPD_BULK", mode)
+        c = rk.Context(0)
+        try:
+            wd = dev(w)
+            h, nrm2 = kern.gram_update(c, Q, k, dev(g), dev(grow.reshape(-1)), wd)
+            out[mode] = (host(wd), host(h), host(nrm2)[0])
+        finally:
+            c.close()
+    assert np.array_equal(out["0"][0], out["2"][0])
+    assert np.array_equal(out["0"][1], out["2"][1])
+    assert abs(out["0"][2] - out["2"][2]) <= 1e-13 * out["0"][2]
+    rh, rw, rnn = K.gram_update(Qh, k, g, grow, w)
+    check_vec(out["2"][0], rw, abs_update_terms(Qh, rh, w))
+    assert abs(out["2"][2] - rnn) <= TOL * rnn
