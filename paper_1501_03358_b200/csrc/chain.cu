@@ -55,6 +55,9 @@
 #ifndef RK_C19_ROT
 #define RK_C19_ROT 1    // 19-point chain: in-plane neighbourhoods carried in registers (bit 0 stage 0, bit 1 stage 1)
 #endif
+#ifndef RK_C19_ALLLANES
+#define RK_C19_ALLLANES 1   // 19-point chain: stage 0 unconditional in every lane (no branch around the carried registers)
+#endif
 #ifndef RK_C19_INVD
 #define RK_C19_INVD 0   // 19-point chain: 1/D recomputed (0) or streamed as a 20th band (1)
 #endif

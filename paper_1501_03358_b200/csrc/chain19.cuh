@@ -277,7 +277,9 @@ chain19_kernel(const __grid_constant__ CUtensorMap mbM, const __grid_constant__ 
     mbar_wait(&bbar[bs0], bpar);                                                                  \
     mbar_wait(&bars[XP], (U) < 6 ? par : par ^ 1u);                                               \
     double v0 = 0.0;                                                                              \
-    if (active) {                                                                                 \
+    /* every thread runs stage 0: the spare lanes of the halo warp (!active) alias halo cell 0 */ \
+    /* and store the same value to the same ring entry, so no branch splits the carried registers */ \
+    if (RK_C19_ALLLANES || active) {                                                              \
       /* stage 0 at plane tau: bands / rhs to registers, input neighbours from the tiles */      \
       const double* bsl = bbase + bs0 * BSD + boff;                                               \
       if (mwarp) {                                                                                \
