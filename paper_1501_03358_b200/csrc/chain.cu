@@ -828,11 +828,14 @@ void chain_run(rk_op* op, const std::vector<int>& kinds, const std::vector<doubl
     // several ranks: the launch reads its input len planes and the sweeps'
     // right-hand side len - 1 planes beyond the slab (stage 0 recomputes the
     // halo planes the later stages need)
+    // (input and right-hand-side halos of one launch in one collective launch)
+    comm_group_begin(op->ctx);
     halo(op, cur, len);
     if (kinds[a] != CK_SPMV1 && rhs && len - 1 > rhs_depth) {
       halo(op, rhs, len - 1);
       rhs_depth = len - 1;
     }
+    comm_group_end(op->ctx);
     chain_launch(op, len, kinds.data() + a, om.data() + a, cur, rhs,
                  (kinds[a] == CK_SPMV1) ? out_t : nullptr, last ? out_mid : nullptr, dst,
                  loc.data() + a, zbs);

@@ -186,6 +186,24 @@ void exchange(rk_op* op, const double* lo_src, const double* hi_src, double* lo_
 #endif
 }
 
+// Collectives issued between comm_group_begin / comm_group_end go out as one
+// NCCL launch (NCCL groups nest; the outermost end issues them); the
+// in-process rank group runs them one by one as issued.
+void comm_group_begin(rk_ctx* ctx) {
+#ifdef RK_WITH_NCCL
+  if (ctx->nranks > 1 && !ctx->lgrp) RK_NCCL(ncclGroupStart());
+#else
+  (void)ctx;
+#endif
+}
+void comm_group_end(rk_ctx* ctx) {
+#ifdef RK_WITH_NCCL
+  if (ctx->nranks > 1 && !ctx->lgrp) RK_NCCL(ncclGroupEnd());
+#else
+  (void)ctx;
+#endif
+}
+
 // Fill `depth` ghost planes below and above the padded vector v (local
 // planes [0, nz_local)) from the z-neighbours' boundary planes.
 void halo(rk_op* op, const double* v, int depth) {

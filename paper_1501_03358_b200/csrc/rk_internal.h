@@ -386,6 +386,10 @@ void halo(rk_op* op, const double* v, int depth = 1);
 void exchange(rk_op* op, const double* lo_src, const double* hi_src, double* lo_dst, double* hi_dst,
               size_t count);
 void allreduce(rk_ctx* ctx, double* buf, int n);
+// one NCCL launch for the collectives issued in between (no-op on one rank
+// and for in-process rank groups)
+void comm_group_begin(rk_ctx* ctx);
+void comm_group_end(rk_ctx* ctx);
 // two reduction outputs (not adjacent in memory) in one collective launch
 void allreduce2(rk_ctx* ctx, double* a, int na, double* b, int nb);
 // in-process rank groups (tests of the multi-rank schedule on one device)
