@@ -273,6 +273,12 @@ rk_status rk_block_project(rk_ctx* ctx, int ncol, const double* const* Q, double
  * 0 <= k <= ncol; n even and every pointer 16-byte aligned. */
 rk_status rk_gram_update(rk_ctx* ctx, int ncol, int k, const double* const* Q, const double* g,
                          const double* grow, double* h_out, double* w, int64_t n, double* nrm2);
+/* Recycle-space correction (Alg. 3 line 1b, Alg. 4 line 1c, reading D20):
+ * r <- r - sum_c C_c xi[c]; if x != NULL (then U != NULL), x <- x + sum_c
+ * U_c xi[c]; nrm2 = ||r_new||^2.  C, U: HOST arrays of k (1 <= k <= 48)
+ * DEVICE pointers. */
+rk_status rk_project_update(rk_ctx* ctx, int k, const double* const* C, const double* const* U,
+                            const double* xi, double* r, double* x, int64_t n, double* nrm2);
 /* Arnoldi normalisation (Alg. 3 line 10, reading D18): h = sqrt(nrm2[0]);
  * if nin2 != NULL and !(h > 1e-14 sqrt(nin2[0])) (happy breakdown) then
  * w <- 0 and flag[0] = 1, else w <- w / h and flag[0] = 0 (flag nullable). */

@@ -19,7 +19,7 @@ Pins (tests/oracle/test_kernel_pins.py):
     g1) (the algebra DESIGN.md R19 rests on), computed independently here
     in exact rational arithmetic; with G = I it is block_update(Q, g, w);
   * normalize: unit norm, and the D18 breakdown branch;
-  * lincomb / rotate: exact rational arithmetic;
+  * project_update, lincomb, rotate: exact rational arithmetic;
   * bicg_p, bicg_project_s, bicg_xr (with block_dot / block_update for
     line 12a) composed into whole iterations reproduce oracle.krylov.
     rbicgstab's per-iteration scalars and iterates, whose iterates are in
@@ -84,6 +84,21 @@ def gram_update(Q, k, g, grow, w):
     h = np.array([2.0 * g[c] - _dot(G[c], g) for c in range(len(Q))])
     wn, (nn,) = block_update(Q, h, w, (None,))
     return h, wn, nn
+
+
+def project_update(C, U, xi, r, x=None):
+    """Alg. 3 line 1b / Alg. 4 line 1c (reading D20: also at every cycle
+    start): r <- r - C xi, x <- x + U xi.  Returns (r_new, x_new or None,
+    ||r_new||^2)."""
+    rn = r.copy()
+    for c, q in enumerate(C):
+        rn = rn - xi[c] * q
+    xn = None
+    if x is not None:
+        xn = x.copy()
+        for c, u in enumerate(U):
+            xn = xn + xi[c] * u
+    return rn, xn, _dot(rn, rn)
 
 
 def normalize(w, nrm2, nin2=None):

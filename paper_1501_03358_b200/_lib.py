@@ -96,6 +96,7 @@ def lib():
         "rk_block_update": ([vp, i32, vp, vp, vp, i64, i32, vp, vp], i32),
         "rk_block_project": ([vp, i32, vp, vp, i64, vp, vp], i32),
         "rk_gram_update": ([vp, i32, i32, vp, vp, vp, vp, vp, i64, vp], i32),
+        "rk_project_update": ([vp, i32, vp, vp, vp, vp, vp, i64, vp], i32),
         "rk_normalize": ([vp, vp, i64, vp, vp, vp], i32),
         "rk_lincomb": ([vp, i32, vp, vp, i32, vp, vp, vp, i64], i32),
         "rk_rotate": ([vp, i32, vp, vp, i32, i64], i32),
@@ -126,6 +127,6 @@ EXPORTED = ["rk_last_error", "rk_version", "rk_nccl_unique_id", "rk_ctx_create",
             "rk_solve", "rk_solve_host", "rk_solve_host_ex", "rk_stage_rhs", "rk_solve_staged",
             "rk_host_sync", "rk_history", "rk_trace", "rk_solver_workspace", "rk_launch_count",
             "rk_profile_enable", "rk_profile_every", "rk_profile_read",
-            "rk_block_dot", "rk_block_update", "rk_block_project", "rk_gram_update",
+            "rk_block_dot", "rk_block_update", "rk_block_project", "rk_gram_update", "rk_project_update",
             "rk_normalize", "rk_lincomb", "rk_rotate", "rk_bicg_p", "rk_bicg_s",
             "rk_bicg_project_s", "rk_bicg_xr"]

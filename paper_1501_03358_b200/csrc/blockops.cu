@@ -445,10 +445,13 @@ __global__ void __launch_bounds__(256) bupd_gram_kernel(ColPtrs Q, int ncol, int
 // runs while the first items are in flight, and the new w rows are stored
 // from registers.  Every element's update w - h_0 q_0 - h_1 q_1 - ... is
 // the tile kernel's FMA chain in the same column order (bit-identical w and
-// h); only ||w||^2 is summed in another order.
+// h); only ||w||^2 is summed in another order.  grow == nullptr: a plain
+// block update with h = gs g (the recycle projection r -= C xi, x += U xi);
+// hout nullable; ra.out == nullptr: no ||w||^2.
 __global__ void __launch_bounds__(256, 1) bupd_gram_bulk_kernel(ColPtrs Q, int ncol, int k,
                                                                 const double* __restrict__ g,
                                                                 const double* __restrict__ grow,
+                                                                double gs_scale,
                                                                 double* __restrict__ hout, double* w,
                                                                 int64_t N, RedArgs ra) {
   RK_PDL_ENTRY();
@@ -488,17 +491,22 @@ __global__ void __launch_bounds__(256, 1) bupd_gram_bulk_kernel(ColPtrs Q, int n
   for (int c = threadIdx.x; c < MAXCOL; c += blockDim.x) gs[c] = c < ncol ? g[c] : 0.0;
   __syncthreads();
   for (int c = threadIdx.x; c < ncol; c += blockDim.x) {
-    double gg = 0.0;
-    for (int l = 0; l < ncol; ++l) {
-      double Gcl;
-      if (c < k && l < k) Gcl = (c == l) ? 1.0 : 0.0;
-      else if (c >= l) Gcl = grow[(int64_t)c * MAXCOL + l];
-      else Gcl = grow[(int64_t)l * MAXCOL + c];
-      gg = fma(Gcl, gs[l], gg);
+    double h;
+    if (grow) {
+      double gg = 0.0;
+      for (int l = 0; l < ncol; ++l) {
+        double Gcl;
+        if (c < k && l < k) Gcl = (c == l) ? 1.0 : 0.0;
+        else if (c >= l) Gcl = grow[(int64_t)c * MAXCOL + l];
+        else Gcl = grow[(int64_t)l * MAXCOL + c];
+        gg = fma(Gcl, gs[l], gg);
+      }
+      h = 2.0 * gs[c] - gg;
+    } else {
+      h = gs_scale * gs[c];
     }
-    const double h = 2.0 * gs[c] - gg;
     hs[c] = h;
-    if (blockIdx.x == 0) hout[c] = h;
+    if (hout && blockIdx.x == 0) hout[c] = h;
   }
   __syncthreads();
   int slot = 0;
@@ -560,7 +568,7 @@ __global__ void __launch_bounds__(256, 1) bupd_gram_bulk_kernel(ColPtrs Q, int n
     acc[0] = fma(wn.x, wn.x, acc[0]);
     acc[0] = fma(wn.y, wn.y, acc[0]);
   }
-  block_reduce_store<1>(acc, 1, ra);
+  if (ra.out) block_reduce_store<1>(acc, 1, ra);
 }
 
 // gsh[c] = gs g_c with g_c the deferred block-dot sums; CTA 0 stores g_c
@@ -926,6 +934,45 @@ __global__ void __launch_bounds__(256) rotate_kernel(ColPtrs Qc, int k, int kout
 }
 
 
+// The same rotation with T in the kernel's parameter space (constant bank,
+// up to 18 KB of parameters: CUDA >= 12.1 on sm_70+): every T entry is a
+// compile-time operand of its FMA -- the shared-memory form spent one LDS per
+// FMA (1.5 TB/s at c4, k = 31); stride NC (t[o * NC + c] = T(c, o)); the
+// same FMA order as rotate_kernel (bit-identical).
+template <int NC>
+struct TMat {
+  double t[NC * NC];
+};
+template <int NC, int VEC>
+__global__ void __launch_bounds__(256) rotate_cb_kernel(ColPtrs Qc, int k, int kout,
+                                                        const __grid_constant__ TMat<NC> T, int64_t N) {
+  RK_PDL_ENTRY();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t NE = N / VEC;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < NE; e += stride) {
+    const int64_t n = e * VEC;
+    Vec<VEC> in[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+      if (c < k) in[c] = ldv<VEC>(Qc.p[c] + n);
+#pragma unroll
+    for (int o = 0; o < NC; ++o) {
+      if (o < kout) {
+        Vec<VEC> s;
+#pragma unroll
+        for (int t = 0; t < VEC; ++t) s.v[t] = 0.0;
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+          if (c < k) {
+#pragma unroll
+            for (int t = 0; t < VEC; ++t) s.v[t] = fma(in[c].v[t], T.t[o * NC + c], s.v[t]);
+          }
+        stv<VEC>(const_cast<double*>(Qc.p[o]) + n, s);
+      }
+    }
+  }
+}
+
 // =================================================================== host
 namespace {
 // one CTA per SM (the ring fills the shared memory), grid = #SMs
@@ -1185,7 +1232,7 @@ void bupd_gram(rk_ctx* ctx, const std::vector<const double*>& cols, int k, const
   // bulk-copy form at large N (>= 16 ring tiles per SM: the ring's fill and
   // drain are amortised); RK_BUPD_BULK: 0 never, 2 always
   if (ctx->bupd_bulk == 2 || (ctx->bupd_bulk == 1 && N >= (int64_t)BK_ROWS * ctx->sms * 16)) {
-    launch_bulk(ctx, bupd_gram_bulk_kernel, Q, ncol, k, g, grow, hout, w, N, ra);
+    launch_bulk(ctx, bupd_gram_bulk_kernel, Q, ncol, k, g, grow, 1.0, hout, w, N, ra);
     L.done();
     allreduce(ctx, red_out, 1);
     return;
@@ -1259,6 +1306,23 @@ void proj(rk_ctx* ctx, const std::vector<const double*>& C, const std::vector<co
   ColPtrs Cp = make_cols_padded(C, nc), Up = make_cols_padded(U, nc);
   int vec = pick_vec(N, {r, x}, C);
   if (x && pick_vec(N, {}, U) == 1) vec = 1;
+  // large N: two bulk-copy block updates in column-chunk order (r -= C xi
+  // with ||r||^2, then x += U xi) -- the row-interleaved kernel below reads
+  // the 2k columns with poor DRAM page locality (4.4 TB/s at c4)
+  if (vec == 2 && ctx->bupd_bulk != 0 &&
+      (ctx->bupd_bulk == 2 || N >= (int64_t)BK_ROWS * ctx->sms * 16)) {
+    Launch L(ctx, "proj", 8.0 * N * (k * (x ? 2 : 1) + 2 + (x ? 2 : 0)));
+    launch_bulk(ctx, bupd_gram_bulk_kernel, Cp, k, 0, xi, (const double*)nullptr, 1.0, (double*)nullptr, r, N,
+                ra);
+    if (x) {
+      RedArgs none = red_args(ctx, nullptr);
+      launch_bulk(ctx, bupd_gram_bulk_kernel, Up, k, 0, xi, (const double*)nullptr, -1.0, (double*)nullptr, x,
+                  N, none);
+    }
+    L.done();
+    allreduce(ctx, red_out, 1);
+    return;
+  }
   const int64_t work = N / vec;
   Launch L(ctx, "proj", 8.0 * N * (k * (x ? 2 : 1) + 2 + (x ? 2 : 0)));
 #define RK_PJ(NCV)                                                                               \
@@ -1277,7 +1341,21 @@ void proj(rk_ctx* ctx, const std::vector<const double*>& C, const std::vector<co
   allreduce(ctx, red_out, 1);
 }
 
-void rotate(rk_ctx* ctx, const std::vector<double*>& cols, const double* T, int64_t N, int kout) {
+namespace {
+template <int NC>
+void launch_rotate_cb(rk_ctx* ctx, const ColPtrs& Q, int k, int kout, const double* Th, int64_t N, bool vec2) {
+  TMat<NC> tm;
+  memset(&tm, 0, sizeof(tm));
+  for (int o = 0; o < kout; ++o)
+    for (int c = 0; c < k; ++c) tm.t[o * NC + c] = Th[(size_t)o * k + c];
+  // two cells per thread while the k inputs fit the registers
+  if (vec2 && NC <= 32) launch_k(ctx, rotate_cb_kernel<NC, 2>, N / 2, dim3(256), Q, k, kout, tm, N);
+  else launch_k(ctx, rotate_cb_kernel<NC, 1>, N, dim3(256), Q, k, kout, tm, N);
+}
+}  // namespace
+
+void rotate(rk_ctx* ctx, const std::vector<double*>& cols, const double* T, int64_t N, int kout,
+            const double* T_host) {
   const int k = (int)cols.size();
   if (k == 0) return;
   if (kout < 0) kout = k;
@@ -1287,6 +1365,18 @@ void rotate(rk_ctx* ctx, const std::vector<double*>& cols, const double* T, int6
   memset(&Q, 0, sizeof(Q));
   for (int c = 0; c < k; ++c) Q.p[c] = cols[c];
   Launch L(ctx, "rotate", 8.0 * N * (k + kout));
+  if (T_host) {
+    std::vector<const double*> cc(cols.begin(), cols.end());
+    const bool vec2 = pick_vec(N, {}, cc) == 2;
+    switch (nc) {
+      case 8: launch_rotate_cb<8>(ctx, Q, k, kout, T_host, N, vec2); break;
+      case 16: launch_rotate_cb<16>(ctx, Q, k, kout, T_host, N, vec2); break;
+      case 32: launch_rotate_cb<32>(ctx, Q, k, kout, T_host, N, vec2); break;
+      default: launch_rotate_cb<48>(ctx, Q, k, kout, T_host, N, vec2); break;
+    }
+    L.done();
+    return;
+  }
   switch (nc) {
     case 8: launch_k(ctx, rotate_kernel<8>, N, dim3(256), Q, k, kout, T, N); break;
     case 16: launch_k(ctx, rotate_kernel<16>, N, dim3(256), Q, k, kout, T, N); break;

@@ -525,8 +525,8 @@ struct rk_solver {
           Cw.push_back(Cs[s]);
           Uw.push_back(Us[s]);
         }
-        rotate(ctx, Cw, dsc + o_T, N);
-        rotate(ctx, Uw, dsc + o_T, N);
+        rotate(ctx, Cw, dsc + o_T, N, -1, hsc + o_T);
+        rotate(ctx, Uw, dsc + o_T, N, -1, hsc + o_T);
         sync();  // the pinned T buffer is reused by the second pass
         break;
       }
@@ -777,8 +777,8 @@ struct rk_solver {
               Uw.push_back(Us[s]);
               Cw.push_back(Cs[s]);
             }
-            rotate(ctx, Uw, dsc + o_T, N, keep);
-            rotate(ctx, Cw, dsc + o_T, N, keep);
+            rotate(ctx, Uw, dsc + o_T, N, keep, hsc + o_T);
+            rotate(ctx, Cw, dsc + o_T, N, keep, hsc + o_T);
             order.resize(keep);
             sync();  // the pinned W buffer is reused
           } else {
@@ -1354,7 +1354,7 @@ rk_status rk_recycle_set(rk_solver* s, int k, const double* U, const double* C, 
       RK_CUDA(cudaMemcpyAsync(s->dsc + s->o_T, s->hsc + s->o_T, sizeof(double) * k * k,
                               cudaMemcpyHostToDevice, s->ctx->stream));
       std::vector<double*> Uw(s->Us.begin(), s->Us.begin() + k);
-      rotate(s->ctx, Uw, s->dsc + s->o_T, s->N);
+      rotate(s->ctx, Uw, s->dsc + s->o_T, s->N, -1, s->hsc + s->o_T);
     }
     s->c_valid = (C != nullptr) || k == 0;
     s->c_kind = s->kind_for(s->method);
@@ -1681,6 +1681,22 @@ rk_status rk_gram_update(rk_ctx* ctx, int ncol, int k, const double* const* Q, c
   });
 }
 
+rk_status rk_project_update(rk_ctx* ctx, int k, const double* const* C, const double* const* U,
+                            const double* xi, double* r, double* x, int64_t n, double* nrm2) {
+  return guarded([&] {
+    kernel_entry(ctx);
+    auto cc = col_list(k, C, 48);
+    std::vector<const double*> uu;
+    if (x) {
+      RK_REQUIRE(U, RK_EINVAL, "U needed with x");
+      uu = col_list(k, U, 48);
+    }
+    RK_REQUIRE(xi && r && nrm2 && n >= 1, RK_EINVAL, "NULL argument or n < 1");
+    proj(ctx, cc, uu, xi, r, x, n, nrm2);
+    kernel_done(ctx);
+  });
+}
+
 rk_status rk_normalize(rk_ctx* ctx, double* w, int64_t n, const double* nrm2, const double* nin2,
                        double* flag) {
   return guarded([&] {
@@ -1717,7 +1733,9 @@ rk_status rk_rotate(rk_ctx* ctx, int k, double* const* Q, const double* T, int k
     RK_REQUIRE(Q && T && n >= 1 && k >= 1 && k <= MAXCOL, RK_EINVAL, "NULL argument, n < 1 or bad k");
     std::vector<double*> cols(Q, Q + k);
     for (auto p : cols) RK_REQUIRE(p, RK_EINVAL, "NULL column pointer");
-    rotate(ctx, cols, T, n, kout);
+    std::vector<double> Th((size_t)k * k);
+    RK_CUDA(cudaMemcpy(Th.data(), T, sizeof(double) * k * k, cudaMemcpyDeviceToHost));
+    rotate(ctx, cols, T, n, kout, Th.data());
     kernel_done(ctx);
   });
 }

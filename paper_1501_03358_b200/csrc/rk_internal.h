@@ -346,7 +346,10 @@ void proj(rk_ctx* ctx, const std::vector<const double*>& C, const std::vector<co
           const double* xi, double* r, double* x, int64_t N, double* red_out);
 // [q_0 .. q_{k-1}] <- [q_0 .. q_{k-1}] T in place, T k x kout (column-major),
 // outputs into the first kout columns (kout = -1: square).
-void rotate(rk_ctx* ctx, const std::vector<double*>& cols, const double* T, int64_t N, int kout = -1);
+// T: DEVICE k x k column-major; T_host (same matrix on the host), when given,
+// is passed in the kernel's parameter space instead (rotate_cb_kernel)
+void rotate(rk_ctx* ctx, const std::vector<double*>& cols, const double* T, int64_t N, int kout = -1,
+            const double* T_host = nullptr);
 // also decides whether iteration `cur` runs at all (lookahead): it stops when
 // the previous iteration ended the loop (flag / sigma), converged
 // (||r|| <= thr_conv), diverged (||r|| > thr_div) or rho == 0; cur->stop gates

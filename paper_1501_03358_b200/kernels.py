@@ -66,6 +66,15 @@ def gram_update(ctx, Q, k, g, grow, w):
     return h, nrm2
 
 
+def project_update(ctx, C, U, xi, r, x=None):
+    """Line 1b / D20: r <- r - C xi, x <- x + U xi (x optional) in place;
+    returns ||r_new||^2."""
+    nrm2 = _dev(1, r)
+    L.check(L.lib().rk_project_update(ctx.h, len(C), _ptrs(C), _ptrs(U) if x is not None else None,
+                                      _p(xi), _p(r), _p(x), r.numel(), _p(nrm2)), "rk_project_update")
+    return nrm2
+
+
 def normalize(ctx, w, nrm2, nin2=None):
     """Alg. 3 line 10 in place; returns the breakdown flag tensor."""
     flag = _dev(1, w)

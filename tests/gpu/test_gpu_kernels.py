@@ -425,3 +425,25 @@ def test_gram_update_bulk_bitwise(rk, kern, n, ncol, k, monkeypatch):
     rh, rw, rnn = K.gram_update(Qh, k, g, grow, w)
     check_vec(out["2"][0], rw, abs_update_terms(Qh, rh, w))
     assert abs(out["2"][2] - rnn) <= TOL * rnn
+
+
+@pytest.mark.parametrize("n", SIZES)
+@pytest.mark.parametrize("k", [1, 20, 30, 48])
+@pytest.mark.parametrize("with_x", [True, False])
+def test_project_update(kern, ctx, n, k, with_x):
+    """Line 1b / D20 (the bulk-copy pair of block updates at large n, the
+    row-interleaved kernel below)."""
+    Ch, C = cols(n, k, 1000 + k)
+    Uh, U = cols(n, k, 2000 + k)
+    rng = np.random.default_rng(3000 + k)
+    xi = rng.uniform(-1, 1, k)
+    r, x = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+    rd, xd = dev(r), dev(x)
+    nrm2 = kern.project_update(ctx, C, U, dev(xi), rd, xd if with_x else None)
+    rr, rx, rnn = K.project_update(Ch, Uh, xi, r, x if with_x else None)
+    check_vec(host(rd), rr, abs_update_terms(Ch, xi, r))
+    if with_x:
+        check_vec(host(xd), rx, abs_update_terms(Uh, xi, x))
+    else:
+        assert np.array_equal(host(xd), x)
+    assert abs(host(nrm2)[0] - rnn) <= TOL * rnn

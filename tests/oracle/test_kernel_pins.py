@@ -203,3 +203,17 @@ def test_bicg_kernels_compose_to_rbicgstab(k):
             assert np.linalg.norm(xi - h["xi"]) <= 1e-12 * np.linalg.norm(h["xi"])
         prev = dict(cur)
         cur = dict(rho=rho_n, rr=rr_n)
+
+
+def test_project_update_exact_rational():
+    C, r = _rand(7, 3, 12)
+    U, x = _rand(7, 3, 13)
+    xi = np.random.default_rng(14).uniform(-1, 1, 3)
+    rn, xn, nn = K.project_update(C, U, xi, r, x)
+    for i in range(7):
+        er = Fraction(float(r[i])) - sum(Fraction(float(xi[c])) * Fraction(float(C[c][i])) for c in range(3))
+        ex = Fraction(float(x[i])) + sum(Fraction(float(xi[c])) * Fraction(float(U[c][i])) for c in range(3))
+        assert abs(rn[i] - float(er)) <= 1e-15 * 4 and abs(xn[i] - float(ex)) <= 1e-15 * 4
+    assert abs(nn - _exact_dot(rn, rn)) <= 1e-15 * nn
+    rn2, xn2, _ = K.project_update(C, U, xi, r)
+    assert xn2 is None and np.array_equal(rn2, rn)
