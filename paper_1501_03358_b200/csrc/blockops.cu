@@ -951,10 +951,11 @@ __global__ void __launch_bounds__(256) rotate_cb_kernel(ColPtrs Qc, int k, int k
   const int64_t NE = N / VEC;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < NE; e += stride) {
     const int64_t n = e * VEC;
+    // columns c >= k are column 0 again with T(c, o) = 0 (host padding): the
+    // FMA chain needs no per-term predicate (x * 0 adds an exact zero)
     Vec<VEC> in[NC];
 #pragma unroll
-    for (int c = 0; c < NC; ++c)
-      if (c < k) in[c] = ldv<VEC>(Qc.p[c] + n);
+    for (int c = 0; c < NC; ++c) in[c] = ldv<VEC>(Qc.p[c] + n);
 #pragma unroll
     for (int o = 0; o < NC; ++o) {
       if (o < kout) {
@@ -963,10 +964,8 @@ __global__ void __launch_bounds__(256) rotate_cb_kernel(ColPtrs Qc, int k, int k
         for (int t = 0; t < VEC; ++t) s.v[t] = 0.0;
 #pragma unroll
         for (int c = 0; c < NC; ++c)
-          if (c < k) {
 #pragma unroll
-            for (int t = 0; t < VEC; ++t) s.v[t] = fma(in[c].v[t], T.t[o * NC + c], s.v[t]);
-          }
+          for (int t = 0; t < VEC; ++t) s.v[t] = fma(in[c].v[t], T.t[o * NC + c], s.v[t]);
         stv<VEC>(const_cast<double*>(Qc.p[o]) + n, s);
       }
     }
@@ -1343,14 +1342,20 @@ void proj(rk_ctx* ctx, const std::vector<const double*>& C, const std::vector<co
 
 namespace {
 template <int NC>
-void launch_rotate_cb(rk_ctx* ctx, const ColPtrs& Q, int k, int kout, const double* Th, int64_t N, bool vec2) {
+void launch_rotate_cb(rk_ctx* ctx, ColPtrs Q, int k, int kout, const double* Th, int64_t N, bool vec2) {
+  for (int c = k; c < NC; ++c) Q.p[c] = Q.p[0];
   TMat<NC> tm;
   memset(&tm, 0, sizeof(tm));
   for (int o = 0; o < kout; ++o)
     for (int c = 0; c < k; ++c) tm.t[o * NC + c] = Th[(size_t)o * k + c];
   // two cells per thread while the k inputs fit the registers
-  if (vec2 && NC <= 32) launch_k(ctx, rotate_cb_kernel<NC, 2>, N / 2, dim3(256), Q, k, kout, tm, N);
-  else launch_k(ctx, rotate_cb_kernel<NC, 1>, N, dim3(256), Q, k, kout, tm, N);
+  if constexpr (NC <= 32) {
+    if (vec2) {
+      launch_k(ctx, rotate_cb_kernel<NC, 2>, N / 2, dim3(256), Q, k, kout, tm, N);
+      return;
+    }
+  }
+  launch_k(ctx, rotate_cb_kernel<NC, 1>, N, dim3(256), Q, k, kout, tm, N);
 }
 }  // namespace
 
