@@ -1734,7 +1734,8 @@ rk_status rk_rotate(rk_ctx* ctx, int k, double* const* Q, const double* T, int k
     std::vector<double*> cols(Q, Q + k);
     for (auto p : cols) RK_REQUIRE(p, RK_EINVAL, "NULL column pointer");
     std::vector<double> Th((size_t)k * k);
-    RK_CUDA(cudaMemcpy(Th.data(), T, sizeof(double) * k * k, cudaMemcpyDeviceToHost));
+    RK_CUDA(cudaMemcpyAsync(Th.data(), T, sizeof(double) * k * k, cudaMemcpyDeviceToHost, ctx->stream));
+    RK_CUDA(cudaStreamSynchronize(ctx->stream));   // T may come from work queued on the context stream
     rotate(ctx, cols, T, n, kout, Th.data());
     kernel_done(ctx);
   });
