@@ -181,6 +181,13 @@ __device__ __forceinline__ bool bk_try(uint64_t* b, uint32_t parity) {
 }  // namespace
 
 constexpr int BK_ROWS = 2048, BK_SLOTS = 8, BK_BYTES = BK_ROWS * 8;
+// columns per two-right-hand-side bulk launch (2 x 40 accumulators per thread
+// at one CTA per SM; wider [C V_j] is split into balanced launches, each
+// re-reading w and v)
+#ifndef RK_BK_MAXC2
+#define RK_BK_MAXC2 40
+#endif
+constexpr int BK_MAXC2 = RK_BK_MAXC2;
 constexpr size_t BK_SMEM = (size_t)BK_SLOTS * BK_BYTES + BK_SLOTS * sizeof(uint64_t);
 
 // NR = 1: Q^T w; NR = 2: [Q^T w, Q^T v] (values NC.. for v, as bdot2_tile_kernel)
@@ -1171,12 +1178,12 @@ void bdot2(rk_ctx* ctx, const std::vector<const double*>& cols_all, const double
     bdot(ctx, cols_all, v, N, out_v);
     return;
   }
-  // bulk-copy path: launches of up to 32 columns (one CTA per SM leaves
-  // registers for 64 accumulators), balanced (72 columns: 3 x 24; each
-  // launch re-reads w and v, 2 W), else <= 24 columns per tiled launch
+  // bulk-copy path: launches of up to BK_MAXC2 columns, balanced (71
+  // columns: 2 x 36; each launch re-reads w and v, 2 W), else <= 24 columns
+  // per tiled launch
   if (ctx->bdot_bulk == 2 ||
       (ctx->bdot_bulk == 1 && total >= 4 && N >= (int64_t)BK_ROWS * ctx->sms)) {
-    const int nch = (total + 31) / 32;
+    const int nch = (total + BK_MAXC2 - 1) / BK_MAXC2;
     const int per = (total + nch - 1) / nch;
     for (int off = 0; off < total; off += per) {
       const int ncol = std::min(per, total - off);
@@ -1192,7 +1199,8 @@ void bdot2(rk_ctx* ctx, const std::vector<const double*>& cols_all, const double
         case 8: launch_bulk(ctx, bdot_bulk_kernel<8, 2>, Q, ncol, w, v, N, ra); break;
         case 16: launch_bulk(ctx, bdot_bulk_kernel<16, 2>, Q, ncol, w, v, N, ra); break;
         case 24: launch_bulk(ctx, bdot_bulk_kernel<24, 2>, Q, ncol, w, v, N, ra); break;
-        default: launch_bulk(ctx, bdot_bulk_kernel<32, 2>, Q, ncol, w, v, N, ra); break;
+        case 32: launch_bulk(ctx, bdot_bulk_kernel<32, 2>, Q, ncol, w, v, N, ra); break;
+        default: launch_bulk(ctx, bdot_bulk_kernel<40, 2>, Q, ncol, w, v, N, ra); break;
       }
       L.done();
       allreduce2(ctx, out_w + off, ncol, out_v + off, ncol);
