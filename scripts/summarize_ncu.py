@@ -29,6 +29,8 @@ def cls_of(name, grid=None):
     m = re.search(r"chain_kernel(_x2)?<(\d+), (\d+)", name)
     if m:
         return "chain"
+    if "rotate_cb_kernel" in name:
+        return "rotate"
     for k in ("bdot2", "bupd_gram", "bproj_s", "bdot", "bupd", "normalize", "lincomb", "proj", "rotate", "bicg_p", "bicg_s",
               "bicg_xr", "bicg_setup", "validate", "chain", "invdiag", "colour_sweep"):
         if re.search(rf"\b{k}_(tile_|bulk_)?kernel\b", name):
