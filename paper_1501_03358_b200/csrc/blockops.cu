@@ -189,6 +189,12 @@ constexpr int BK_ROWS = 2048, BK_SLOTS = 8, BK_BYTES = BK_ROWS * 8;
 #endif
 constexpr int BK_MAXC2 = RK_BK_MAXC2;
 constexpr size_t BK_SMEM = (size_t)BK_SLOTS * BK_BYTES + BK_SLOTS * sizeof(uint64_t);
+// ring slots of the bulk block update (read-modify-write of w)
+#ifndef RK_BU_SLOTS
+#define RK_BU_SLOTS 8
+#endif
+constexpr int BU_SLOTS = RK_BU_SLOTS;
+constexpr size_t BU_SMEM = (size_t)BU_SLOTS * BK_BYTES + BU_SLOTS * sizeof(uint64_t);
 
 // NR = 1: Q^T w; NR = 2: [Q^T w, Q^T v] (values NC.. for v, as bdot2_tile_kernel)
 template <int NC, int NR>
@@ -464,7 +470,7 @@ __global__ void __launch_bounds__(256, 1) bupd_gram_bulk_kernel(ColPtrs Q, int n
   RK_PDL_ENTRY();
   extern __shared__ __align__(128) unsigned char bk_sm[];
   double2* ring = reinterpret_cast<double2*>(bk_sm);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(bk_sm + (size_t)BK_SLOTS * BK_BYTES);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(bk_sm + (size_t)BU_SLOTS * BK_BYTES);
   __shared__ double gs[MAXCOL], hs[MAXCOL];
   constexpr int RV = BK_ROWS / 512;
   const int64_t ntile = N / BK_ROWS;
@@ -489,10 +495,10 @@ __global__ void __launch_bounds__(256, 1) bupd_gram_bulk_kernel(ColPtrs Q, int n
         : "memory");
   };
   if (threadIdx.x == 0) {
-    for (int q = 0; q < BK_SLOTS; ++q)
+    for (int q = 0; q < BU_SLOTS; ++q)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bk_smem(bar + q)) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int q = 0; q < BK_SLOTS && q < nitem; ++q) issue(q);
+    for (int q = 0; q < BU_SLOTS && q < nitem; ++q) issue(q);
   }
   // h = 2 g - G g (bupd_gram_kernel's prologue, same FMA order)
   for (int c = threadIdx.x; c < MAXCOL; c += blockDim.x) gs[c] = c < ncol ? g[c] : 0.0;
@@ -521,9 +527,9 @@ __global__ void __launch_bounds__(256, 1) bupd_gram_bulk_kernel(ColPtrs Q, int n
   int64_t it = 0;
   auto next = [&]() {
     __syncthreads();   // every thread is done with the slot
-    if (threadIdx.x == 0 && it + BK_SLOTS < nitem) issue(slot);
+    if (threadIdx.x == 0 && it + BU_SLOTS < nitem) issue(slot);
     ++it;
-    if (++slot == BK_SLOTS) {
+    if (++slot == BU_SLOTS) {
       slot = 0;
       phase ^= 1;
     }
@@ -983,14 +989,18 @@ __global__ void __launch_bounds__(256) rotate_cb_kernel(ColPtrs Qc, int k, int k
 namespace {
 // one CTA per SM (the ring fills the shared memory), grid = #SMs
 template <typename... KArgs, typename... Args>
-int launch_bulk(rk_ctx* ctx, void (*kern)(KArgs...), Args&&... args) {
+int launch_bulk_smem(rk_ctx* ctx, size_t smem, void (*kern)(KArgs...), Args&&... args) {
   auto it = ctx->occ_cache.find((const void*)kern);
   if (it == ctx->occ_cache.end()) {
-    RK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BK_SMEM));
+    RK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     ctx->occ_cache[(const void*)kern] = 1;
   }
-  launch_pdl(ctx, kern, dim3(ctx->sms), dim3(256), BK_SMEM, std::forward<Args>(args)...);
+  launch_pdl(ctx, kern, dim3(ctx->sms), dim3(256), smem, std::forward<Args>(args)...);
   return ctx->sms;
+}
+template <typename... KArgs, typename... Args>
+int launch_bulk(rk_ctx* ctx, void (*kern)(KArgs...), Args&&... args) {
+  return launch_bulk_smem(ctx, BK_SMEM, kern, std::forward<Args>(args)...);
 }
 }  // namespace
 // One block-dot launch over <= 40 columns; returns its grid (the number of
@@ -1239,7 +1249,7 @@ void bupd_gram(rk_ctx* ctx, const std::vector<const double*>& cols, int k, const
   // bulk-copy form at large N (>= 16 ring tiles per SM: the ring's fill and
   // drain are amortised); RK_BUPD_BULK: 0 never, 2 always
   if (ctx->bupd_bulk == 2 || (ctx->bupd_bulk == 1 && N >= (int64_t)BK_ROWS * ctx->sms * 16)) {
-    launch_bulk(ctx, bupd_gram_bulk_kernel, Q, ncol, k, g, grow, 1.0, hout, w, N, ra);
+    launch_bulk_smem(ctx, BU_SMEM, bupd_gram_bulk_kernel, Q, ncol, k, g, grow, 1.0, hout, w, N, ra);
     L.done();
     allreduce(ctx, red_out, 1);
     return;
@@ -1319,11 +1329,11 @@ void proj(rk_ctx* ctx, const std::vector<const double*>& C, const std::vector<co
   if (vec == 2 && ctx->bupd_bulk != 0 &&
       (ctx->bupd_bulk == 2 || N >= (int64_t)BK_ROWS * ctx->sms * 16)) {
     Launch L(ctx, "proj", 8.0 * N * (k * (x ? 2 : 1) + 2 + (x ? 2 : 0)));
-    launch_bulk(ctx, bupd_gram_bulk_kernel, Cp, k, 0, xi, (const double*)nullptr, 1.0, (double*)nullptr, r, N,
+    launch_bulk_smem(ctx, BU_SMEM, bupd_gram_bulk_kernel, Cp, k, 0, xi, (const double*)nullptr, 1.0, (double*)nullptr, r, N,
                 ra);
     if (x) {
       RedArgs none = red_args(ctx, nullptr);
-      launch_bulk(ctx, bupd_gram_bulk_kernel, Up, k, 0, xi, (const double*)nullptr, -1.0, (double*)nullptr, x,
+      launch_bulk_smem(ctx, BU_SMEM, bupd_gram_bulk_kernel, Up, k, 0, xi, (const double*)nullptr, -1.0, (double*)nullptr, x,
                   N, none);
     }
     L.done();
