@@ -786,8 +786,8 @@ __global__ void __launch_bounds__(256) bproj_s_kernel(ColPtrs Q, int k, double* 
   block_reduce_store<1>(acc, 1, ra);
 }
 
-// v_{j+1} = w / h_{j+1,j}, with the happy-breakdown test h <= 1e-14 ||A_hat v_j||
-// (reading D18): on breakdown v_{j+1} = 0 and *flag = 1.
+// v_{j+1} = w / h_{j+1,j} (as w * (1 / h)), with the happy-breakdown test
+// h <= 1e-14 ||A_hat v_j|| (reading D18): on breakdown v_{j+1} = 0 and *flag = 1.
 template <int VEC>
 __global__ void __launch_bounds__(256) normalize_kernel(double* __restrict__ w, int64_t N,
                                                         const double* nrm2, const double* nin2,
@@ -807,12 +807,15 @@ __global__ void __launch_bounds__(256) normalize_kernel(double* __restrict__ w, 
   const double h = sqrt(*nrm2);
   bool brk = false;
   if (nin2) brk = !(h > 1e-14 * sqrt(*nin2));
+  // v = w * (1 / h): one division per thread (the fused chain19 launch that
+  // folds line 10 in applies the same product, so both paths store the same v)
+  const double inv = brk ? 0.0 : 1.0 / h;
   for (; e < NE; e += U * stride) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       if (e + u * stride < NE) {
 #pragma unroll
-        for (int t = 0; t < VEC; ++t) v[u].v[t] = brk ? 0.0 : v[u].v[t] / h;
+        for (int t = 0; t < VEC; ++t) v[u].v[t] = v[u].v[t] * inv;
         stv<VEC>(w + (e + u * stride) * VEC, v[u]);
       }
     }

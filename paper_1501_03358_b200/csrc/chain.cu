@@ -58,6 +58,9 @@
 #ifndef RK_C19_ALLLANES
 #define RK_C19_ALLLANES 1   // 19-point chain: stage 0 unconditional in every lane (no branch around the carried registers)
 #endif
+#ifndef RK_C19_XREG
+#define RK_C19_XREG 1   // 19-point chain, folded normalisation: scale input values in registers (1) or the tile in shared memory (0)
+#endif
 #ifndef RK_C19_INVD
 #define RK_C19_INVD 0   // 19-point chain: 1/D recomputed (0) or streamed as a 20th band (1)
 #endif
@@ -749,7 +752,7 @@ int chain_max_stages(const rk_op* op) {
 
 void chain_launch(rk_op* op, int nst, const int* kinds, const double* omegas, const double* xin,
                   const double* r, double* out_t, double* out_mid, double* out, const int* local,
-                  int zb) {
+                  int zb, const XScale* xs) {
   rk_ctx* ctx = op->ctx;
   const int ci = cfg_index();
   const TileCfg tc = CFGS[ci];
@@ -776,11 +779,19 @@ void chain_launch(rk_op* op, int nst, const int* kinds, const double* omegas, co
   cp.zg0 = (int)op->g.z0;
   cp.gate = ctx->gate;
   for (int s = 0; s < nst; ++s) cp.local[s] = local ? local[s] : 0;
+  if (xs) {
+    RK_REQUIRE(op->S == 19 && kinds[0] == CK_SPMV1 && xs->n2 && xs->out, RK_EINVAL,
+               "input normalisation needs the 19-point chain with stage 0 = A v");
+    cp.xs_n2 = xs->n2;
+    cp.xs_in2 = xs->in2;
+    cp.xs_out = xs->out;
+    cp.xs_flag = xs->flag;
+  }
   dim3 grid((unsigned)(op->g.nx / tc.tx), (unsigned)(op->g.ny / tc.ty), 1);   // z: launch_one
   // algorithmic bytes: bands once + stage-0 input + rhs (if any) + outputs (the
   // 1/D array is an implementation choice -- flops for bytes -- and not counted)
   const double words = op->S + 1 + ((kinds[0] != CK_SPMV1) ? 1 : 0) + 1 + (out_t ? 1 : 0) +
-                       (out_mid ? 1 : 0);
+                       (out_mid ? 1 : 0) + (xs ? 1 : 0);
   Launch L(ctx, op->S == 19 ? "chain19" : "chain", 8.0 * op->N * words);
   if (op->S == 19) chain19_dispatch(op, nst, kinds, cp);
   else if (nst == 3) chain_dispatch_cfg<3>(ci, op, kinds, cp, grid);
@@ -789,9 +800,11 @@ void chain_launch(rk_op* op, int nst, const int* kinds, const double* omegas, co
   L.done();
 }
 
+bool chain_scales_input(const rk_op* op) { return op->S == 19 && chain_max_stages(op) > 0; }
+
 void chain_run(rk_op* op, const std::vector<int>& kinds, const std::vector<double>& om,
                const double* xin, const double* r, double* out_t, double* out_mid, double* out,
-               double* za, double* zb, const std::vector<int>& local, int zbs) {
+               double* za, double* zb, const std::vector<int>& local, int zbs, const XScale* xs) {
   const int n = (int)kinds.size();
   // TMA tensor maps need 16-byte aligned bases and the x-pair stores 16-byte
   // aligned outputs; a caller's misaligned vector (rk_precond_apply accepts
@@ -799,6 +812,8 @@ void chain_run(rk_op* op, const std::vector<int>& kinds, const std::vector<doubl
   auto al16 = [](const void* p) { return p == nullptr || ((uintptr_t)p & 15u) == 0; };
   const bool aligned = al16(xin - GHOST * op->P) && al16(r) && al16(out_t) && al16(out_mid) && al16(out);
   const int nmax = aligned ? chain_max_stages(op) : 0;
+  RK_REQUIRE(!xs || (nmax > 0 && op->S == 19 && kinds[0] == CK_SPMV1 && al16(xs->out)), RK_EINVAL,
+             "input normalisation needs the fused 19-point chain");
   std::vector<int> loc(n, 0);
   for (int q = 0; q < n && q < (int)local.size(); ++q) loc[q] = local[q];
   double* bufs[2] = {za, zb};
@@ -838,7 +853,7 @@ void chain_run(rk_op* op, const std::vector<int>& kinds, const std::vector<doubl
     comm_group_end(op->ctx);
     chain_launch(op, len, kinds.data() + a, om.data() + a, cur, rhs,
                  (kinds[a] == CK_SPMV1) ? out_t : nullptr, last ? out_mid : nullptr, dst,
-                 loc.data() + a, zbs);
+                 loc.data() + a, zbs, i == 0 ? xs : nullptr);
     cur = dst;
     a += len;
   }

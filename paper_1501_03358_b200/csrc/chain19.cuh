@@ -195,6 +195,27 @@ chain19_kernel(const __grid_constant__ CUtensorMap mbM, const __grid_constant__ 
     }
   };
 
+  // Arnoldi line 10 folded in (ChainParams::xs_*): the input tiles hold w;
+  // each is scaled by 1 / h in shared memory once, after its TMA lands and a
+  // step before its first read (normalize_kernel's arithmetic, so every
+  // value the stages read is the v_{j+1} that kernel would have stored)
+  const bool xsc = (K0 == CK_SPMV1) && cp.xs_n2 != nullptr;
+  double xs_inv = 1.0;
+  if (xsc) {
+    const double h = sqrt(*cp.xs_n2);
+    const bool brk = cp.xs_in2 && !(h > 1e-14 * sqrt(*cp.xs_in2));
+    xs_inv = brk ? 0.0 : 1.0 / h;
+    if (cp.xs_flag && tid == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
+      *cp.xs_flag = brk ? 1.0 : 0.0;
+  }
+  auto scale_x = [&](int xs) {   // input-tile slot xs: regions L, M, R
+    double* xb = reinterpret_cast<double*>(smem + G::XBASE + xs * G::XSLOT);
+    constexpr int NL = G::XROWS * HW, NM = G::XROWS * TX;
+    for (int i = tid; i < NM; i += G::NTHR) xb[G::X_M / 8 + i] *= xs_inv;
+    if (tid < 2 * NL) xb[tid < NL ? tid : G::X_R / 8 + (tid - NL)] *= xs_inv;
+  };
+  static_assert(2 * G::XROWS * G::HW <= G::NTHR, "one halo-region value per thread");
+
   if (tid == 0) {
     for (int s = 0; s < NXB + NB; ++s) mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -208,6 +229,20 @@ chain19_kernel(const __grid_constant__ CUtensorMap mbM, const __grid_constant__ 
   }
   mbar_wait(&bars[0], 0);
   mbar_wait(&bars[1], 0);
+  // RK_C19_XREG (with the carried neighbourhoods, ROT0): the scale is applied
+  // to each input value as it is loaded into registers (every input value
+  // stage 0 uses passes through xcm / xcc / xn / a0 / p0 / nb), not by a pass
+  // over the tile in shared memory
+  constexpr bool XREG = RK_C19_XREG && (RK_C19_ROT & 1) && K0 == CK_SPMV1;
+  if (!XREG && xsc) {   // planes qfirst .. qfirst + 2: the tiles step tau0 reads
+    scale_x(0);
+    scale_x(1);
+    if (qfirst + 2 <= qlast) {
+      mbar_wait(&bars[2], 0);
+      scale_x(2);
+    }
+    __syncthreads();
+  }
   // Input-tile slots are compile-time: the step loop is unrolled 8 times and
   // plane tau - tau0 = 8 it + U reads tiles of planes tau-1, tau, tau+1 from
   // slots U, U+1, U+2 (mod 8; plane p lives in slot (p - qfirst) & 7), ring
@@ -236,7 +271,9 @@ chain19_kernel(const __grid_constant__ CUtensorMap mbM, const __grid_constant__ 
   }
   // own z-columns: input at planes tau-1, tau (registers); stage 0's outputs
   // at the two planes below the one it produced last
-  double xcm = xbase[xo[1][1]], xcc = xbase[XS + xo[1][1]];   // planes qfirst, tau0: slots 0, 1
+  // (XREG: x * 1.0 when the launch does not normalise -- the same value)
+  const double xm = XREG ? xs_inv : 1.0;
+  double xcm = xbase[xo[1][1]] * xm, xcc = xbase[XS + xo[1][1]] * xm;   // planes qfirst, tau0: slots 0, 1
   double hm = 0.0, hc = 0.0;
   // In-plane neighbourhoods carried in registers from step to step (each
   // tile / ring value is read from shared memory once per thread instead of
@@ -251,12 +288,12 @@ chain19_kernel(const __grid_constant__ CUtensorMap mbM, const __grid_constant__ 
   double a0[8], p0[4], a1[8], p1[4];
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
-    a0[e] = ROT0 ? xbase[XS + xn8[e]] : 0.0;
+    a0[e] = ROT0 ? xbase[XS + xn8[e]] * xm : 0.0;
     a1[e] = 0.0;
   }
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
-    p0[e] = ROT0 ? xbase[xn8[e]] : 0.0;
+    p0[e] = ROT0 ? xbase[xn8[e]] * xm : 0.0;
     p1[e] = 0.0;
   }
 
@@ -298,9 +335,9 @@ chain19_kernel(const __grid_constant__ CUtensorMap mbM, const __grid_constant__ 
         cut_m = (g % cp.zb) == 0;                                                                 \
         cut_p = ((g + 1) % cp.zb) == 0;                                                           \
       }                                                                                           \
-      const double xn = tp[xo[1][1]];                                                             \
+      const double xn = tp[xo[1][1]] * xm;                                                        \
       double nb[8];   /* plane tau+1's neighbours (all 8 when carried, else the 4 edges) */      \
-      _Pragma("unroll") for (int e = 0; e < (ROT0 ? 8 : 4); ++e) nb[e] = tp[xn8[e]];            \
+      _Pragma("unroll") for (int e = 0; e < (ROT0 ? 8 : 4); ++e) nb[e] = tp[xn8[e]] * xm;       \
       double v[19];                                                                               \
       v[0] = xcc;                                                                                 \
       v[1] = ROT0 ? a0[0] : t0[xo[1][0]];                                                         \
@@ -338,12 +375,18 @@ chain19_kernel(const __grid_constant__ CUtensorMap mbM, const __grid_constant__ 
       if (interior && tau >= z0 && tau < z1 && (pz || tau < nz)) {                                \
         const int64_t nn = (int64_t)pl_of(tau) * cp.P + cxy;                                      \
         if (K0 == CK_SPMV1 && cp.out_t) cp.out_t[nn] = y;                                         \
+        if (xsc && cp.xs_out) cp.xs_out[nn] = xcc;   /* v_{j+1} at plane tau */                   \
         if (NST == 1) cp.out[nn] = v0;                                                            \
         if (NST == 2 && cp.out_mid) cp.out_mid[nn] = v0;                                          \
       }                                                                                           \
       if (NST > 1) ring[((U) & 3) * RP + gofs] = v0;   /* ring slot (tau - tau0) & 3 */          \
       xcm = xcc;                                                                                  \
       xcc = xn;                                                                                   \
+    }                                                                                             \
+    /* normalisation folded in: plane tau+2's tile (slot (U+3)&7), first read at step tau+1 */    \
+    if (!XREG && xsc && tau + 2 <= qlast) {                                                       \
+      mbar_wait(&bars[((U) + 3) & 7], (U) < 5 ? par : par ^ 1u);                                  \
+      scale_x(((U) + 3) & 7);                                                                     \
     }                                                                                             \
     __syncthreads();                                                                              \
     /* the slots of plane tau-1's tile and plane tau's bands / rhs are free */                    \

@@ -285,6 +285,10 @@ struct rk_solver {
   std::vector<double*> Us, Cs;                // k_max + 2 slots each
   std::vector<int> order;                     // recycle space: slot ids, oldest first
   double *x = nullptr, *t = nullptr, *za = nullptr, *zb = nullptr, *rt = nullptr;
+  // Arnoldi line 10 folded into the next step's chain (19-point fused chain):
+  // the normalised v_{j+1} is written here and swapped into V[j+1]
+  double* vspare = nullptr;
+  bool nfuse = true;                          // RK_NFUSE=0 keeps normalize_kernel
   double* bdev = nullptr;                     // for rk_solve_host
   // recycle-space validity: C matches the operator of `c_kind` at `c_epoch`
   bool c_valid = true;
@@ -376,8 +380,21 @@ struct rk_solver {
   // when available, else one stencil launch per stage (same arithmetic).
   void run_chain(const std::vector<int>& kinds, const std::vector<double>& om, const double* xin,
                  const double* r, double* out_t, double* out_mid, double* out,
-                 const std::vector<int>& local = {}) {
-    chain_run(op, kinds, om, xin, r, out_t, out_mid, out, za, zb, local, zblock());
+                 const std::vector<int>& local = {}, const XScale* xs = nullptr) {
+    chain_run(op, kinds, om, xin, r, out_t, out_mid, out, za, zb, local, zblock(), xs);
+  }
+  // Line 10 (v_{j+1} = w / h) inside the first launch of step j+1's A_hat
+  // chain: saves normalize_kernel's read + write of w (1 W net: the chain
+  // stores v_{j+1}) and a launch per Arnoldi step; same arithmetic, so the
+  // results are bit-identical to the unfused step
+  bool fuse_normalize() {
+    if (!nfuse || !jac() || !chain_scales_input(op)) return false;
+    if (!vspare) {
+      double* b;
+      vspare = alloc_padded(op, &b, &nvec);
+      bases.push_back(b);
+    }
+    return true;
   }
   // block-Jacobi: planes per z-block of the local sweeps (0 = all sweeps global) [R17]
   int zblock() const {
@@ -415,7 +432,9 @@ struct rk_solver {
 
   // dst = M^-1 A v  (left-preconditioned operator, Alg. 3 line 6):
   // stages [t = A v, z1 = w_l t/D], sweeps 2..5 (w_l, local), sweep 6 (w_g)
-  void apply_ahat(const double* v, double* dst) {
+  // xs: v is the unnormalised w of the previous Arnoldi step, taken as
+  // w / h by the chain, which also stores v_{j+1} = w / h (fuse_normalize())
+  void apply_ahat(const double* v, double* dst, const XScale* xs = nullptr) {
     if (jac()) {
       std::vector<int> k(cfg.pc.sweeps + 1, CK_SWEEP);
       std::vector<double> w(cfg.pc.sweeps + 1, cfg.pc.omega_local);
@@ -424,7 +443,7 @@ struct rk_solver {
       loc[0] = 0;
       w.back() = cfg.pc.omega_global;
       loc.back() = 0;
-      run_chain(k, w, v, nullptr, t, nullptr, dst, loc);
+      run_chain(k, w, v, nullptr, t, nullptr, dst, loc, xs);
     } else if (ssor()) {
       stencil(op, SM_SPMV, v, nullptr, t, nullptr, 0.0, nullptr);
       ssor_to(t, dst, nullptr);
@@ -615,9 +634,19 @@ struct rk_solver {
       const int k = (int)order.size();
       normalize(ctx, V[0], N, misc(RHO2), nullptr, nullptr);  // line 4: v1 = r / rho
       auto Q = ccols();
+      // line 10 of step j-1 pending in the chain of step j (fuse_normalize)
+      XScale pend{nullptr, nullptr, nullptr, nullptr};
+      const bool fuse = fuse_normalize();
       for (int j = 0; j < m; ++j) {
         double* w = V[j + 1];
-        apply_ahat(V[j], w);                                  // line 6
+        if (pend.n2) {
+          pend.out = vspare;
+          apply_ahat(V[j], w, &pend);                         // lines 10 (step j-1) + 6
+          std::swap(V[j], vspare);                            // v_{j} now in V[j]
+          pend.n2 = nullptr;
+        } else {
+          apply_ahat(V[j], w);                                // line 6
+        }
         Q.push_back(V[j]);
         const int ncol = (int)Q.size();
         double* g1 = arn(j);
@@ -634,7 +663,10 @@ struct rk_solver {
           bupd(ctx, Q, g1, 1.0, w, N, {}, nullptr);
           bproject(ctx, Q, w, N, g2, {nullptr}, g1 + 2 * (MAXCOL + 1));   // CGS pass 2 [D8]
         }
-        normalize(ctx, w, N, g1 + 2 * (MAXCOL + 1), g1 + ncol, g1 + 2 * (MAXCOL + 1) + 1);  // line 10
+        if (fuse && j + 1 < m)   // line 10 runs inside the next step's chain launch
+          pend = XScale{g1 + 2 * (MAXCOL + 1), g1 + ncol, nullptr, g1 + 2 * (MAXCOL + 1) + 1};
+        else
+          normalize(ctx, w, N, g1 + 2 * (MAXCOL + 1), g1 + ncol, g1 + 2 * (MAXCOL + 1) + 1);  // line 10
       }
       fetch(o_arn, STEP * m);
       fetch(o_misc, MISC_XI);
@@ -1288,6 +1320,7 @@ rk_status rk_solver_create(rk_op* op, const rk_config* cfg, rk_solver** out) {
       RK_CUDA(cudaMallocHost(&s->hsc, o * sizeof(double)));
       for (auto& e : s->bev) RK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       if (const char* la = std::getenv("RK_BICG_LOOKAHEAD")) s->lookahead = std::atoi(la) != 0;
+      if (const char* nf = std::getenv("RK_NFUSE")) s->nfuse = std::atoi(nf) != 0;
       std::memset(s->hsc, 0, o * sizeof(double));
       RK_CUDA(cudaStreamSynchronize(s->ctx->stream));
     } catch (...) {

@@ -129,6 +129,24 @@ struct ChainParams {
   const double* gate;   // no-op when *gate != 0 (rBiCGStab lookahead)
   int ghost;            // several ranks: bands of planes outside [0, nz) from the ghost-band map
   int rz;               // z coordinate of plane 0 in the rhs tensor map (GHOST: padded rhs)
+  // Arnoldi line 10 folded into the next line 6 (19-point chain, stage 0 =
+  // CK_SPMV1 only): when xs_n2 != nullptr the input is the unnormalised w and
+  // every input value is taken as w * (1 / h), h = sqrt(*xs_n2) (0 on the
+  // happy breakdown h <= 1e-14 sqrt(*xs_in2)) -- normalize_kernel's
+  // arithmetic; v_{j+1} of the interior cells goes to xs_out, the breakdown
+  // flag to *xs_flag.
+  const double* xs_n2;
+  const double* xs_in2;
+  double* xs_out;
+  double* xs_flag;
+};
+
+// The normalisation a chain launch applies to its input (ChainParams::xs_*).
+struct XScale {
+  const double* n2;
+  const double* in2;
+  double* out;
+  double* flag;
 };
 
 // Per-iteration device scalars of rBiCGStab (one 64-byte record per iteration).
@@ -302,14 +320,18 @@ void launch_pdl(rk_ctx* ctx, void (*kern)(KArgs...), dim3 grid, dim3 blk, size_t
 int chain_max_stages(const rk_op* op);
 void chain_launch(rk_op* op, int nst, const int* kinds, const double* omegas, const double* xin,
                   const double* r, double* out_t, double* out_mid, double* out,
-                  const int* local = nullptr, int zb = 0);
+                  const int* local = nullptr, int zb = 0, const XScale* xs = nullptr);
+// true when chain_run can take an XScale (the first launch is a fused 19-point
+// chain launch with stage 0 = CK_SPMV1)
+bool chain_scales_input(const rk_op* op);
 // Runs n chained stencil stages; fused (TMA) launches of up to chain_max_stages()
 // stages when available, else one stencil launch per stage.  za/zb: padded scratch.
 // local[q] != 0: stage q is a local sweep of the block-Jacobi preconditioner
 // (couplings across z-blocks of zbs planes dropped; reading R17).
 void chain_run(rk_op* op, const std::vector<int>& kinds, const std::vector<double>& om,
                const double* xin, const double* r, double* out_t, double* out_mid, double* out,
-               double* za, double* zb, const std::vector<int>& local = {}, int zbs = 0);
+               double* za, double* zb, const std::vector<int>& local = {}, int zbs = 0,
+               const XScale* xs = nullptr);
 
 // ------------------------------------------------------------ launch layer
 // All kernels are launched through these wrappers (stencil.cu, blockops.cu, bicg.cu).  Each

@@ -259,6 +259,38 @@ def test_chain19_solver_paths_bitwise(rk, ctx, monkeypatch):
     compare_sequences(w, g1, ora, w.params.method)
 
 
+def test_chain19_folded_normalisation_bitwise(rk, ctx, monkeypatch):
+    """Arnoldi line 10 (v_{j+1} = w / h, PAPER Alg. 3) folded
+    into the first 19-point chain launch of the next step's A_hat v: the
+    same iterates, recycle space and per-cycle H, B, y, bit for bit, as
+    with normalize_kernel (RK_NFUSE=0), and m - 1 fewer normalize launches
+    per rGCROT cycle."""
+    w = get_workload("c2m")
+    monkeypatch.setenv("RK_FORCE_CHAIN", "1")
+    runs = []
+    for nf in ("1", "0"):
+        monkeypatch.setenv("RK_NFUSE", nf)
+        ctx.profile(True)
+        ctx.profile_read(reset=True)
+        g, sp = gpu_sequence(rk, ctx, w, solver_name="rgcrot")
+        prof = ctx.profile_read()
+        ctx.profile(False)
+        ctx.profile_read(reset=True)
+        runs.append((g, sp, prof))
+    monkeypatch.delenv("RK_NFUSE")
+    monkeypatch.delenv("RK_FORCE_CHAIN")
+    (g1, sp1, p1), (g2, sp2, p2) = runs
+    for (r1, x1), (r2, x2) in zip(g1, g2):
+        assert r1["krylov_matvecs"] == r2["krylov_matvecs"] and r1["outcome"] == r2["outcome"]
+        assert np.array_equal(x1, x2)
+    assert np.array_equal(sp1[0], sp2[0]) and np.array_equal(sp1[1], sp2[1])
+    cycles = sum(r["cycles_or_iters"] for r, _ in g1)
+    m = w.params.m
+    n1 = p1.get("normalize", {}).get("launches", 0)
+    n2 = p2.get("normalize", {}).get("launches", 0)
+    assert n2 - n1 == cycles * (m - 1), (n1, n2, cycles)
+
+
 # Block-Jacobi preconditioner (SURVEY §8(f) row 2, reading R17): the local
 # sweeps drop every coupling between z-blocks.  Unfused and fused (chain) paths.
 @pytest.mark.parametrize("name,mk,zblocks,force", [
