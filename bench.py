@@ -224,11 +224,11 @@ def run_reference(args):
 # Krylov matvecs per system used to turn the oracle's ms per matvec into ms
 # per system in the reference arm (a separate process that cannot see the
 # GPU arm's counts): the mean over systems 5-24 of the c4 rGCROT(40,30) T2
-# run (profiles/r02_bench_c4_rot_bulk.json); GPU and oracle counts agree per system
+# run (profiles/r02_bench_c4_nfuse.json); GPU and oracle counts agree per system
 # within one cycle (tests/gpu/test_gpu_parity.py).  The GPU arm's own
 # cpu_baseline uses the counts of its own timed systems.
-MV_PER_SYSTEM = {"c4": 422.0, "c3": 178.8}
-MV_SOURCE = "mean Krylov matvecs per timed system of the GPU run, profiles/r02_bench_c4_rot_bulk.json"
+MV_PER_SYSTEM = {"c4": 438.0, "c3": 179.5}
+MV_SOURCE = "mean Krylov matvecs per timed system of the GPU run, profiles/r02_bench_c4_nfuse.json"
 
 
 # ------------------------------------------------------------------ GPU arm
