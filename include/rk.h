@@ -350,6 +350,14 @@ rk_status rk_bicg_xr(rk_op* op, double* x, double* r, const double* s, const dou
  * rk_profile_read returns, per class, launches, summed device ms and summed
  * algorithmic bytes. */
 rk_status rk_launch_count(rk_ctx* ctx, int64_t* count);
+/* Collective launches this context has issued so far on several ranks
+ * ("batched so each iteration issues as few collectives as
+ * the algorithm allows"; BASELINE north_star): *allreduces = all-reduce
+ * launches (a group of all-reduces counts once, as NCCL launches it),
+ * *halos = neighbour-exchange launches (one grouped send/recv set; the two
+ * halos of one fused chain launch count once).  Both stay 0 on one rank.
+ * HOST pointers; either may be NULL. */
+rk_status rk_comm_count(rk_ctx* ctx, int64_t* allreduces, int64_t* halos);
 rk_status rk_profile_enable(rk_ctx* ctx, int on, const char* filter);
 /* Bracket only every `every`-th matching launch (>= 1; default 1): a live
  * sample of a kernel class with less event traffic in a timed region. */

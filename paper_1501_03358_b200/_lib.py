@@ -88,6 +88,7 @@ def lib():
         "rk_trace": ([vp, i32, vp, i64, P(i64)], i32),
         "rk_solver_workspace": ([vp, P(i64)], i32),
         "rk_launch_count": ([vp, P(i64)], i32),
+        "rk_comm_count": ([vp, P(i64), P(i64)], i32),
         "rk_profile_enable": ([vp, i32, C.c_char_p], i32),
         "rk_profile_every": ([vp, i32], i32),
         "rk_profile_read": ([vp, i32, vp, vp, vp, vp, P(i32)], i32),
@@ -126,6 +127,7 @@ EXPORTED = ["rk_last_error", "rk_version", "rk_nccl_unique_id", "rk_ctx_create",
             "rk_solver_set_method", "rk_recycle_set", "rk_recycle_dim", "rk_recycle_export",
             "rk_solve", "rk_solve_host", "rk_solve_host_ex", "rk_stage_rhs", "rk_solve_staged",
             "rk_host_sync", "rk_history", "rk_trace", "rk_solver_workspace", "rk_launch_count",
+            "rk_comm_count",
             "rk_profile_enable", "rk_profile_every", "rk_profile_read",
             "rk_block_dot", "rk_block_update", "rk_block_project", "rk_gram_update", "rk_project_update",
             "rk_normalize", "rk_lincomb", "rk_rotate", "rk_bicg_p", "rk_bicg_s",

@@ -4,7 +4,7 @@ PyTorch is used only for device memory, streams and process groups: every
 numeric step of the solvers runs in librk's sm_100a kernels behind the
 C-ABI.  The objects mirror the ABI one to one:
 
-  Context       rk_ctx_create / rk_launch_count / rk_profile_*
+  Context       rk_ctx_create / rk_launch_count / rk_comm_count / rk_profile_*
   GridOperator  rk_op_create / rk_op_apply / rk_precond_apply / rk_op_update_bands
   Solver        rk_solver_create / rk_solve / rk_solve_host(_ex) / rk_solver_set_method /
                 rk_recycle_set / rk_recycle_dim / rk_recycle_export / rk_history
@@ -43,6 +43,12 @@ class Context:
         n = C.c_int64()
         L.check(L.lib().rk_launch_count(self.h, C.byref(n)), "rk_launch_count")
         return n.value
+
+    def comm_count(self):
+        """(all-reduce launches, halo launches) issued so far (0, 0 on one rank)."""
+        a, h = C.c_int64(), C.c_int64()
+        L.check(L.lib().rk_comm_count(self.h, C.byref(a), C.byref(h)), "rk_comm_count")
+        return a.value, h.value
 
     def profile(self, on=True, filter=None, every=1):
         L.check(L.lib().rk_profile_enable(self.h, 1 if on else 0,

@@ -1067,8 +1067,8 @@ void bdot(rk_ctx* ctx, const std::vector<const double*>& cols_all, const double*
     Launch L(ctx, "bdot", 8.0 * N * (ncol + 1));
     bdot_launch(ctx, cols, w, N, red_args(ctx, out + off));
     L.done();
-    allreduce(ctx, out + off, ncol);
   }
+  allreduce(ctx, out, total);   // one collective for all column chunks
 }
 
 void bproject(rk_ctx* ctx, const std::vector<const double*>& cols, double* w, int64_t N,
@@ -1233,8 +1233,9 @@ void bdot2(rk_ctx* ctx, const std::vector<const double*>& cols_all, const double
         default: launch_bulk(ctx, bdot_bulk_kernel<40, 2>, Q, ncol, w, v, N, ra); break;
       }
       L.done();
-      allreduce2(ctx, out_w + off, ncol, out_v + off, ncol);
     }
+    // one collective for all column chunks (out_w / out_v are contiguous over the chunks)
+    allreduce2(ctx, out_w, total, out_v, total);
     return;
   }
   for (int off = 0; off < total; off += 24) {
@@ -1253,8 +1254,8 @@ void bdot2(rk_ctx* ctx, const std::vector<const double*>& cols_all, const double
       default: launch_k(ctx, bdot2_tile_kernel<24>, N / 4, dim3(256), Q, ncol, w, v, N, ra); break;
     }
     L.done();
-    allreduce2(ctx, out_w + off, ncol, out_v + off, ncol);
   }
+  allreduce2(ctx, out_w, total, out_v, total);
 }
 
 void bupd_gram(rk_ctx* ctx, const std::vector<const double*>& cols, int k, const double* g,

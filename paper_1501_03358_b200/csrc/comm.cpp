@@ -163,6 +163,27 @@ void allreduce_local(rk_ctx* ctx, double* buf, int n) {
   } while (0)
 #endif
 
+// Collective-launch accounting (rk_comm_count): what NCCL would launch --
+// one per all-reduce or halo exchange issued outside a group, one per
+// outermost group (a group holding a halo counts as a halo launch).  The
+// in-process rank group counts the same way, so the schedule's collective
+// count per Krylov step is testable on one GPU.
+static void note_collective(rk_ctx* ctx, bool is_halo) {
+  if (ctx->comm_depth > 0) {
+    (is_halo ? ctx->comm_pend_halo : ctx->comm_pend_ar) = true;
+  } else {
+    ++(is_halo ? ctx->n_halo : ctx->n_allreduce);
+  }
+}
+static void note_group(rk_ctx* ctx, int delta) {
+  ctx->comm_depth += delta;
+  if (ctx->comm_depth == 0) {
+    if (ctx->comm_pend_halo) ++ctx->n_halo;
+    else if (ctx->comm_pend_ar) ++ctx->n_allreduce;
+    ctx->comm_pend_halo = ctx->comm_pend_ar = false;
+  }
+}
+
 // Ordering (NCCL): first every rank sends its hi_src up and receives its
 // lo_dst from below, then sends its lo_src down and receives its hi_dst from
 // above; sends/recvs between one pair of ranks are matched in issue order,
@@ -171,6 +192,7 @@ void exchange(rk_op* op, const double* lo_src, const double* hi_src, double* lo_
               size_t count) {
   rk_ctx* ctx = op->ctx;
   if (ctx->nranks == 1) return;
+  note_collective(ctx, true);
   if (ctx->lgrp) return exchange_local(op, lo_src, hi_src, lo_dst, hi_dst, count);
 #ifdef RK_WITH_NCCL
   int up, dn;
@@ -190,6 +212,7 @@ void exchange(rk_op* op, const double* lo_src, const double* hi_src, double* lo_
 // NCCL launch (NCCL groups nest; the outermost end issues them); the
 // in-process rank group runs them one by one as issued.
 void comm_group_begin(rk_ctx* ctx) {
+  if (ctx->nranks > 1) note_group(ctx, +1);
 #ifdef RK_WITH_NCCL
   if (ctx->nranks > 1 && !ctx->lgrp) RK_NCCL(ncclGroupStart());
 #else
@@ -199,9 +222,8 @@ void comm_group_begin(rk_ctx* ctx) {
 void comm_group_end(rk_ctx* ctx) {
 #ifdef RK_WITH_NCCL
   if (ctx->nranks > 1 && !ctx->lgrp) RK_NCCL(ncclGroupEnd());
-#else
-  (void)ctx;
 #endif
+  if (ctx->nranks > 1) note_group(ctx, -1);
 }
 
 // Fill `depth` ghost planes below and above the padded vector v (local
@@ -217,10 +239,11 @@ void halo(rk_op* op, const double* v, int depth) {
 // Several reduction outputs in ONE collective launch: NCCL aggregates the
 // all-reduces of a group (batch each reduction's values).
 void allreduce2(rk_ctx* ctx, double* a, int na, double* b, int nb) {
-  if (ctx->nranks == 1) return;
+  if (ctx->nranks == 1 || na + nb == 0) return;
+  note_collective(ctx, false);
   if (ctx->lgrp) {
-    allreduce_local(ctx, a, na);
-    allreduce_local(ctx, b, nb);
+    if (na) allreduce_local(ctx, a, na);
+    if (nb) allreduce_local(ctx, b, nb);
     return;
   }
 #ifdef RK_WITH_NCCL
@@ -235,6 +258,7 @@ void allreduce2(rk_ctx* ctx, double* a, int na, double* b, int nb) {
 
 void allreduce(rk_ctx* ctx, double* buf, int n) {
   if (ctx->nranks == 1 || n == 0) return;
+  note_collective(ctx, false);
   if (ctx->lgrp) return allreduce_local(ctx, buf, n);
 #ifdef RK_WITH_NCCL
   RK_NCCL(ncclAllReduce(buf, buf, (size_t)n, ncclDouble, ncclSum, ctx->comm, ctx->stream));

@@ -1583,6 +1583,14 @@ rk_status rk_launch_count(rk_ctx* ctx, int64_t* count) {
   });
 }
 
+rk_status rk_comm_count(rk_ctx* ctx, int64_t* allreduces, int64_t* halos) {
+  return guarded([&] {
+    RK_REQUIRE(ctx, RK_EINVAL, "NULL ctx");
+    if (allreduces) *allreduces = ctx->n_allreduce;
+    if (halos) *halos = ctx->n_halo;
+  });
+}
+
 rk_status rk_profile_enable(rk_ctx* ctx, int on, const char* filter) {
   return guarded([&] {
     RK_REQUIRE(ctx, RK_EINVAL, "NULL ctx");

@@ -187,6 +187,11 @@ struct rk_ctx {
   size_t partials_cap = 0;      // doubles
   unsigned* counter = nullptr;
   int64_t launches = 0;
+  // collective launches issued on several ranks (comm.cpp; rk_comm_count): a
+  // group (comm_group_begin/end, allreduce2) counts once, as NCCL launches it
+  int64_t n_allreduce = 0, n_halo = 0;
+  int comm_depth = 0;
+  bool comm_pend_ar = false, comm_pend_halo = false;
   // profiling
   bool prof_on = false;
   std::string prof_filter;
