@@ -238,3 +238,65 @@ def test_full_size_c4_solve_two_slabs_vs_one_rank(rk):
     for x in (x1, x2):
         assert np.linalg.norm(b - A.apply(x)) <= prm.tol * bn * (1 + 1e-6)
     assert np.linalg.norm(x2 - x1) <= 1e-4 * np.linalg.norm(x1)
+
+
+@pytest.mark.parametrize("wname,force,halos_per_op", [("c2m", True, 3), ("c4hs", False, 6)])
+def test_collectives_per_krylov_step(rk, wname, force, halos_per_op, monkeypatch):
+    """SURVEY §8(e) / north_star: "allreduce for every dot product, batched so
+    each iteration issues as few collectives as the algorithm allows".
+    rk_comm_count counts collective launches the way NCCL issues them (a group
+    counts once); on two z-slabs, per system:
+      * rGCROT: 2 all-reduces per Arnoldi step ([C V_j]^T [w v_j] in one
+        collective whatever the column count; ||w||^2) + 3 per cycle
+        (line 1b / true residual / cycle-start norms) + <= 3 per solve;
+      * rBiCGStab: exactly 4 per iteration + 10 per solve, + 6
+        when the space is refreshed first;
+      * halos: one launch per fused 19-point chain launch (3 per
+        preconditioned operator: input and rhs halos grouped), 6 per
+        operator on the unfused path (one plane per stencil application),
+        plus a few per cycle / solve (true residual, M^-1 r, refresh)."""
+    w = get_workload(wname)
+    if force:
+        monkeypatch.setenv("RK_FORCE_CHAIN", "1")
+    prob, prm, T, R = w.problem(), w.params, w.n_systems, 2
+
+    def rank(r):
+        st = torch.cuda.Stream()
+        with torch.cuda.stream(st):
+            ctx, op, z0, z1 = slab_op(rk, prob, r, R, f"coll_{wname}", st, epoch=w.epoch(0))
+            s = rk.Solver(op, rk.config_from_params(prm))
+            rows = []
+            for t in range(T):
+                a0, h0 = ctx.comm_count()
+                rep = rk.solve_sequence(s, lambda q: dev(prob.rhs(q, z0, z1).reshape(-1)), 1, prm.method,
+                                        n_sw=prm.n_sw, epoch_of=w.epoch,
+                                        bands_for_epoch=lambda e: dev(prob.bands(z0, z1, epoch=e)), start=t)[0]
+                a1, h1 = ctx.comm_count()
+                rows.append((rep["tag"], rep["krylov_matvecs"], rep["operator_applications"],
+                             rep["cycles_or_iters"], a1 - a0, h1 - h0))
+            st.synchronize()
+            s.close()
+            op.close()
+            ctx.close()
+            return rows
+
+    res = run_ranks(R, rank)
+    monkeypatch.delenv("RK_FORCE_CHAIN", raising=False)
+    assert res[0] == res[1]
+    tags = set()
+    for tag, mv, oa, cy, a, h in res[0]:
+        tags.add(tag)
+        if tag == "rgcrot":
+            assert mv == prm.m * cy
+            assert 2 * mv + 3 * cy <= a <= 2 * mv + 3 * cy + 3, (tag, mv, cy, a)
+            assert halos_per_op * mv <= h <= halos_per_op * mv + (halos_per_op + 2) * cy + 8, (tag, mv, cy, h)
+        else:
+            assert mv == 2 * cy
+            refreshed = oa > 1
+            assert a == 4 * cy + 10 + (6 if refreshed else 0), (tag, cy, oa, a)
+            assert halos_per_op * mv <= h <= halos_per_op * (mv + oa) + 16, (tag, mv, oa, h)
+    assert tags == {"rgcrot", "rbicgstab"}
+    # one rank: no collectives at all
+    ctx1 = rk.Context(0)
+    assert ctx1.comm_count() == (0, 0)
+    ctx1.close()
