@@ -309,6 +309,7 @@ def run_rk(args):
     clocks = Clocks(local) if rank == 0 else None
     ctx.profile(True, dominant, every=8)
     launches0 = ctx.launches()
+    coll0 = ctx.comm_count()
     barrier()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -318,6 +319,7 @@ def run_rk(args):
     barrier()
     ms = ev0.elapsed_time(ev1)
     launches = ctx.launches() - launches0
+    coll1 = ctx.comm_count()
     prof_dom = ctx.profile_read().get(dominant, {"launches": 0, "ms": 0.0, "bytes": 0.0})
     ctx.profile(False)
     ctx.profile_read(reset=True)
@@ -395,6 +397,10 @@ def run_rk(args):
                      "share_of_step": round(prof_all[dominant]["ms"] / total_ms, 4) if total_ms else None},
         "step_effective_gbs": round(alg_bytes / (total_ms * 1e-3) / 1e9, 1) if total_ms else None,
         "gpu_launches": launches,
+        # collective launches per rank inside the timed region (0 on one GPU)
+        "collectives": {"allreduce": coll1[0] - coll0[0], "halo": coll1[1] - coll0[1],
+                        "allreduce_per_matvec": round((coll1[0] - coll0[0]) / max(1, sum(mv)), 3),
+                        "halo_per_matvec": round((coll1[1] - coll0[1]) / max(1, sum(mv)), 3)},
         "clocks": clk,
         "e2e": e2e,
         "kernel_breakdown": {k: {"ms": round(v["ms"], 3), "launches": v["launches"],
