@@ -31,7 +31,14 @@ for R in Rs:
     nzl = prob.nz // R
     z0 = (prob.nz // 2) if R > 1 else 0
     z0 = min(z0, prob.nz - nzl)
-    bands = torch.from_numpy(prob.bands(z0, z0 + nzl)).cuda()
+    hb = prob.bands(z0, z0 + nzl)
+    if R > 1:                      # cut faces: couplings out of the slab are dropped
+        for d, (_, _, dz) in enumerate(np.asarray(prob.offsets)):
+            if dz < 0:
+                hb[d, 0] = 0.0
+            elif dz > 0:
+                hb[d, -1] = 0.0
+    bands = torch.from_numpy(hb).cuda()
     periodic = prob.periodic if R == 1 else (prob.periodic & ~4)
     op = rk.GridOperator(ctx, prob.nx, prob.ny, nzl, prob.offsets, bands, periodic)
     cfg = rk.config_from_params(prm)
