@@ -175,7 +175,7 @@ def oracle_matvec_sample(workload, planes=32, threads=None):
 # ------------------------------------------------------------------ reference arm
 def run_reference(args):
     """--impl reference: the CPU oracle, one bounded sample per step (the
-    two cycles of oracle_matvec_sample on the first 16 z-planes,
+    two cycles of oracle_matvec_sample on the first 8 z-planes,
     scaled to the full grid), composed into ms per system with the
     workload's Krylov matvecs and cycles per system (below)."""
     rank = int(os.environ.get("RANK", "0"))
@@ -186,9 +186,9 @@ def run_reference(args):
     mvs, cys = [], []
     kk = nz = None
     walls = []
-    for i in range(args.warmup + args.steps):   # 16 planes: ~12 s per step on the box's host
+    for i in range(args.warmup + args.steps):   # 8 planes: ~6 s per step on the box's host (default 25 steps: ~3 min)
         t0 = time.perf_counter()
-        a, c, kk, nz = oracle_matvec_sample(args.workload, planes=16)
+        a, c, kk, nz = oracle_matvec_sample(args.workload, planes=8)
         if i >= args.warmup:
             mvs.append(a)
             cys.append(c)
