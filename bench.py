@@ -383,7 +383,9 @@ def run_rk(args):
                    "method": prm.method, "m": prm.m, "k": prm.k_max, "k_t": prm.k_t, "p1": prm.p1,
                    "tol": prm.tol, "precond": "jacobi(5+1)", "ortho": "cgs2 gram-corrected (R19)",
                    "parallelism": f"z-slab x{world}",
-                   "l2": "inputs larger than L2 (bases+bands ~ 17 GB at 256^3)"},
+                   "l2": "inputs larger than L2 (bases + bands per rank ~ %.1f GB)"
+                         % (8e-9 * Nl * ((prm.m + 1) + 2 * prm.k_max + (2 if prm.p1 == 2 else 0) + 8
+                                         + len(prob.offsets) + 1))},
         "iterations": {"krylov_matvecs_per_system": mv, "mean": float(np.mean(mv)),
                        "outcomes": sorted(set(outcomes)),
                        "ms_per_matvec": round(ms / max(1, sum(mv)), 4)},
