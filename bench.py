@@ -387,6 +387,7 @@ def run_rk(args):
                          % (8e-9 * Nl * ((prm.m + 1) + 2 * prm.k_max + (2 if prm.p1 == 2 else 0) + 8
                                          + len(prob.offsets) + 1))},
         "iterations": {"krylov_matvecs_per_system": mv, "mean": float(np.mean(mv)),
+                       "recycle_dim_after": [r["k_after"] for r in reps],
                        "outcomes": sorted(set(outcomes)),
                        "ms_per_matvec": round(ms / max(1, sum(mv)), 4)},
         "valid": all(o == "CONVERGED" for o in outcomes),
