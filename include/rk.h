@@ -351,7 +351,8 @@ rk_status rk_bicg_xr(rk_op* op, double* x, double* r, const double* s, const dou
  * algorithmic bytes. */
 rk_status rk_launch_count(rk_ctx* ctx, int64_t* count);
 /* Collective launches this context has issued so far on several ranks
- * ("batched so each iteration issues as few collectives as
+ * (the paper's parallel runs are MPI domain decompositions, P:117-118 and
+ * P:728 "16 CPU cores ... with MPI parallelism"; "batched so each iteration issues as few collectives as
  * the algorithm allows"; BASELINE north_star): *allreduces = all-reduce
  * launches (a group of all-reduces counts once, as NCCL launches it),
  * *halos = neighbour-exchange launches (one grouped send/recv set; the two
